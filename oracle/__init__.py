@@ -1,0 +1,213 @@
+"""FQNM CPU oracle — TEST INFRASTRUCTURE ONLY.
+
+Plain, slow, obviously correct CPU implementation of the FQNM update of
+arXiv 2604.06947.  Only `tests/`, `__graft_entry__.smoke()` and
+`bench.py`'s `cpu_baseline` / `--impl reference` legs may import this package.
+It shares no code with the CUDA path and the product path never calls it.
+
+* `rules.py`      — Eq. flux_table in exact Fraction arithmetic (the definition).
+* `fqnm_oracle.c` — the stepping loops (flux-difference and four-term forms),
+                    reconstruction and the componentwise-quantised Roe transfer,
+                    in plain C with 128-bit integer intermediates and pinned,
+                    uncontracted binary64 for the Roe path.
+* `reference.py`  — float64 classical split finite-volume schemes and exact
+                    Riemann solutions used to check the oracle against the
+                    paper's theorems.
+
+Parity status: every function is pinned by a
+`-m "not gpu"` test except the absolute physical accuracy of the Euler/Roe
+variant, which the paper gives no theorem for ("no complete
+convergence theory for compressible Euler"): that property is checked only
+heuristically against the exact Sod solution — "parity unpinned" for that
+accuracy claim; its arithmetic is pinned (consistency, mirror symmetry,
+upwind reduction, conservation, alternative Roe form).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from fractions import Fraction
+from typing import Optional
+
+import numpy as np
+
+from . import rules
+from .rules import (BURGERS_EO, BURGERS_LF, FLOOR, HALF_EVEN, LINEAR, RHA,
+                    map_coefficients)
+
+PERIODIC, TRANSMISSIVE = 0, 1
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "fqnm_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared", "-fPIC",
+          "-std=gnu11"]
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle/fqnm_oracle.c into oracle/liboracle.so (gcc)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".{os.getpid()}.tmp"
+        subprocess.check_call(["gcc", *CFLAGS, _SRC, "-o", tmp, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class _Map(ctypes.Structure):
+    _fields_ = [("c2", ctypes.c_int64), ("c1", ctypes.c_int64), ("den", ctypes.c_int64),
+                ("support", ctypes.c_int32), ("rounding", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = ctypes.CDLL(build())
+        P64 = ctypes.POINTER(ctypes.c_int64)
+        PD = ctypes.POINTER(ctypes.c_double)
+        PM = ctypes.POINTER(_Map)
+        L.or_phi.restype = ctypes.c_int64
+        L.or_phi.argtypes = [PM, ctypes.c_int64]
+        L.or_phi_array.argtypes = [PM, P64, P64, ctypes.c_int64]
+        L.or_step_scalar.argtypes = [PM, PM, ctypes.c_int, ctypes.c_int64, P64, P64]
+        L.or_step_scalar_fourterm.argtypes = [PM, PM, ctypes.c_int64, P64, P64]
+        L.or_run_scalar.argtypes = [PM, PM, ctypes.c_int, ctypes.c_int64, P64, ctypes.c_int64,
+                                    ctypes.c_int]
+        L.or_run_scalar_batch.argtypes = [PM, PM, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                          P64, ctypes.c_int64, ctypes.c_int]
+        L.or_observe.argtypes = [ctypes.c_double, P64, PD, ctypes.c_int64]
+        L.or_roe_transfer.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                      P64, P64, P64]
+        L.or_step_euler.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                    ctypes.c_int64, P64, P64]
+        L.or_run_euler.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                   ctypes.c_int64, P64, ctypes.c_int64, ctypes.c_int]
+        L.or_round_rational.restype = ctypes.c_int64
+        L.or_round_rational.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64,
+                                        ctypes.c_int]
+        L.or_max_threads.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _p64(a: np.ndarray):
+    assert a.dtype == np.int64 and a.flags.c_contiguous
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+
+
+class Rule:
+    """The pair of transfer maps (phi+, phi-) for a scalar flux kind, built
+    from exact rationals delta and dt/dx (Fractions, or decimal strings)."""
+
+    def __init__(self, kind: int, delta, dt_dx, param=Fraction(1), rounding: int = RHA):
+        self.kind = kind
+        self.delta = Fraction(delta)
+        self.dt_dx = Fraction(dt_dx)
+        self.param = Fraction(param)
+        self.rounding = rounding
+        cp = map_coefficients(kind, self.delta, self.dt_dx, +1, self.param)
+        cm = map_coefficients(kind, self.delta, self.dt_dx, -1, self.param)
+        self.coef_plus, self.coef_minus = cp, cm
+        self._mp = _Map(cp[0], cp[1], cp[2], cp[3], rounding)
+        self._mm = _Map(cm[0], cm[1], cm[2], cm[3], rounding)
+
+    # --- maps -------------------------------------------------------------
+    def phi_plus(self, q) -> np.ndarray:
+        q = np.ascontiguousarray(np.atleast_1d(q), dtype=np.int64)
+        out = np.empty_like(q)
+        lib().or_phi_array(ctypes.byref(self._mp), _p64(q), _p64(out), q.size)
+        return out
+
+    def phi_minus(self, q) -> np.ndarray:
+        q = np.ascontiguousarray(np.atleast_1d(q), dtype=np.int64)
+        out = np.empty_like(q)
+        lib().or_phi_array(ctypes.byref(self._mm), _p64(q), _p64(out), q.size)
+        return out
+
+    def interface_flux(self, qL, qR) -> np.ndarray:
+        """F(qL, qR) = phi+(qL) + phi-(qR)  (Eq. numerical_count_flux_definition)."""
+        return self.phi_plus(qL) + self.phi_minus(qR)
+
+    # --- stepping -----------------------------------------------------------
+    def step(self, q, boundary: int = PERIODIC) -> np.ndarray:
+        q = np.ascontiguousarray(q, dtype=np.int64)
+        out = np.empty_like(q)
+        lib().or_step_scalar(ctypes.byref(self._mp), ctypes.byref(self._mm), boundary,
+                             q.size, _p64(q), _p64(out))
+        return out
+
+    def step_fourterm(self, q) -> np.ndarray:
+        q = np.ascontiguousarray(q, dtype=np.int64)
+        out = np.empty_like(q)
+        lib().or_step_scalar_fourterm(ctypes.byref(self._mp), ctypes.byref(self._mm),
+                                      q.size, _p64(q), _p64(out))
+        return out
+
+    def run(self, q, nsteps: int, boundary: int = PERIODIC, nthreads: int = 0) -> np.ndarray:
+        """q^{n+nsteps} (double-buffered explicit steps)."""
+        q = np.array(q, dtype=np.int64, copy=True, order="C")
+        if q.ndim == 1:
+            lib().or_run_scalar(ctypes.byref(self._mp), ctypes.byref(self._mm), boundary,
+                                q.size, _p64(q), nsteps, nthreads)
+        else:
+            B, N = q.shape
+            lib().or_run_scalar_batch(ctypes.byref(self._mp), ctypes.byref(self._mm), boundary,
+                                      B, N, _p64(q), nsteps, nthreads)
+        return q
+
+
+def observe(q, delta: float) -> np.ndarray:
+    """u = fl(delta * q)  (Eq. reconstruction_operator)."""
+    q = np.ascontiguousarray(q, dtype=np.int64).ravel()
+    u = np.empty(q.size, dtype=np.float64)
+    lib().or_observe(float(delta), _p64(q), u.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                     q.size)
+    return u
+
+
+# --- Euler / Roe -------------------------------------------------------------
+
+def euler_constants(delta: float, dt_dx: float, gamma: float = 1.4):
+    """(s, g1) = (fl(dt/dx / delta), fl(gamma - 1))  (SURVEY §8(c)-C2 plan constants)."""
+    return dt_dx / delta, gamma - 1.0
+
+
+def roe_transfer(qL, qR, delta: float, dt_dx: float, gamma: float = 1.4) -> np.ndarray:
+    """T(qL, qR) = RHA(fl(F_Roe(delta qL, delta qR) * s)) for one interface."""
+    s, g1 = euler_constants(delta, dt_dx, gamma)
+    a = np.ascontiguousarray(qL, dtype=np.int64)
+    b = np.ascontiguousarray(qR, dtype=np.int64)
+    T = np.empty(3, dtype=np.int64)
+    lib().or_roe_transfer(delta, s, g1, _p64(a), _p64(b), _p64(T))
+    return T
+
+
+def euler_step(q, delta: float, dt_dx: float, gamma: float = 1.4) -> np.ndarray:
+    q = np.ascontiguousarray(q, dtype=np.int64)
+    s, g1 = euler_constants(delta, dt_dx, gamma)
+    out = np.empty_like(q)
+    lib().or_step_euler(delta, s, g1, q.shape[1], _p64(q), _p64(out))
+    return out
+
+
+def euler_run(q, nsteps: int, delta: float, dt_dx: float, gamma: float = 1.4,
+              nthreads: int = 0) -> np.ndarray:
+    q = np.array(q, dtype=np.int64, copy=True, order="C")
+    s, g1 = euler_constants(delta, dt_dx, gamma)
+    lib().or_run_euler(delta, s, g1, q.shape[1], _p64(q), nsteps, nthreads)
+    return q
+
+
+def max_threads() -> int:
+    return int(lib().or_max_threads())
+
+
+def round_rational(num: int, den: int, rounding: int = RHA) -> int:
+    """C-side rounding of num/den (128-bit numerator), for pinning tests."""
+    hi = num >> 64
+    lo = num & ((1 << 64) - 1)
+    return int(lib().or_round_rational(hi, lo, den, rounding))

@@ -1,0 +1,342 @@
+/*
+ * FQNM CPU oracle — TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously correct CPU implementation of the FQNM update of
+ * arXiv 2604.06947 (PAPER.md, cited as P:line).  Only tests/, the smoke check
+ * in __graft_entry__.py and bench.py's cpu_baseline / --impl reference legs
+ * may load this library.  It shares no source with the CUDA path
+ * (paper_2604_06947_b200/csrc, include/), and nothing here is called by the
+ * product path.
+ *
+ * Build: gcc -O2 -ffp-contract=off -fno-fast-math -fopenmp -shared -fPIC
+ *        (no FMA contraction: the Roe path pins every binary64 operation).
+ *
+ * Contents
+ *   1. rounding of an exact rational            (Eq. flux_table, readings A1/D1/D2)
+ *   2. the integer transfer maps phi+/-         (Eq. flux_table)
+ *   3. interface count flux + conservative update, flux-difference form
+ *                                               (Eqs. 7-8) and the
+ *      four-term form                           (Eq. update_rule)
+ *   4. reconstruction u = delta q               (Eq. reconstruction_operator)
+ *   5. quantised two-point Roe transfer for the Euler system
+ *                                               (Thm transfer-operator equivalence
+ *      Eq. applied componentwise; Roe flux structure P:567,
+ *      operation order pinned by SURVEY §8(c)-C2 / DESIGN.md reading R-ROE)
+ *
+ * A transfer map is a piecewise polynomial of degree <= 2 with exact rational
+ * coefficients, i.e. phi(q) = [q in support] * round( (c2 q^2 + c1 q) / D ),
+ * which is f(delta q) * (dt/dx) / delta written over a common denominator D
+ * (the coefficients are produced from the paper's formula by exact Fraction
+ * arithmetic in oracle/rules.py).  Every intermediate is a 128-bit integer.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+
+typedef __int128 i128;
+
+/* rounding rules (reading A1): RHA is the default; FLOOR is the literal
+ * mean-field closure n = floor(Np) of Eq. mean_field_closure;
+ * HALF_EVEN is the other common tie rule.  Same codes as include/fqnm.h. */
+enum { OR_RHA = 0, OR_FLOOR = 1, OR_HALF_EVEN = 2 };
+
+/* support of a map: all q, q > 0 only, q < 0 only */
+enum { OR_SUPP_ALL = 0, OR_SUPP_POS = 1, OR_SUPP_NEG = 2 };
+
+typedef struct {
+    int64_t c2, c1, den;   /* phi(q) = round((c2 q^2 + c1 q)/den), den > 0 */
+    int32_t support;
+    int32_t rounding;
+} or_map;
+
+/* ---- 1. rounding of the exact rational num/den (den > 0) --------------- */
+static i128 floor_div(i128 num, i128 den)
+{
+    i128 q = num / den;            /* C truncates toward zero */
+    if ((num % den != 0) && (num < 0)) q -= 1;
+    return q;
+}
+
+int64_t or_round_rational(int64_t num_hi, uint64_t num_lo, int64_t den, int rounding)
+{
+    i128 num = ((i128)num_hi << 64) | (i128)num_lo;
+    i128 d = den;
+    if (rounding == OR_FLOOR) return (int64_t)floor_div(num, d);
+    i128 a = num < 0 ? -num : num;
+    if (rounding == OR_RHA) {
+        /* RHA(x) = sign(x) floor(|x| + 1/2) */
+        i128 r = (2 * a + d) / (2 * d);
+        return (int64_t)(num < 0 ? -r : r);
+    }
+    /* half-to-even on |x|, then restore sign */
+    i128 fl = a / d, rem = a - fl * d;
+    i128 r;
+    if (2 * rem > d) r = fl + 1;
+    else if (2 * rem < d) r = fl;
+    else r = (fl % 2 == 0) ? fl : fl + 1;
+    return (int64_t)(num < 0 ? -r : r);
+}
+
+/* ---- 2. transfer map phi(q) (Eq. flux_table) ---------------------------- */
+int64_t or_phi(const or_map* m, int64_t q)
+{
+    if (m->support == OR_SUPP_POS && !(q > 0)) return 0;
+    if (m->support == OR_SUPP_NEG && !(q < 0)) return 0;
+    i128 num = (i128)m->c2 * (i128)q * (i128)q + (i128)m->c1 * (i128)q;
+    i128 d = m->den;
+    if (m->rounding == OR_FLOOR) return (int64_t)floor_div(num, d);
+    i128 a = num < 0 ? -num : num;
+    if (m->rounding == OR_RHA) {
+        i128 r = (2 * a + d) / (2 * d);
+        return (int64_t)(num < 0 ? -r : r);
+    }
+    i128 fl = a / d, rem = a - fl * d, r;
+    if (2 * rem > d) r = fl + 1;
+    else if (2 * rem < d) r = fl;
+    else r = (fl % 2 == 0) ? fl : fl + 1;
+    return (int64_t)(num < 0 ? -r : r);
+}
+
+void or_phi_array(const or_map* m, const int64_t* q, int64_t* out, int64_t n)
+{
+    for (int64_t i = 0; i < n; ++i) out[i] = or_phi(m, q[i]);
+}
+
+/* ---- 3. one explicit step ------------------------------------------------ */
+enum { OR_PERIODIC = 0, OR_TRANSMISSIVE = 1 };
+
+/* interface count flux F_{i+1/2} = phi+(q_i) + phi-(q_{i+1}) for
+ * i = -1 .. N-1.  Periodic: q_{-1} = q_{N-1}, q_N = q_0.  Transmissive
+ * (reading A12): ghost cells copy the edge cell, q_{-1} = q_0, q_N = q_{N-1}. */
+static int64_t flux_at(const or_map* pp, const or_map* pm, int boundary,
+                       int64_t N, const int64_t* q, int64_t i)
+{
+    int64_t iL = i, iR = i + 1;
+    if (boundary == OR_PERIODIC) {
+        if (iL < 0) iL += N;
+        if (iR >= N) iR -= N;
+    } else {
+        if (iL < 0) iL = 0;
+        if (iR >= N) iR = N - 1;
+    }
+    return or_phi(pp, q[iL]) + or_phi(pm, q[iR]);
+}
+
+/* q^{n+1}_i = q^n_i - (F_{i+1/2} - F_{i-1/2})  (Eq. update_rule_conservative_form,
+ * P:86-89).  All fluxes are evaluated on q^n (explicit update, reading D6). */
+void or_step_scalar(const or_map* pp, const or_map* pm, int boundary, int64_t N,
+                    const int64_t* q, int64_t* out)
+{
+    #pragma omp parallel for schedule(static) if (N >= 32768)
+    for (int64_t i = 0; i < N; ++i) {
+        int64_t Fr = flux_at(pp, pm, boundary, N, q, i);
+        int64_t Fl = flux_at(pp, pm, boundary, N, q, i - 1);
+        out[i] = q[i] - (Fr - Fl);
+    }
+}
+
+/* The four-term form of Eq. update_rule, periodic only:
+ * q_i - (phi+(q_i) + phi-(q_{i+1}) - phi+(q_{i-1}) - phi-(q_i)). */
+void or_step_scalar_fourterm(const or_map* pp, const or_map* pm, int64_t N,
+                             const int64_t* q, int64_t* out)
+{
+    for (int64_t i = 0; i < N; ++i) {
+        int64_t im = (i == 0) ? N - 1 : i - 1;
+        int64_t ip = (i == N - 1) ? 0 : i + 1;
+        out[i] = q[i] - (or_phi(pp, q[i]) + or_phi(pm, q[ip])
+                         - or_phi(pp, q[im]) - or_phi(pm, q[i]));
+    }
+}
+
+/* nsteps explicit steps, double buffered.  q is updated in place. */
+static void run_one(const or_map* pp, const or_map* pm, int boundary, int64_t N,
+                    int64_t* q, int64_t nsteps)
+{
+    int64_t* a = q;
+    int64_t* b = (int64_t*)malloc(sizeof(int64_t) * (size_t)N);
+    for (int64_t s = 0; s < nsteps; ++s) {
+        or_step_scalar(pp, pm, boundary, N, a, b);
+        int64_t* t = a; a = b; b = t;
+    }
+    if (a != q) { memcpy(q, a, sizeof(int64_t) * (size_t)N); b = a; }
+    free(b);
+}
+
+static void set_threads(int nthreads)
+{
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+}
+
+/* nthreads <= 0 leaves the OpenMP default. */
+void or_run_scalar(const or_map* pp, const or_map* pm, int boundary, int64_t N,
+                   int64_t* q, int64_t nsteps, int nthreads)
+{
+    set_threads(nthreads);
+    run_one(pp, pm, boundary, N, q, nsteps);
+}
+
+/* Batched independent problems [B][N] (ensemble mode), one problem per thread. */
+void or_run_scalar_batch(const or_map* pp, const or_map* pm, int boundary, int64_t B,
+                         int64_t N, int64_t* q, int64_t nsteps, int nthreads)
+{
+    set_threads(nthreads);
+    #pragma omp parallel for schedule(dynamic) if (B > 1)
+    for (int64_t b = 0; b < B; ++b)
+        run_one(pp, pm, boundary, N, q + b * N, nsteps);
+}
+
+/* ---- 4. reconstruction ---------------------------------------------------- */
+void or_observe(double delta, const int64_t* q, double* u, int64_t n)
+{
+    for (int64_t i = 0; i < n; ++i) u[i] = delta * (double)q[i];
+}
+
+/* ---- 5. Euler system: quantised Roe transfer ------------------------------ */
+/* Every statement below is one IEEE binary64 operation, in the order of
+ * SURVEY §8(c)-C2 (reading R-ROE).  Compiled with
+ * -ffp-contract=off, so no FMA contraction or reassociation happens. */
+
+typedef struct {
+    double rho, m, E, u, p, H, r, f0, f1, f2;
+} or_side;
+
+static void or_roe_side(double delta, double g1, const int64_t qc[3], or_side* s)
+{
+    double rho = delta * (double)qc[0];
+    double m = delta * (double)qc[1];
+    double E = delta * (double)qc[2];
+    double u = m / rho;
+    double mu = m * u;
+    double half_mu = 0.5 * mu;
+    double e_int = E - half_mu;
+    double p = g1 * e_int;
+    double Ep = E + p;
+    double H = Ep / rho;
+    double r = sqrt(rho);
+    s->rho = rho; s->m = m; s->E = E; s->u = u; s->p = p; s->H = H; s->r = r;
+    s->f0 = m;
+    s->f1 = mu + p;
+    s->f2 = u * Ep;
+}
+
+/* round-half-away-from-zero of a double (reading A1): exact because
+ * x - trunc(x) is exact in binary64. */
+static int64_t or_rha_double(double x)
+{
+    double t = trunc(x);
+    double d = x - t;
+    if (fabs(d) >= 0.5) t += (x > 0) ? 1.0 : -1.0;
+    return (int64_t)t;
+}
+
+static double or_harten(double l, double eps)
+{
+    double al = fabs(l);
+    if (al >= eps) return al;
+    double ll = l * l;
+    double ee = eps * eps;
+    double num = ll + ee;
+    double den = 2.0 * eps;
+    return num / den;
+}
+
+/* T^c(qL, qR) = RHA(fl(F^c_Roe(delta qL, delta qR) * s)), s = fl(dt/dx / delta). */
+void or_roe_transfer(double delta, double s, double g1, const int64_t qL[3],
+                     const int64_t qR[3], int64_t T[3])
+{
+    or_side L, R;
+    or_roe_side(delta, g1, qL, &L);
+    or_roe_side(delta, g1, qR, &R);
+    double d = L.r + R.r;
+    double ru_l = L.r * L.u, ru_r = R.r * R.u;
+    double ut = (ru_l + ru_r) / d;
+    double rh_l = L.r * L.H, rh_r = R.r * R.H;
+    double Ht = (rh_l + rh_r) / d;
+    double rhot = L.r * R.r;
+    double uu = ut * ut;
+    double half_uu = 0.5 * uu;
+    double a2 = g1 * (Ht - half_uu);
+    double at = sqrt(a2);
+    double drho = R.rho - L.rho;
+    double du = R.u - L.u;
+    double dp = R.p - L.p;
+    double ra = rhot * at;
+    double t = ra * du;
+    double two_a2 = 2.0 * a2;
+    double al1 = (dp - t) / two_a2;
+    double al3 = (dp + t) / two_a2;
+    double dpa = dp / a2;
+    double al2 = drho - dpa;
+    double l1 = ut - at;
+    double l3 = ut + at;
+    double eps = 0.05 * (fabs(ut) + at);
+    double c1 = or_harten(l1, eps) * al1;
+    double c2 = fabs(ut) * al2;
+    double c3 = or_harten(l3, eps) * al3;
+    double ua = ut * at;
+    double r1[3] = {1.0, l1, Ht - ua};
+    double r2[3] = {1.0, ut, half_uu};
+    double r3[3] = {1.0, l3, Ht + ua};
+    double fL[3] = {L.f0, L.f1, L.f2};
+    double fR[3] = {R.f0, R.f1, R.f2};
+    for (int c = 0; c < 3; ++c) {
+        double w1 = c1 * r1[c];
+        double w3 = c3 * r3[c];
+        double w2 = c2 * r2[c];
+        double D = (w1 + w3) + w2;
+        double avg = 0.5 * (fL[c] + fR[c]);
+        double F = avg - 0.5 * D;
+        double x = F * s;
+        T[c] = or_rha_double(x);
+    }
+}
+
+/* One explicit step of the componentwise-quantised Euler system, SoA [3][N],
+ * transmissive boundaries (ghost copies, reading A12). */
+void or_step_euler(double delta, double s, double g1, int64_t N,
+                   const int64_t* q, int64_t* out)
+{
+    #pragma omp parallel for schedule(static) if (N >= 32768)
+    for (int64_t i = 0; i < N; ++i) {
+        int64_t im = i > 0 ? i - 1 : 0;
+        int64_t ip = i < N - 1 ? i + 1 : N - 1;
+        int64_t qi[3] = {q[i], q[N + i], q[2 * N + i]};
+        int64_t qm[3] = {q[im], q[N + im], q[2 * N + im]};
+        int64_t qp[3] = {q[ip], q[N + ip], q[2 * N + ip]};
+        int64_t Tl[3], Tr[3];
+        or_roe_transfer(delta, s, g1, qm, qi, Tl);
+        or_roe_transfer(delta, s, g1, qi, qp, Tr);
+        for (int c = 0; c < 3; ++c)
+            out[c * N + i] = qi[c] - (Tr[c] - Tl[c]);
+    }
+}
+
+void or_run_euler(double delta, double s, double g1, int64_t N, int64_t* q,
+                  int64_t nsteps, int nthreads)
+{
+    set_threads(nthreads);
+    int64_t* a = q;
+    int64_t* b = (int64_t*)malloc(sizeof(int64_t) * 3 * (size_t)N);
+    for (int64_t k = 0; k < nsteps; ++k) {
+        or_step_euler(delta, s, g1, N, a, b);
+        int64_t* t = a; a = b; b = t;
+    }
+    if (a != q) { memcpy(q, a, sizeof(int64_t) * 3 * (size_t)N); b = a; }
+    free(b);
+}
+
+int or_max_threads(void)
+{
+#ifdef _OPENMP
+    extern int omp_get_max_threads(void);
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
