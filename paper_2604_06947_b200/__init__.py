@@ -1,0 +1,382 @@
+"""Thin Python binding of libfqnm (include/fqnm.h) — argument marshalling only.
+
+Every step of the FQNM hot path runs in the CUDA kernels of libfqnm.so
+(paper_2604_06947_b200/csrc).  This module converts torch tensors to device
+pointers, passes torch's current CUDA stream, and turns status codes into
+exceptions.  There is no CPU fallback: importing it without the built library
+raises, and every call needs CUDA tensors.
+
+Names follow the C ABI: fqnm_plan, fqnm_plan_ex, fqnm_step, fqnm_step_block,
+fqnm_observe, fqnm_step_host, fqnm_get_info, fqnm_transfer,
+fqnm_transfer_device, fqnm_roe_transfer_device, fqnm_debug_override,
+fqnm_launch_count, fqnm_destroy.  `Plan` is a small owning wrapper.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+__all__ = [
+    "FqnmError", "Plan", "fqnm_plan", "fqnm_plan_ex", "fqnm_step", "fqnm_step_block",
+    "fqnm_observe", "fqnm_step_host", "fqnm_get_info", "fqnm_transfer", "fqnm_transfer_device",
+    "fqnm_roe_transfer_device", "fqnm_debug_override", "fqnm_launch_count", "fqnm_destroy",
+    "fqnm_plan_validate", "fqnm_profile_enable", "fqnm_profile_read",
+    "LINEAR", "BURGERS_EO", "BURGERS_LF", "EULER_ROE", "PERIODIC", "TRANSMISSIVE", "HALO",
+    "I32", "I64", "ROUND_HALF_AWAY", "ROUND_FLOOR", "ROUND_HALF_EVEN", "lib_path",
+]
+
+LINEAR, BURGERS_EO, BURGERS_LF, EULER_ROE = 0, 1, 2, 3
+PERIODIC, TRANSMISSIVE, HALO = 0, 1, 2
+I32, I64 = 0, 1
+ROUND_HALF_AWAY, ROUND_FLOOR, ROUND_HALF_EVEN = 0, 1, 2
+STATUS = {0: "FQNM_OK", 1: "FQNM_ERR_ARG", 2: "FQNM_ERR_CFL", 3: "FQNM_ERR_RANGE",
+          4: "FQNM_ERR_CUDA", 5: "FQNM_ERR_UNSUPPORTED", 6: "FQNM_ERR_NOMEM"}
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def lib_path() -> str:
+    return os.path.join(_HERE, "libfqnm.so")
+
+
+class FqnmError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class PlanDesc(ctypes.Structure):
+    _fields_ = [
+        ("n_local", ctypes.c_int64), ("n_global", ctypes.c_int64), ("offset", ctypes.c_int64),
+        ("batch", ctypes.c_int64), ("nvar", ctypes.c_int32), ("dtype", ctypes.c_int32),
+        ("delta", ctypes.c_double), ("dt_dx", ctypes.c_double), ("flux_kind", ctypes.c_int32),
+        ("rounding", ctypes.c_int32), ("flux_param", ctypes.c_double),
+        ("kappa_num", ctypes.c_int64), ("kappa_den", ctypes.c_int64),
+        ("boundary", ctypes.c_int32), ("k", ctypes.c_int32),
+        ("q_lo", ctypes.c_int64), ("q_hi", ctypes.c_int64), ("halo", ctypes.c_int64),
+        ("check_range", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+        ("stream", ctypes.c_void_p),
+    ]
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [
+        ("kappa_num", ctypes.c_int64), ("kappa_den", ctypes.c_int64),
+        ("q_lo", ctypes.c_int64), ("q_hi", ctypes.c_int64),
+        ("rule", ctypes.c_int32), ("k", ctypes.c_int32), ("cells_per_thread", ctypes.c_int32),
+        ("kernel", ctypes.c_int32), ("scratch_bytes", ctypes.c_int64),
+        ("s_euler", ctypes.c_double), ("g1_euler", ctypes.c_double),
+    ]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = lib_path()
+    if not os.path.exists(path):
+        raise ImportError(f"libfqnm.so not built at {path}: run `python __graft_entry__.py build` "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(path)
+    vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+    L.fqnm_plan.argtypes = [ctypes.POINTER(vp), i64, dbl, dbl, ctypes.c_int, ctypes.c_int]
+    L.fqnm_plan_ex.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(PlanDesc)]
+    L.fqnm_desc_init.argtypes = [ctypes.POINTER(PlanDesc)]
+    L.fqnm_desc_init.restype = None
+    L.fqnm_destroy.argtypes = [vp]
+    L.fqnm_destroy.restype = None
+    L.fqnm_set_stream.argtypes = [vp, vp]
+    L.fqnm_step.argtypes = [vp, vp, i64]
+    L.fqnm_step_block.argtypes = [vp, vp, vp, i32]
+    L.fqnm_observe.argtypes = [vp, vp, vp]
+    L.fqnm_step_host.argtypes = [vp, vp, i64]
+    L.fqnm_get_info.argtypes = [vp, ctypes.POINTER(PlanInfo)]
+    L.fqnm_transfer.argtypes = [vp, i64, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.fqnm_transfer_device.argtypes = [vp, vp, vp, vp, i64]
+    L.fqnm_roe_transfer_device.argtypes = [vp, vp, vp, vp, i64]
+    L.fqnm_debug_override.argtypes = [vp, i32, i32, i32]
+    L.fqnm_plan_validate.argtypes = [ctypes.POINTER(PlanDesc), ctypes.POINTER(PlanInfo)]
+    L.fqnm_profile_enable.argtypes = [vp, ctypes.c_int]
+    L.fqnm_profile_read.argtypes = [vp, ctypes.POINTER(dbl), ctypes.POINTER(i64)]
+    L.fqnm_launch_count.argtypes = [vp]
+    L.fqnm_launch_count.restype = i64
+    L.fqnm_last_error.restype = ctypes.c_char_p
+    L.fqnm_status_str.restype = ctypes.c_char_p
+    L.fqnm_status_str.argtypes = [ctypes.c_int]
+    L.fqnm_abi_version.restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise FqnmError(rc, _load().fqnm_last_error().decode())
+
+
+def _stream_ptr(tensor=None):
+    import torch
+    dev = tensor.device if tensor is not None else None
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _dev_ptr(t, dtype=None, name="tensor"):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Plan:
+    """Owning handle of an fqnm_plan_t."""
+
+    def __init__(self, handle: ctypes.c_void_p, desc: PlanDesc):
+        self._h = handle
+        self.desc = desc
+
+    @property
+    def handle(self):
+        if not self._h:
+            raise ValueError("plan destroyed")
+        return self._h
+
+    @property
+    def dtype(self):
+        import torch
+        return torch.int64 if self.desc.dtype == I64 else torch.int32
+
+    def state_shape(self):
+        n = self.desc.n_local + (2 * self.desc.halo if self.desc.boundary == HALO else 0)
+        shape = (self.desc.batch, self.desc.nvar, n)
+        return tuple(s for s in shape[:-1] if s != 1) + (n,)
+
+    def step(self, q, nsteps: int):
+        return fqnm_step(self, q, nsteps)
+
+    def step_block(self, src, dst, ksteps: int):
+        return fqnm_step_block(self, src, dst, ksteps)
+
+    def observe(self, q, u=None):
+        return fqnm_observe(self, q, u)
+
+    def info(self) -> dict:
+        return fqnm_get_info(self)
+
+    def launches(self) -> int:
+        return fqnm_launch_count(self)
+
+    def close(self):
+        if self._h:
+            _load().fqnm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def fqnm_plan(N: int, delta: float, dt_dx: float, flux_kind: int = LINEAR,
+              boundary: int = PERIODIC) -> Plan:
+    """North-star plan: one problem of N cells (include/fqnm.h fqnm_plan)."""
+    L = _load()
+    h = ctypes.c_void_p()
+    _check(L.fqnm_plan(ctypes.byref(h), int(N), float(delta), float(dt_dx), int(flux_kind),
+                       int(boundary)))
+    d = PlanDesc()
+    L.fqnm_desc_init(ctypes.byref(d))
+    d.n_local = d.n_global = N
+    d.delta, d.dt_dx, d.flux_kind, d.boundary = delta, dt_dx, flux_kind, boundary
+    if flux_kind == EULER_ROE:
+        d.nvar, d.dtype = 3, I64
+    d.check_range = 1 if flux_kind != EULER_ROE else 0
+    return Plan(h, d)
+
+
+def make_desc(n_local: int, delta: float, dt_dx: float, flux_kind: int = LINEAR,
+              boundary: int = PERIODIC, *, batch: int = 1, nvar: Optional[int] = None,
+              dtype: Optional[int] = None, flux_param: float = 0.0, kappa=None,
+              rounding: int = ROUND_HALF_AWAY, q_range=None, k: int = 0, halo: int = 0,
+              n_global: int = 0, offset: int = 0, check_range: bool = False,
+              stream=None) -> PlanDesc:
+    L = _load()
+    d = PlanDesc()
+    L.fqnm_desc_init(ctypes.byref(d))
+    euler = flux_kind == EULER_ROE
+    d.n_local = n_local
+    d.n_global = n_global or n_local
+    d.offset = offset
+    d.batch = batch
+    d.nvar = nvar if nvar is not None else (3 if euler else 1)
+    d.dtype = dtype if dtype is not None else (I64 if euler else I32)
+    d.delta, d.dt_dx = float(delta), float(dt_dx)
+    d.flux_kind, d.rounding = int(flux_kind), int(rounding)
+    d.flux_param = float(flux_param)
+    if kappa is not None:
+        d.kappa_num, d.kappa_den = int(kappa[0]), int(kappa[1])
+    d.boundary = int(boundary)
+    d.k = int(k)
+    if q_range is not None:
+        d.q_lo, d.q_hi = int(q_range[0]), int(q_range[1])
+    d.halo = int(halo)
+    d.check_range = 1 if check_range else 0
+    d.stream = stream
+    return d
+
+
+def fqnm_plan_ex(n_local: int, delta: float, dt_dx: float, flux_kind: int = LINEAR,
+                 boundary: int = PERIODIC, **kw) -> Plan:
+    """General plan (include/fqnm.h fqnm_plan_ex); kappa = (num, den) overrides."""
+    d = make_desc(n_local, delta, dt_dx, flux_kind, boundary, **kw)
+    h = ctypes.c_void_p()
+    _check(_load().fqnm_plan_ex(ctypes.byref(h), ctypes.byref(d)))
+    return Plan(h, d)
+
+
+def fqnm_plan_validate(n_local: int, delta: float, dt_dx: float, flux_kind: int = LINEAR,
+                       boundary: int = PERIODIC, **kw) -> dict:
+    """Host-only rule building + kernel selection (no GPU needed)."""
+    d = make_desc(n_local, delta, dt_dx, flux_kind, boundary, **kw)
+    info = PlanInfo()
+    _check(_load().fqnm_plan_validate(ctypes.byref(d), ctypes.byref(info)))
+    return info.as_dict()
+
+
+def fqnm_profile_enable(plan: Plan, enable: bool = True):
+    _check(_load().fqnm_profile_enable(plan.handle, 1 if enable else 0))
+
+
+def fqnm_profile_read(plan: Plan):
+    """(summed device ms, number of bracketed stepping-kernel launches) since last read."""
+    ms, n = ctypes.c_double(), ctypes.c_int64()
+    _check(_load().fqnm_profile_read(plan.handle, ctypes.byref(ms), ctypes.byref(n)))
+    return ms.value, n.value
+
+
+def fqnm_step(plan: Plan, q, nsteps: int):
+    """q <- q^{n+nsteps} in place (device tensor of the plan's dtype/layout)."""
+    L = _load()
+    ptr = _dev_ptr(q, plan.dtype, "q")
+    if q.numel() != _numel(plan):
+        raise ValueError(f"q has {q.numel()} elements, plan expects {_numel(plan)}")
+    _check(L.fqnm_set_stream(plan.handle, _stream_ptr(q)))
+    _check(L.fqnm_step(plan.handle, ptr, int(nsteps)))
+    return q
+
+
+def fqnm_step_block(plan: Plan, src, dst, ksteps: int):
+    L = _load()
+    s = _dev_ptr(src, plan.dtype, "src")
+    t = _dev_ptr(dst, plan.dtype, "dst")
+    _check(L.fqnm_set_stream(plan.handle, _stream_ptr(src)))
+    _check(L.fqnm_step_block(plan.handle, s, t, int(ksteps)))
+    return dst
+
+
+def fqnm_observe(plan: Plan, q, u=None):
+    """u = fl(delta q) as a float64 device tensor of q's shape."""
+    import torch
+    L = _load()
+    ptr = _dev_ptr(q, plan.dtype, "q")
+    if u is None:
+        u = torch.empty(q.shape, dtype=torch.float64, device=q.device)
+    uptr = _dev_ptr(u, torch.float64, "u")
+    _check(L.fqnm_set_stream(plan.handle, _stream_ptr(q)))
+    _check(L.fqnm_observe(plan.handle, ptr, uptr))
+    return u
+
+
+def fqnm_step_host(plan: Plan, q_host, nsteps: int):
+    """End-to-end: host buffer (pinned torch CPU tensor or numpy array) stepped in place."""
+    L = _load()
+    try:
+        import torch
+        if isinstance(q_host, torch.Tensor):
+            if q_host.is_cuda or not q_host.is_contiguous():
+                raise ValueError("q_host must be a contiguous CPU tensor")
+            ptr = ctypes.c_void_p(q_host.data_ptr())
+            _check(L.fqnm_set_stream(plan.handle, _stream_ptr()))
+            _check(L.fqnm_step_host(plan.handle, ptr, int(nsteps)))
+            return q_host
+    except ImportError:  # pragma: no cover
+        pass
+    import numpy as np
+    a = q_host
+    if not (isinstance(a, np.ndarray) and a.flags.c_contiguous):
+        raise TypeError("q_host must be a contiguous numpy array or CPU tensor")
+    _check(L.fqnm_step_host(plan.handle, ctypes.c_void_p(a.ctypes.data), int(nsteps)))
+    return a
+
+
+def _numel(plan: Plan) -> int:
+    d = plan.desc
+    n = d.n_local + (2 * d.halo if d.boundary == HALO else 0)
+    return d.batch * d.nvar * n
+
+
+def fqnm_get_info(plan: Plan) -> dict:
+    info = PlanInfo()
+    _check(_load().fqnm_get_info(plan.handle, ctypes.byref(info)))
+    return info.as_dict()
+
+
+def fqnm_transfer(plan: Plan, q: int):
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    _check(_load().fqnm_transfer(plan.handle, int(q), ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
+
+
+def fqnm_transfer_device(plan: Plan, q):
+    import torch
+    p = torch.empty_like(q)
+    m = torch.empty_like(q)
+    L = _load()
+    qp = _dev_ptr(q, torch.int32, "q")
+    _check(L.fqnm_set_stream(plan.handle, _stream_ptr(q)))
+    _check(L.fqnm_transfer_device(plan.handle, qp, _dev_ptr(p), _dev_ptr(m), q.numel()))
+    return p, m
+
+
+def fqnm_roe_transfer_device(plan: Plan, qL, qR):
+    """qL, qR: [3][n] int64 device tensors; returns T [3][n]."""
+    import torch
+    T = torch.empty_like(qL)
+    L = _load()
+    a = _dev_ptr(qL, torch.int64, "qL")
+    b = _dev_ptr(qR, torch.int64, "qR")
+    _check(L.fqnm_set_stream(plan.handle, _stream_ptr(qL)))
+    _check(L.fqnm_roe_transfer_device(plan.handle, a, b, _dev_ptr(T), qL.shape[-1]))
+    return T
+
+
+def fqnm_debug_override(plan: Plan, kernel: int = 0, k: int = 0, cells_per_thread: int = 0):
+    _check(_load().fqnm_debug_override(plan.handle, int(kernel), int(k), int(cells_per_thread)))
+
+
+def fqnm_launch_count(plan: Plan) -> int:
+    return int(_load().fqnm_launch_count(plan.handle))
+
+
+def fqnm_destroy(plan: Plan):
+    plan.close()
+
+
+def abi_version() -> int:
+    return int(_load().fqnm_abi_version())

@@ -1,0 +1,846 @@
+// Host side of libfqnm: the C ABI of include/fqnm.h, the transfer-rule builder
+// (exact kappa, D8 validation, range/headroom, fast-path selection) and the
+// planner that picks a kernel family, V and k and drives the launches.
+//
+// Paper references: Eq. flux_table P:62-68 (maps), Eq. count flux
+// P:91-94, update P:86-89, reconstruction P:101-105, CFL/monotonicity Lemma
+// P:189-238 (the integer form D8 is checked here), Roe system P:564-575.
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/fqnm.h"
+#include "fqnm_internal.h"
+
+using namespace fqnm;
+
+typedef __int128 i128;
+
+// ---------------------------------------------------------------------------
+// errors
+static thread_local std::string g_err;
+
+static int fail(int status, const char* fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return status;
+}
+
+#define CUDA_TRY(expr)                                                                       \
+    do {                                                                                     \
+        cudaError_t e_ = (expr);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(FQNM_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(e_));      \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// exact host maps: phi(q) = [q in supp] round((c2 q^2 + c1 q)/den)
+struct HostMap {
+    int64_t c2 = 0, c1 = 0, den = 1;
+    int32_t supp = SUPP_NONE;
+};
+
+static i128 floor_div128(i128 num, i128 den)
+{
+    i128 q = num / den;
+    if ((num % den != 0) && (num < 0)) q -= 1;
+    return q;
+}
+
+static i128 round128(i128 num, i128 den, int rounding)
+{
+    if (rounding == FQNM_ROUND_FLOOR) return floor_div128(num, den);
+    i128 a = num < 0 ? -num : num;
+    i128 r;
+    if (rounding == FQNM_ROUND_HALF_AWAY) {
+        r = (2 * a + den) / (2 * den);
+    } else {
+        i128 fl = a / den, rem = a - fl * den;
+        if (2 * rem > den) r = fl + 1;
+        else if (2 * rem < den) r = fl;
+        else r = (fl % 2 == 0) ? fl : fl + 1;
+    }
+    return num < 0 ? -r : r;
+}
+
+static int64_t host_phi(const HostMap& m, int64_t q, int rounding)
+{
+    if (m.supp == SUPP_NONE) return 0;
+    if (m.supp == SUPP_POS && q <= 0) return 0;
+    if (m.supp == SUPP_NEG && q >= 0) return 0;
+    i128 num = (i128)m.c2 * q * q + (i128)m.c1 * q;
+    return (int64_t)round128(num, m.den, rounding);
+}
+
+static bool map_is_zero(const HostMap& m) { return m.supp == SUPP_NONE || (m.c2 == 0 && m.c1 == 0); }
+
+static int64_t gcd64(int64_t a, int64_t b)
+{
+    a = a < 0 ? -a : a;
+    b = b < 0 ? -b : b;
+    while (b) { int64_t t = a % b; a = b; b = t; }
+    return a;
+}
+
+// exact rational nearest a positive or negative double: simplest convergent of
+// the exact continued fraction of x with den <= 2^31 and |x - p/q| <= 2^-48 |x|
+static bool rationalize(double x, int64_t* pnum, int64_t* pden)
+{
+    if (!std::isfinite(x) || x == 0.0) return false;
+    const bool neg = x < 0;
+    double ax = neg ? -x : x;
+    int e2;
+    double fr = std::frexp(ax, &e2);                  // ax = fr * 2^e2, fr in [0.5, 1)
+    int64_t M = (int64_t)std::ldexp(fr, 53);          // exact 53-bit mantissa
+    int sh = 53 - e2;                                  // ax = M / 2^sh
+    i128 num, den;
+    if (sh <= 0) {
+        if (-sh > 60) return false;
+        num = (i128)M << (-sh);
+        den = 1;
+    } else {
+        if (sh > 120) return false;
+        num = M;
+        den = (i128)1 << sh;
+    }
+    // continued fraction of num/den with convergents h/k
+    i128 h0 = 0, h1 = 1, k0 = 1, k1 = 0;
+    i128 a = num, b = den;
+    for (int it = 0; it < 200 && b != 0; ++it) {
+        i128 t = a / b;
+        i128 h2 = t * h1 + h0, k2 = t * k1 + k0;
+        if (k2 > ((i128)1 << 31)) break;
+        h0 = h1; h1 = h2; k0 = k1; k1 = k2;
+        i128 r = a - t * b;
+        a = b; b = r;
+        // |num/den - h1/k1| <= 2^-48 num/den  <=>  |num k1 - h1 den| 2^48 <= num k1
+        i128 diff = num * k1 - h1 * den;
+        if (diff < 0) diff = -diff;
+        if (diff <= ((num * k1) >> 48)) {
+            if (h1 > INT64_MAX || k1 > INT64_MAX) return false;
+            *pnum = neg ? -(int64_t)h1 : (int64_t)h1;
+            *pden = (int64_t)k1;
+            return true;
+        }
+    }
+    return false;
+}
+
+// ---------------------------------------------------------------------------
+struct fqnm_plan {
+    fqnm_plan_desc d{};
+    // rule
+    HostMap hp, hm;
+    DevRule dr{};
+    int rule = 0;
+    int64_t kap_num = 0, kap_den = 0;
+    int64_t lo = 0, hi = 0;
+    bool dep_left = false, dep_right = false;
+    // kernel choice
+    int family = 0;
+    int V = 0;
+    int k = 0;
+    // Euler constants
+    double s_e = 0, g1_e = 0;
+    // memory
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    long long* d_minmax = nullptr;
+    long long* h_minmax = nullptr;
+    void* e2e_dev = nullptr;
+    size_t e2e_bytes = 0;
+    cudaStream_t st = nullptr;
+    int64_t launches = 0;
+    // profiling (fqnm_profile_enable)
+    bool prof = false;
+    std::vector<cudaEvent_t> ev;      // pairs (start, stop)
+    size_t ev_used = 0;
+};
+
+static void fill_info(const fqnm_plan_t* p, fqnm_plan_info* info);
+static int plan_build(fqnm_plan_t** out, const fqnm_plan_desc* din, bool allocate);
+
+static size_t elem_size(const fqnm_plan_desc& d) { return d.dtype == FQNM_I64 ? 8 : 4; }
+
+static size_t state_elems(const fqnm_plan_desc& d)
+{
+    int64_t n = d.n_local + (d.boundary == FQNM_HALO ? 2 * d.halo : 0);
+    return (size_t)d.batch * (size_t)d.nvar * (size_t)n;
+}
+
+extern "C" void fqnm_desc_init(fqnm_plan_desc* d)
+{
+    if (!d) return;
+    std::memset(d, 0, sizeof *d);
+    d->batch = 1;
+    d->nvar = 1;
+    d->dtype = FQNM_I32;
+    d->rounding = FQNM_ROUND_HALF_AWAY;
+    d->boundary = FQNM_PERIODIC;
+    d->check_range = 0;
+}
+
+// D8 on [lo, hi]: phi+ nondecreasing, phi- nonincreasing, dphi+ - dphi- <= 1.
+// Returns the first failing q (lo - 1 if none).
+static int64_t d8_first_violation(const fqnm_plan_t* p, int64_t lo, int64_t hi)
+{
+    int rd = p->d.rounding;
+    int64_t pp = host_phi(p->hp, lo, rd), pm = host_phi(p->hm, lo, rd);
+    for (int64_t q = lo; q < hi; ++q) {
+        int64_t np_ = host_phi(p->hp, q + 1, rd), nm = host_phi(p->hm, q + 1, rd);
+        int64_t dp = np_ - pp, dm = nm - pm;
+        if (dp < 0 || dm > 0 || dp - dm > 1) return q;
+        pp = np_; pm = nm;
+    }
+    return lo - 1;
+}
+
+// headroom of the int64 generic device path: |2 (c2 q^2 + c1 q)| + den < 2^62
+static bool generic_headroom(const HostMap& m, int64_t a)
+{
+    if (map_is_zero(m)) return true;
+    i128 A = a;
+    i128 num = (i128)(m.c2 < 0 ? -m.c2 : m.c2) * A * A + (i128)(m.c1 < 0 ? -m.c1 : m.c1) * A;
+    return 2 * num + m.den < ((i128)1 << 62);
+}
+
+static int build_rule(fqnm_plan_t* p)
+{
+    fqnm_plan_desc& d = p->d;
+    const int kind = d.flux_kind;
+    int64_t P = d.kappa_num, Q = d.kappa_den;
+    if (kind == FQNM_LINEAR || kind == FQNM_BURGERS_EO) {
+        if (P == 0 && Q == 0) {
+            double a = d.flux_param == 0.0 ? 1.0 : d.flux_param;
+            double kd = (kind == FQNM_LINEAR) ? a * d.dt_dx : d.delta * d.dt_dx / 2.0;
+            if (!rationalize(kd, &P, &Q))
+                return fail(FQNM_ERR_ARG, "kappa = %.17g has no exact rational with "
+                            "denominator <= 2^31 (pass kappa_num/kappa_den)", kd);
+        } else {
+            if (Q <= 0 || P == 0) return fail(FQNM_ERR_ARG, "kappa_den must be > 0, kappa_num != 0");
+            int64_t g = gcd64(P, Q);
+            P /= g; Q /= g;
+        }
+        p->kap_num = P;
+        p->kap_den = Q;
+        if (kind == FQNM_LINEAR) {
+            HostMap m;
+            m.c2 = 0; m.c1 = P; m.den = Q; m.supp = SUPP_ALL;
+            if (P > 0) { p->hp = m; p->hm = HostMap(); }
+            else { p->hm = m; p->hp = HostMap(); }
+        } else {
+            if (P < 0) return fail(FQNM_ERR_ARG, "Burgers EO needs delta*dt_dx > 0");
+            HostMap a, b;
+            a.c2 = P; a.c1 = 0; a.den = Q; a.supp = SUPP_POS;
+            b.c2 = P; b.c1 = 0; b.den = Q; b.supp = SUPP_NEG;
+            p->hp = a; p->hm = b;
+        }
+    } else if (kind == FQNM_BURGERS_LF) {
+        // f+- = (u^2/2 +- alpha u)/2  ->  phi+- = round(k2 q^2 +- k1 q), k2 = delta lam/4, k1 = alpha lam/2
+        if (!(d.flux_param > 0)) return fail(FQNM_ERR_ARG, "Burgers LF needs flux_param alpha > 0");
+        int64_t P2, Q2, P1, Q1;
+        if (!rationalize(d.delta * d.dt_dx / 4.0, &P2, &Q2) ||
+            !rationalize(d.flux_param * d.dt_dx / 2.0, &P1, &Q1))
+            return fail(FQNM_ERR_ARG, "LF coefficients have no exact rational form");
+        int64_t g = gcd64(Q1, Q2);
+        i128 den = (i128)Q1 / g * Q2;
+        i128 c2 = (i128)P2 * (den / Q2), c1 = (i128)P1 * (den / Q1);
+        if (den > INT64_MAX / 4 || c2 > INT64_MAX / 4 || c1 > INT64_MAX / 4)
+            return fail(FQNM_ERR_UNSUPPORTED, "LF coefficients too large for int64");
+        HostMap a, b;
+        a.c2 = (int64_t)c2; a.c1 = (int64_t)c1; a.den = (int64_t)den; a.supp = SUPP_ALL;
+        b.c2 = (int64_t)c2; b.c1 = -(int64_t)c1; b.den = (int64_t)den; b.supp = SUPP_ALL;
+        p->hp = a; p->hm = b;
+        p->kap_num = P2; p->kap_den = Q2;
+    } else {
+        return fail(FQNM_ERR_ARG, "unknown flux kind %d", kind);
+    }
+    p->dep_left = !map_is_zero(p->hp);
+    p->dep_right = !map_is_zero(p->hm);
+
+    // ---- range, D8, fast-path selection ----
+    const bool lin_half = (kind == FQNM_LINEAR && P == 1 && Q == 2 &&
+                           d.rounding == FQNM_ROUND_HALF_AWAY);
+    bool eo_fast_ok = false;
+    int64_t a_fast = 0;
+    if (kind == FQNM_BURGERS_EO && d.rounding == FQNM_ROUND_HALF_AWAY && P >= 1 &&
+        P < (1 << 29) && Q < (1 << 29)) {
+        // largest a with a < 2^23 and P a^2 / Q <= 2^22 - 8
+        double am = std::sqrt((std::ldexp(1.0, 22) - 8.0) * (double)Q / (double)P);
+        a_fast = (int64_t)am;
+        while (a_fast > 0 && (i128)P * a_fast * a_fast > ((i128)((1 << 22) - 8)) * Q) --a_fast;
+        if (a_fast > (1 << 23) - 1) a_fast = (1 << 23) - 1;
+        eo_fast_ok = a_fast > 0;
+    }
+    int64_t lo = d.q_lo, hi = d.q_hi;
+    const int64_t i32lo = INT32_MIN + 1, i32hi = INT32_MAX;
+    if (kind == FQNM_LINEAR) {
+        // D8 holds on all of Z iff |kappa| <= 1 (increments of round(kappa q) are 0/1)
+        if ((P < 0 ? -P : P) > Q)
+            return fail(FQNM_ERR_CFL, "linear |kappa| = %lld/%lld > 1 violates D8", (long long)P,
+                        (long long)Q);
+        if (lo == 0 && hi == 0) { lo = i32lo; hi = i32hi; }
+        if (lo < i32lo || hi > i32hi) return fail(FQNM_ERR_RANGE, "range exceeds int32 state");
+        if (!lin_half && !(generic_headroom(p->hp, lo < 0 ? -lo : lo) &&
+                           generic_headroom(p->hp, hi) && generic_headroom(p->hm, lo < 0 ? -lo : lo)
+                           && generic_headroom(p->hm, hi)))
+            return fail(FQNM_ERR_RANGE, "int64 headroom exceeded");
+        p->rule = lin_half ? R_LIN_HALF : R_GENERIC;
+    } else {
+        if (lo == 0 && hi == 0) {
+            // derive the largest symmetric range on which D8 holds (and the device path is exact)
+            int64_t cap = eo_fast_ok ? a_fast : (1 << 24);
+            int64_t A = 0;
+            int rd = d.rounding;
+            int64_t pp0 = host_phi(p->hp, 0, rd), pm0 = host_phi(p->hm, 0, rd);
+            int64_t ppp = pp0, pmp = pm0, ppn = pp0, pmn = pm0;
+            while (A < cap) {
+                int64_t a1 = A + 1;
+                int64_t pp1 = host_phi(p->hp, a1, rd), pm1 = host_phi(p->hm, a1, rd);
+                int64_t ppm = host_phi(p->hp, -a1, rd), pmm = host_phi(p->hm, -a1, rd);
+                int64_t dp = pp1 - ppp, dm = pm1 - pmp;            // step A -> A+1
+                int64_t dpn = ppn - ppm, dmn = pmn - pmm;          // step -A-1 -> -A
+                if (dp < 0 || dm > 0 || dp - dm > 1 || dpn < 0 || dmn > 0 || dpn - dmn > 1) break;
+                if (!generic_headroom(p->hp, a1) || !generic_headroom(p->hm, a1)) break;
+                ppp = pp1; pmp = pm1; ppn = ppm; pmn = pmm;
+                A = a1;
+            }
+            if (A < 1) return fail(FQNM_ERR_CFL, "D8 fails already at |q| <= 1");
+            lo = -A; hi = A;
+        } else {
+            if (lo >= hi) return fail(FQNM_ERR_ARG, "q_lo must be < q_hi");
+            if (lo < i32lo || hi > i32hi) return fail(FQNM_ERR_RANGE, "range exceeds int32 state");
+            if (hi - lo > ((int64_t)1 << 27))
+                return fail(FQNM_ERR_UNSUPPORTED, "declared range too wide to validate D8");
+            int64_t bad = d8_first_violation(p, lo, hi);
+            if (bad >= lo)
+                return fail(FQNM_ERR_CFL, "D8 (integer monotonicity) fails at q = %lld", (long long)bad);
+            int64_t amax = (lo < 0 ? -lo : lo) > hi ? (lo < 0 ? -lo : lo) : hi;
+            if (!generic_headroom(p->hp, amax) || !generic_headroom(p->hm, amax))
+                return fail(FQNM_ERR_RANGE, "int64 headroom exceeded on the declared range");
+        }
+        int64_t amax = (lo < 0 ? -lo : lo) > hi ? (lo < 0 ? -lo : lo) : hi;
+        p->rule = (eo_fast_ok && amax <= a_fast) ? R_EO_FAST : R_GENERIC;
+    }
+    p->lo = lo;
+    p->hi = hi;
+
+    DevRule& r = p->dr;
+    std::memset(&r, 0, sizeof r);
+    r.c2p = p->hp.c2; r.c1p = p->hp.c1; r.denp = p->hp.den; r.suppp = p->hp.supp;
+    r.c2m = p->hm.c2; r.c1m = p->hm.c1; r.denm = p->hm.den; r.suppm = p->hm.supp;
+    if (map_is_zero(p->hp)) r.suppp = SUPP_NONE;
+    if (map_is_zero(p->hm)) r.suppm = SUPP_NONE;
+    r.rounding = d.rounding;
+    if (p->rule == R_EO_FAST) {
+        r.eo_twoP = (int32_t)(2 * P);
+        r.eo_Q = (int32_t)Q;
+        r.eo_twoQ = (int32_t)(2 * Q);
+        r.eo_cf = (float)((double)P / (double)Q);
+    }
+    return FQNM_OK;
+}
+
+// ---------------------------------------------------------------------------
+static int choose_kernel(fqnm_plan_t* p)
+{
+    const fqnm_plan_desc& d = p->d;
+    if (d.nvar == 3) {
+        p->family = 5;
+        p->V = 2;
+        p->k = 1;
+        return FQNM_OK;
+    }
+    const int64_t n = d.n_local;
+    if (d.boundary == FQNM_HALO) {
+        p->family = 2;
+    } else if (n % 32 == 0 && warp_ensemble_has_V((int)(n / 32)) && n <= 1024) {
+        p->family = 3;
+        p->V = (int)(n / 32);
+    } else if (n <= 16384) {
+        p->family = 4;
+    } else {
+        p->family = 2;
+    }
+    if (p->family == 2) {
+        const bool two = p->dep_left && p->dep_right;
+        if (p->rule == R_LIN_HALF) { p->V = 16; p->k = 32; }
+        else if (p->rule == R_EO_FAST) { p->V = 16; p->k = 16; }
+        else { p->V = 8; p->k = two ? 8 : 16; }
+        if (d.k > 0) p->k = d.k;
+        if (d.boundary == FQNM_HALO && p->k > d.halo) p->k = (int)d.halo;
+    }
+    return FQNM_OK;
+}
+
+static int round4(int x) { return (x + 3) & ~3; }
+
+// largest steps per block the geometry of V admits
+static int max_block_steps(const fqnm_plan_t* p, int V)
+{
+    const int W = 32 * V;
+    const int sides = (p->dep_left ? 1 : 0) + (p->dep_right ? 1 : 0);
+    if (sides == 0) return 1 << 30;
+    // keep at least W/4 useful cells per window
+    int k = (W - W / 4) / sides;
+    return k & ~3;
+}
+
+static int plan_build(fqnm_plan_t** out, const fqnm_plan_desc* din, bool allocate)
+{
+    if (!out || !din) return fail(FQNM_ERR_ARG, "null argument");
+    *out = nullptr;
+    const fqnm_plan_desc& d = *din;
+    if (d.n_local < 2) return fail(FQNM_ERR_ARG, "n_local must be >= 2");
+    if (d.batch < 1) return fail(FQNM_ERR_ARG, "batch must be >= 1");
+    if (!(std::isfinite(d.delta) && d.delta > 0)) return fail(FQNM_ERR_ARG, "delta must be finite and > 0");
+    if (!(std::isfinite(d.dt_dx) && d.dt_dx > 0)) return fail(FQNM_ERR_ARG, "dt_dx must be finite and > 0");
+    if (d.boundary < 0 || d.boundary > 2) return fail(FQNM_ERR_ARG, "unknown boundary %d", d.boundary);
+    if (d.rounding < 0 || d.rounding > 2) return fail(FQNM_ERR_ARG, "unknown rounding %d", d.rounding);
+    fqnm_plan_t* p = new (std::nothrow) fqnm_plan_t();
+    if (!p) return fail(FQNM_ERR_NOMEM, "out of host memory");
+    p->d = d;
+    p->d.n_global = d.n_global ? d.n_global : d.n_local;
+    p->st = (cudaStream_t)d.stream;
+    int rc;
+    if (d.flux_kind == FQNM_EULER_ROE) {
+        if (d.nvar != 3 || d.dtype != FQNM_I64) {
+            delete p;
+            return fail(FQNM_ERR_ARG, "Euler plans need nvar = 3 and dtype = FQNM_I64");
+        }
+        if (d.boundary == FQNM_HALO) { delete p; return fail(FQNM_ERR_UNSUPPORTED, "Euler split domains"); }
+        double gamma = d.flux_param == 0.0 ? 1.4 : d.flux_param;
+        if (!(gamma > 1.0)) { delete p; return fail(FQNM_ERR_ARG, "gamma must be > 1"); }
+        p->s_e = d.dt_dx / d.delta;          // s = fl(dt/dx / delta)
+        p->g1_e = gamma - 1.0;                // g1 = fl(gamma - 1)
+        p->lo = INT64_MIN;
+        p->hi = INT64_MAX;
+    } else {
+        if (d.nvar != 1 || d.dtype != FQNM_I32) {
+            delete p;
+            return fail(FQNM_ERR_UNSUPPORTED, "scalar plans need nvar = 1 and dtype = FQNM_I32");
+        }
+        if ((rc = build_rule(p)) != FQNM_OK) { delete p; return rc; }
+    }
+    if (d.boundary == FQNM_HALO) {
+        if (d.halo < 4 || d.halo % 4 != 0) { delete p; return fail(FQNM_ERR_ARG, "halo must be a positive multiple of 4"); }
+        if (d.batch != 1) { delete p; return fail(FQNM_ERR_UNSUPPORTED, "split domains with batch > 1"); }
+    }
+    choose_kernel(p);
+    if (p->family == 2) {
+        int kmax = max_block_steps(p, p->V);
+        if (p->k > kmax) p->k = kmax;
+        if (p->k < 1) p->k = 1;
+    }
+    if (!allocate) {
+        *out = p;
+        return FQNM_OK;
+    }
+    // device buffers
+    cudaError_t e;
+    if (p->family == 2 || p->family == 1 || p->family == 5) {
+        if (d.boundary != FQNM_HALO) {
+            p->scratch_bytes = state_elems(p->d) * elem_size(p->d);
+            e = cudaMalloc(&p->scratch, p->scratch_bytes);
+            if (e != cudaSuccess) {
+                delete p;
+                return fail(FQNM_ERR_NOMEM, "cudaMalloc(%zu) scratch: %s", (size_t)state_elems(d) * elem_size(d),
+                            cudaGetErrorString(e));
+            }
+        }
+    }
+    if ((e = cudaMalloc(&p->d_minmax, 2 * sizeof(long long))) != cudaSuccess ||
+        (e = cudaMallocHost(&p->h_minmax, 4 * sizeof(long long))) != cudaSuccess) {
+        fqnm_destroy(p);
+        return fail(FQNM_ERR_CUDA, "allocating range-check buffers: %s", cudaGetErrorString(e));
+    }
+    *out = p;
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_plan_ex(fqnm_plan_t** out, const fqnm_plan_desc* din)
+{
+    return plan_build(out, din, true);
+}
+
+extern "C" int fqnm_plan(fqnm_plan_t** out, int64_t N, double delta, double dt_dx, int flux_kind,
+                         int boundary)
+{
+    fqnm_plan_desc d;
+    fqnm_desc_init(&d);
+    d.n_local = N;
+    d.n_global = N;
+    d.delta = delta;
+    d.dt_dx = dt_dx;
+    d.flux_kind = flux_kind;
+    d.boundary = boundary;
+    d.check_range = 1;
+    if (boundary != FQNM_PERIODIC && boundary != FQNM_TRANSMISSIVE)
+        return fail(FQNM_ERR_ARG, "fqnm_plan: boundary must be PERIODIC or TRANSMISSIVE");
+    if (flux_kind == FQNM_EULER_ROE) {
+        d.nvar = 3;
+        d.dtype = FQNM_I64;
+        d.flux_param = 1.4;
+        d.check_range = 0;
+    }
+    return fqnm_plan_ex(out, &d);
+}
+
+extern "C" void fqnm_destroy(fqnm_plan_t* p)
+{
+    if (!p) return;
+    cudaStreamSynchronize(p->st);
+    if (p->scratch) cudaFree(p->scratch);
+    if (p->d_minmax) cudaFree(p->d_minmax);
+    if (p->h_minmax) cudaFreeHost(p->h_minmax);
+    if (p->e2e_dev) cudaFree(p->e2e_dev);
+    for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
+    delete p;
+}
+
+extern "C" int fqnm_set_stream(fqnm_plan_t* p, void* stream)
+{
+    if (!p) return fail(FQNM_ERR_ARG, "null plan");
+    p->st = (cudaStream_t)stream;
+    return FQNM_OK;
+}
+
+static bool aligned16(const void* x) { return ((uintptr_t)x & 15u) == 0; }
+
+// ---------------------------------------------------------------------------
+static int check_range(fqnm_plan_t* p, const void* q)
+{
+    const fqnm_plan_desc& d = p->d;
+    long long init[2] = {LLONG_MAX, LLONG_MIN};
+    p->h_minmax[0] = init[0];
+    p->h_minmax[1] = init[1];
+    CUDA_TRY(cudaMemcpyAsync(p->d_minmax, p->h_minmax, 2 * sizeof(long long), cudaMemcpyHostToDevice, p->st));
+    CUDA_TRY(launch_minmax(q, d.dtype, (int64_t)state_elems(d), p->d_minmax, p->st));
+    p->launches++;
+    CUDA_TRY(cudaMemcpyAsync(p->h_minmax + 2, p->d_minmax, 2 * sizeof(long long), cudaMemcpyDeviceToHost, p->st));
+    CUDA_TRY(cudaStreamSynchronize(p->st));
+    long long mn = p->h_minmax[2], mx = p->h_minmax[3];
+    if (mn < p->lo || mx > p->hi)
+        return fail(FQNM_ERR_RANGE, "state range [%lld, %lld] outside the plan's admissible "
+                    "range [%lld, %lld]", mn, mx, (long long)p->lo, (long long)p->hi);
+    return FQNM_OK;
+}
+
+static int prof_begin(fqnm_plan_t* p)
+{
+    if (!p->prof) return FQNM_OK;
+    if (p->ev_used + 2 > p->ev.size()) {
+        for (int i = 0; i < 64; ++i) {
+            cudaEvent_t e;
+            CUDA_TRY(cudaEventCreate(&e));
+            p->ev.push_back(e);
+        }
+    }
+    CUDA_TRY(cudaEventRecord(p->ev[p->ev_used], p->st));
+    return FQNM_OK;
+}
+
+static int prof_end(fqnm_plan_t* p)
+{
+    if (!p->prof) return FQNM_OK;
+    CUDA_TRY(cudaEventRecord(p->ev[p->ev_used + 1], p->st));
+    p->ev_used += 2;
+    return FQNM_OK;
+}
+
+#define PROF_LAUNCH(expr)                                  \
+    do {                                                   \
+        int rc_ = prof_begin(p);                           \
+        if (rc_ != FQNM_OK) return rc_;                    \
+        CUDA_TRY(expr);                                    \
+        if ((rc_ = prof_end(p)) != FQNM_OK) return rc_;    \
+        p->launches++;                                     \
+    } while (0)
+
+static int bmode_of(const fqnm_plan_desc& d)
+{
+    return d.boundary == FQNM_TRANSMISSIVE ? BM_TRANSMISSIVE
+           : (d.boundary == FQNM_HALO ? BM_HALO : BM_PERIODIC);
+}
+
+static int launch_block(fqnm_plan_t* p, const int32_t* src, int32_t* dst, int ksteps)
+{
+    const fqnm_plan_desc& d = p->d;
+    BlockedArgs a;
+    a.src = src;
+    a.dst = dst;
+    a.n = d.n_local;
+    a.batch = d.batch;
+    a.halo = d.boundary == FQNM_HALO ? d.halo : 0;
+    a.ksteps = ksteps;
+    a.KL = p->dep_left ? round4(ksteps) : 0;
+    a.KR = p->dep_right ? round4(ksteps) : 0;
+    a.bmode = bmode_of(d);
+    const int64_t S = 32 * p->V - a.KL - a.KR;
+    if (S < 4) return fail(FQNM_ERR_ARG, "k = %d too large for V = %d", ksteps, p->V);
+    a.nwin = (d.n_local + S - 1) / S;
+    PROF_LAUNCH(launch_blocked(p->rule, p->V, a, p->dr, p->st, 148 * 32));
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
+{
+    if (!p || !q) return fail(FQNM_ERR_ARG, "null argument");
+    if (nsteps < 0) return fail(FQNM_ERR_ARG, "nsteps must be >= 0");
+    if (!aligned16(q)) return fail(FQNM_ERR_ARG, "q must be 16-byte aligned");
+    const fqnm_plan_desc& d = p->d;
+    if (d.boundary == FQNM_HALO)
+        return fail(FQNM_ERR_UNSUPPORTED, "split-domain plans step through fqnm_step_block");
+    if (nsteps == 0) return FQNM_OK;
+    int rc;
+    if (d.check_range && d.nvar == 1 && (rc = check_range(p, q)) != FQNM_OK) return rc;
+    const int bm = bmode_of(d);
+    const int64_t n = d.n_local;
+    const size_t bytes = state_elems(d) * elem_size(d);
+
+    if (p->family == 3) {
+        PROF_LAUNCH(launch_warp_ensemble(p->rule, p->V, (int32_t*)q, d.batch, nsteps, bm, p->dr, p->st));
+        return FQNM_OK;
+    }
+    if (p->family == 4) {
+        PROF_LAUNCH(launch_cta_ensemble(p->rule, (int32_t*)q, n, d.batch, nsteps, bm, p->dr, p->st));
+        return FQNM_OK;
+    }
+    // ping-pong families
+    void* bufs[2] = {q, p->scratch};
+    int cur = 0;
+    if (p->family == 1 || p->family == 5) {
+        for (int64_t s = 0; s < nsteps; ++s) {
+            if (p->family == 1) {
+                PROF_LAUNCH(launch_naive(p->rule, (const int32_t*)bufs[cur], (int32_t*)bufs[cur ^ 1], n,
+                                         d.batch, bm, p->dr, p->st));
+            } else {
+                EulerArgs a;
+                a.src = (const int64_t*)bufs[cur];
+                a.dst = (int64_t*)bufs[cur ^ 1];
+                a.n = n;
+                a.batch = d.batch;
+                a.nwin = (n + (32 * p->V - 2) - 1) / (32 * p->V - 2);
+                a.delta = d.delta;
+                a.s = p->s_e;
+                a.g1 = p->g1_e;
+                a.bmode = bm;
+                PROF_LAUNCH(launch_euler(p->V, a, p->st));
+            }
+            cur ^= 1;
+        }
+    } else {
+        // temporally blocked: an even number of blocks so the result lands in q
+        int64_t nb = (nsteps + p->k - 1) / p->k;
+        if (nb % 2 == 1 && nsteps >= nb + 1) nb += 1;
+        const int64_t base = nsteps / nb, rem = nsteps % nb;
+        for (int64_t b = 0; b < nb; ++b) {
+            int ks = (int)(base + (b < rem ? 1 : 0));
+            if ((rc = launch_block(p, (const int32_t*)bufs[cur], (int32_t*)bufs[cur ^ 1], ks)) != FQNM_OK)
+                return rc;
+            cur ^= 1;
+        }
+    }
+    if (cur != 0) CUDA_TRY(cudaMemcpyAsync(q, bufs[cur], bytes, cudaMemcpyDeviceToDevice, p->st));
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_step_block(fqnm_plan_t* p, const void* src, void* dst, int32_t ksteps)
+{
+    if (!p || !src || !dst) return fail(FQNM_ERR_ARG, "null argument");
+    if (p->d.boundary != FQNM_HALO) return fail(FQNM_ERR_ARG, "fqnm_step_block needs a FQNM_HALO plan");
+    if (src == dst) return fail(FQNM_ERR_ARG, "src and dst must differ");
+    if (ksteps < 1 || ksteps > p->d.halo) return fail(FQNM_ERR_ARG, "need 1 <= ksteps <= halo");
+    if (ksteps > max_block_steps(p, p->V)) return fail(FQNM_ERR_ARG, "ksteps too large for this plan");
+    if (!aligned16(src) || !aligned16(dst)) return fail(FQNM_ERR_ARG, "buffers must be 16-byte aligned");
+    return launch_block(p, (const int32_t*)src, (int32_t*)dst, ksteps);
+}
+
+extern "C" int fqnm_observe(const fqnm_plan_t* p, const void* q, double* u)
+{
+    if (!p || !q || !u) return fail(FQNM_ERR_ARG, "null argument");
+    CUDA_TRY(launch_observe(q, p->d.dtype, p->d.delta, u, (int64_t)state_elems(p->d), p->st));
+    const_cast<fqnm_plan_t*>(p)->launches++;
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_step_host(fqnm_plan_t* p, void* q_host, int64_t nsteps)
+{
+    if (!p || !q_host) return fail(FQNM_ERR_ARG, "null argument");
+    const size_t bytes = state_elems(p->d) * elem_size(p->d);
+    if (!p->e2e_dev) {
+        cudaError_t e = cudaMalloc(&p->e2e_dev, bytes);
+        if (e != cudaSuccess) return fail(FQNM_ERR_NOMEM, "cudaMalloc e2e: %s", cudaGetErrorString(e));
+        p->e2e_bytes = bytes;
+    }
+    CUDA_TRY(cudaMemcpyAsync(p->e2e_dev, q_host, bytes, cudaMemcpyHostToDevice, p->st));
+    int rc = fqnm_step(p, p->e2e_dev, nsteps);
+    if (rc != FQNM_OK) return rc;
+    CUDA_TRY(cudaMemcpyAsync(q_host, p->e2e_dev, bytes, cudaMemcpyDeviceToHost, p->st));
+    CUDA_TRY(cudaStreamSynchronize(p->st));
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_get_info(const fqnm_plan_t* p, fqnm_plan_info* info)
+{
+    if (!p || !info) return fail(FQNM_ERR_ARG, "null argument");
+    fill_info(p, info);
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_transfer(const fqnm_plan_t* p, int64_t q, int64_t* phi_plus, int64_t* phi_minus)
+{
+    if (!p || !phi_plus || !phi_minus) return fail(FQNM_ERR_ARG, "null argument");
+    if (p->d.nvar != 1) return fail(FQNM_ERR_ARG, "scalar plans only");
+    *phi_plus = host_phi(p->hp, q, p->d.rounding);
+    *phi_minus = host_phi(p->hm, q, p->d.rounding);
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_transfer_device(const fqnm_plan_t* p, const int32_t* q, int32_t* pp, int32_t* pm,
+                                    int64_t n)
+{
+    if (!p || !q || !pp || !pm) return fail(FQNM_ERR_ARG, "null argument");
+    if (p->d.nvar != 1) return fail(FQNM_ERR_ARG, "scalar plans only");
+    if (n <= 0) return FQNM_OK;
+    CUDA_TRY(launch_transfer(p->rule, q, pp, pm, n, p->dr, p->st));
+    const_cast<fqnm_plan_t*>(p)->launches++;
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_roe_transfer_device(const fqnm_plan_t* p, const int64_t* qL, const int64_t* qR,
+                                        int64_t* T, int64_t n)
+{
+    if (!p || !qL || !qR || !T) return fail(FQNM_ERR_ARG, "null argument");
+    if (p->d.nvar != 3) return fail(FQNM_ERR_ARG, "Euler plans only");
+    if (n <= 0) return FQNM_OK;
+    CUDA_TRY(launch_roe_transfer(qL, qR, T, n, p->d.delta, p->s_e, p->g1_e, p->st));
+    const_cast<fqnm_plan_t*>(p)->launches++;
+    return FQNM_OK;
+}
+
+static void fill_info(const fqnm_plan_t* p, fqnm_plan_info* info)
+{
+    std::memset(info, 0, sizeof *info);
+    info->kappa_num = p->kap_num;
+    info->kappa_den = p->kap_den;
+    info->q_lo = p->lo;
+    info->q_hi = p->hi;
+    info->rule = p->rule;
+    info->k = p->k;
+    info->cells_per_thread = p->V;
+    info->kernel = p->family;
+    info->scratch_bytes = (int64_t)p->scratch_bytes;
+    info->s_euler = p->s_e;
+    info->g1_euler = p->g1_e;
+}
+
+extern "C" int fqnm_plan_validate(const fqnm_plan_desc* d, fqnm_plan_info* info)
+{
+    if (!d || !info) return fail(FQNM_ERR_ARG, "null argument");
+    fqnm_plan_t* p = nullptr;
+    int rc = plan_build(&p, d, /*allocate=*/false);
+    if (rc != FQNM_OK) return rc;
+    fill_info(p, info);
+    delete p;
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_profile_enable(fqnm_plan_t* p, int enable)
+{
+    if (!p) return fail(FQNM_ERR_ARG, "null plan");
+    p->prof = enable != 0;
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_profile_read(fqnm_plan_t* p, double* total_ms, int64_t* launches)
+{
+    if (!p || !total_ms || !launches) return fail(FQNM_ERR_ARG, "null argument");
+    CUDA_TRY(cudaStreamSynchronize(p->st));
+    double tot = 0;
+    for (size_t i = 0; i + 1 < p->ev_used; i += 2) {
+        float ms = 0;
+        CUDA_TRY(cudaEventElapsedTime(&ms, p->ev[i], p->ev[i + 1]));
+        tot += ms;
+    }
+    *total_ms = tot;
+    *launches = (int64_t)(p->ev_used / 2);
+    p->ev_used = 0;
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_debug_override(fqnm_plan_t* p, int32_t kernel, int32_t k, int32_t V)
+{
+    if (!p) return fail(FQNM_ERR_ARG, "null plan");
+    const fqnm_plan_desc& d = p->d;
+    if (d.nvar == 3) {
+        if (V && !euler_has_V(V)) return fail(FQNM_ERR_UNSUPPORTED, "Euler V must be 1, 2 or 4");
+        if (V) p->V = V;
+        return FQNM_OK;
+    }
+    if (kernel) {
+        if (d.boundary == FQNM_HALO && kernel != 2) return fail(FQNM_ERR_UNSUPPORTED, "split domains use K2");
+        if (kernel == 3) {
+            if (d.n_local % 32 != 0 || !warp_ensemble_has_V((int)(d.n_local / 32)))
+                return fail(FQNM_ERR_UNSUPPORTED, "warp ensemble needs n = 32 V, V in {1..32}");
+            p->V = (int)(d.n_local / 32);
+        } else if (kernel == 4) {
+            if (d.n_local > 16384) return fail(FQNM_ERR_UNSUPPORTED, "CTA ensemble needs n <= 16384");
+        } else if (kernel == 1 || kernel == 2) {
+            if (!p->scratch && d.boundary != FQNM_HALO) {
+                p->scratch_bytes = state_elems(d) * elem_size(d);
+                CUDA_TRY(cudaMalloc(&p->scratch, p->scratch_bytes));
+            }
+            if (kernel == 2 && !p->V) { p->V = 16; p->k = 16; }
+            if (kernel == 2 && (p->V < 8 || !blocked_has_V(p->V))) p->V = 16;
+            if (kernel == 2 && p->k < 1) p->k = 8;
+        } else {
+            return fail(FQNM_ERR_ARG, "unknown kernel family %d", kernel);
+        }
+        p->family = kernel;
+    }
+    if (V) {
+        if (p->family != 2 || !blocked_has_V(V)) return fail(FQNM_ERR_UNSUPPORTED, "V override needs K2 and V in {8,16,32}");
+        p->V = V;
+    }
+    if (k) {
+        if (p->family != 2) return fail(FQNM_ERR_UNSUPPORTED, "k override needs K2");
+        if (k > max_block_steps(p, p->V)) return fail(FQNM_ERR_ARG, "k too large for V");
+        if (d.boundary == FQNM_HALO && k > d.halo) return fail(FQNM_ERR_ARG, "k > halo");
+        p->k = k;
+    }
+    if (p->family == 2 && p->k > max_block_steps(p, p->V)) p->k = max_block_steps(p, p->V);
+    return FQNM_OK;
+}
+
+extern "C" int64_t fqnm_launch_count(const fqnm_plan_t* p) { return p ? p->launches : 0; }
+
+extern "C" const char* fqnm_last_error(void) { return g_err.c_str(); }
+
+extern "C" const char* fqnm_status_str(int s)
+{
+    switch (s) {
+        case FQNM_OK: return "FQNM_OK";
+        case FQNM_ERR_ARG: return "FQNM_ERR_ARG";
+        case FQNM_ERR_CFL: return "FQNM_ERR_CFL";
+        case FQNM_ERR_RANGE: return "FQNM_ERR_RANGE";
+        case FQNM_ERR_CUDA: return "FQNM_ERR_CUDA";
+        case FQNM_ERR_UNSUPPORTED: return "FQNM_ERR_UNSUPPORTED";
+        case FQNM_ERR_NOMEM: return "FQNM_ERR_NOMEM";
+        default: return "FQNM_ERR_UNKNOWN";
+    }
+}
+
+extern "C" int fqnm_abi_version(void) { return FQNM_ABI_VERSION; }

@@ -1,0 +1,82 @@
+// Internal declarations shared by the host planner (fqnm_api.cu) and the kernels.
+// Not part of the C ABI (include/fqnm.h is).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fqnm {
+
+// ---- device rule: how the kernels evaluate (phi+, phi-) ------------------
+// Selected by the planner (rule builder) from the exact rational maps.
+enum RuleKind : int32_t {
+    R_LIN_HALF = 1,   // LINEAR a > 0, kappa = 1/2 exactly, RHA: phi+ = q - trunc(q/2), phi- = 0
+    R_EO_FAST = 2,    // BURGERS_EO, RHA: g(|q|) = floor((2P q^2 + Q)/(2Q)) by float estimate +
+                      // exact 32-bit remainder correction (valid range proven at plan time)
+    R_GENERIC = 3     // any piecewise-quadratic map, exact int64 arithmetic, any rounding
+};
+
+enum Support : int32_t { SUPP_ALL = 0, SUPP_POS = 1, SUPP_NEG = 2, SUPP_NONE = 3 };
+
+struct DevRule {
+    // generic maps: phi(q) = [q in supp] round((c2 q^2 + c1 q)/den)
+    int64_t c2p, c1p, denp;
+    int64_t c2m, c1m, denm;
+    int32_t suppp, suppm;
+    int32_t rounding;
+    // EO fast path constants
+    int32_t eo_twoP;      // 2P
+    int32_t eo_Q;         // Q
+    int32_t eo_twoQ;      // 2Q
+    float eo_cf;          // fl32(P/Q)
+    int32_t pad;
+};
+
+enum Bmode : int32_t { BM_PERIODIC = 0, BM_TRANSMISSIVE = 1, BM_HALO = 2 };
+
+struct BlockedArgs {
+    const int32_t* src;
+    int32_t* dst;
+    int64_t n;          // cells per problem (owned cells for HALO)
+    int64_t batch;
+    int64_t nwin;       // windows per problem
+    int64_t halo;       // HALO: halo cells each side in src/dst
+    int32_t ksteps;
+    int32_t KL, KR;     // garbage-shrink per side (multiples of 4)
+    int32_t bmode;
+};
+
+struct EulerArgs {
+    const int64_t* src;
+    int64_t* dst;
+    int64_t n;
+    int64_t batch;
+    int64_t nwin;
+    double delta, s, g1;
+    int32_t bmode;
+};
+
+// kernel launchers (kernels_scalar.cu / kernels_euler.cu); return cudaError_t
+cudaError_t launch_blocked(int rule, int V, const BlockedArgs& a, const DevRule& r,
+                           cudaStream_t st, int grid_cap);
+cudaError_t launch_naive(int rule, const int32_t* src, int32_t* dst, int64_t n, int64_t batch,
+                         int bmode, const DevRule& r, cudaStream_t st);
+cudaError_t launch_warp_ensemble(int rule, int V, int32_t* q, int64_t batch, int64_t nsteps,
+                                 int bmode, const DevRule& r, cudaStream_t st);
+cudaError_t launch_cta_ensemble(int rule, int32_t* q, int64_t n, int64_t batch, int64_t nsteps,
+                                int bmode, const DevRule& r, cudaStream_t st);
+cudaError_t launch_transfer(int rule, const int32_t* q, int32_t* pp, int32_t* pm, int64_t n,
+                            const DevRule& r, cudaStream_t st);
+cudaError_t launch_minmax(const void* q, int dtype, int64_t n, long long* out2, cudaStream_t st);
+cudaError_t launch_observe(const void* q, int dtype, double delta, double* u, int64_t n,
+                           cudaStream_t st);
+cudaError_t launch_euler(int V, const EulerArgs& a, cudaStream_t st);
+cudaError_t launch_roe_transfer(const int64_t* qL, const int64_t* qR, int64_t* T, int64_t n,
+                                double delta, double s, double g1, cudaStream_t st);
+
+int blocked_max_V();
+bool blocked_has_V(int V);
+bool warp_ensemble_has_V(int V);
+bool euler_has_V(int V);
+
+}  // namespace fqnm

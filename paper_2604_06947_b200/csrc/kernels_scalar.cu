@@ -1,0 +1,458 @@
+// Scalar FQNM kernels for sm_100a (B200).
+//
+// The update:
+//   F_{i+1/2} = phi+(q_i) + phi-(q_{i+1}),   q_i <- q_i - (F_{i+1/2} - F_{i-1/2})
+// is a 3-point integer stencil with no dense contraction, so no tensor cores:
+// the design goal is integer-issue throughput with HBM traffic amortised over k
+// steps per round trip.
+//
+//   K1 k_naive            one thread per cell, one step per launch (reference/fallback)
+//   K2 k_blocked          temporally blocked: each warp holds a window of 32*V
+//                         contiguous cells in registers (V per lane), advances it
+//                         k steps with warp shuffles for the neighbour maps, and
+//                         stores the cells whose light cone stayed inside the
+//                         window (overlapped trapezoids, no smem, no barriers)
+//   K3 k_warp_ensemble    one periodic/transmissive problem of 32*V cells per
+//                         warp, all nsteps in registers (ensembles, cfg1)
+//   K4 k_cta_ensemble     one problem per CTA in shared memory (general small N)
+//   +  transfer / min-max / observe helpers
+#include <climits>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "fqnm_internal.h"
+#include "maps.cuh"
+
+namespace fqnm {
+
+static constexpr unsigned FULL = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// one explicit step of V register-resident cells of a lane.
+//   pl, mr: phi+ of the cell left of q[0], phi- of the cell right of q[V-1]
+//   WALL:   transmissive ghost rule (interface -1/2 and N-1/2 use the edge cell)
+template <int RULE, int V, bool WALL>
+__device__ __forceinline__ void step_cells(int32_t (&q)[V], const int32_t (&p)[V],
+                                           const int32_t (&m)[V], int32_t pl, int32_t mr,
+                                           int64_t g0, int64_t n)
+{
+    int32_t Tl = pl + m[0];                 // F_{j-1/2} for j = 0
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        int32_t Tr = (j + 1 < V) ? p[j] + m[j + 1] : p[V - 1] + mr;   // F_{j+1/2}
+        if (WALL) {
+            if (g0 + j == 0) Tl = p[j] + m[j];          // F_{-1/2} with ghost q_{-1} = q_0
+            if (g0 + j == n - 1) Tr = p[j] + m[j];      // F_{N-1/2} with ghost q_N = q_{N-1}
+        }
+        q[j] = q[j] + Tl - Tr;
+        Tl = Tr;
+    }
+}
+
+template <int RULE, int V>
+__device__ __forceinline__ void eval_maps(const int32_t (&q)[V], int32_t (&p)[V],
+                                          int32_t (&m)[V], const DevRule& r)
+{
+#pragma unroll
+    for (int j = 0; j < V; ++j) phi_pm<RULE>(q[j], p[j], m[j], r);
+}
+
+// ---------------------------------------------------------------------------
+// K2: temporally blocked stencil
+template <int RULE, int V, bool WALL>
+__device__ __forceinline__ void run_window_steps(int32_t (&q)[V], int ksteps, const DevRule& r,
+                                                 int64_t g0, int64_t n)
+{
+    for (int s = 0; s < ksteps; ++s) {
+        int32_t p[V], m[V];
+        eval_maps<RULE, V>(q, p, m, r);
+        // lane 0 / lane 31 receive their own values: the garbage this creates
+        // moves inward one cell per step and is cut off by KL/KR at the store.
+        int32_t pl = __shfl_up_sync(FULL, p[V - 1], 1);
+        int32_t mr = __shfl_down_sync(FULL, m[0], 1);
+        step_cells<RULE, V, WALL>(q, p, m, pl, mr, g0, n);
+    }
+}
+
+__device__ __forceinline__ int64_t wrap_index(int64_t i, int64_t n, int bmode, int64_t halo)
+{
+    if (bmode == BM_PERIODIC) {
+        i %= n;
+        return i < 0 ? i + n : i;
+    }
+    if (bmode == BM_TRANSMISSIVE) return i < 0 ? 0 : (i >= n ? n - 1 : i);
+    // HALO: buffer index = i + halo, valid range [-halo, n + halo)
+    if (i < -halo) i = -halo;
+    if (i >= n + halo) i = n + halo - 1;
+    return i + halo;
+}
+
+template <int RULE, int V>
+__global__ void __launch_bounds__(256) k_blocked(BlockedArgs a, DevRule r)
+{
+    static_assert(V % 4 == 0, "V must be a multiple of 4 (int4 vectors)");
+    constexpr int W = 32 * V;
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t S = W - a.KL - a.KR;
+    const int64_t n = a.n;
+    const int64_t total = a.nwin * a.batch;
+    const int64_t base_off = (a.bmode == BM_HALO) ? a.halo : 0;
+    const int64_t pstride = (a.bmode == BM_HALO) ? n + 2 * a.halo : n;
+
+    for (int64_t wid = gw; wid < total; wid += nwarps) {
+        const int64_t b = wid / a.nwin;
+        const int64_t w = wid - b * a.nwin;
+        const int32_t* src = a.src + b * pstride;
+        int32_t* dst = a.dst + b * pstride;
+        const int64_t ws = w * S - a.KL;               // first cell of the window
+        const int64_t g0 = ws + lane * V;              // first cell of this lane
+        int32_t q[V];
+        const bool fast = (a.bmode == BM_HALO) ? (ws + W <= n + a.halo)
+                                               : (ws >= 0 && ws + W <= n);
+        if (fast) {
+            const int4* s4 = reinterpret_cast<const int4*>(src + base_off + g0);
+#pragma unroll
+            for (int j = 0; j < V / 4; ++j) {
+                int4 v = __ldg(s4 + j);
+                q[4 * j] = v.x; q[4 * j + 1] = v.y; q[4 * j + 2] = v.z; q[4 * j + 3] = v.w;
+            }
+            run_window_steps<RULE, V, false>(q, a.ksteps, r, g0, n);
+        } else {
+#pragma unroll
+            for (int j = 0; j < V; ++j) q[j] = src[wrap_index(g0 + j, n, a.bmode, a.halo)];
+            if (a.bmode == BM_TRANSMISSIVE)
+                run_window_steps<RULE, V, true>(q, a.ksteps, r, g0, n);
+            else
+                run_window_steps<RULE, V, false>(q, a.ksteps, r, g0, n);
+        }
+        // store the cells whose dependence cone stayed inside the window
+        const int lo = a.KL, hi = W - a.KR;
+#pragma unroll
+        for (int j = 0; j < V / 4; ++j) {
+            const int pos = lane * V + 4 * j;
+            if (pos >= lo && pos < hi) {
+                const int64_t gi = ws + pos;
+                if (gi + 4 <= n) {
+                    int4 v = make_int4(q[4 * j], q[4 * j + 1], q[4 * j + 2], q[4 * j + 3]);
+                    *reinterpret_cast<int4*>(dst + base_off + gi) = v;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (gi + e < n && gi + e >= 0) dst[base_off + gi + e] = q[4 * j + e];
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1: naive, one thread per cell, one step per launch
+template <int RULE>
+__global__ void k_naive(const int32_t* __restrict__ src, int32_t* __restrict__ dst, int64_t n,
+                        int64_t batch, int bmode, DevRule r)
+{
+    const int64_t total = n * batch;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = t / n, i = t - b * n;
+        const int32_t* s = src + b * n;
+        int64_t il = i - 1, ir = i + 1;
+        if (bmode == BM_PERIODIC) {
+            if (il < 0) il += n;
+            if (ir >= n) ir -= n;
+        } else {
+            if (il < 0) il = 0;
+            if (ir >= n) ir = n - 1;
+        }
+        int32_t pl, ml, pc, mc, pr, mr;
+        phi_pm<RULE>(s[il], pl, ml, r);
+        phi_pm<RULE>(s[i], pc, mc, r);
+        phi_pm<RULE>(s[ir], pr, mr, r);
+        const int32_t Fr = pc + mr, Fl = pl + mc;
+        dst[b * n + i] = s[i] - (Fr - Fl);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3: one problem of 32*V cells per warp, all steps in registers
+template <int RULE, int V, bool WALL>
+__global__ void __launch_bounds__(128) k_warp_ensemble(int32_t* __restrict__ q, int64_t batch,
+                                                        int64_t nsteps, DevRule r)
+{
+    constexpr int N = 32 * V;
+    const int lane = threadIdx.x & 31;
+    const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (b >= batch) return;
+    int32_t* qb = q + b * N + lane * V;
+    int32_t c[V];
+    if (V >= 4) {
+#pragma unroll
+        for (int j = 0; j < V / 4; ++j) {
+            int4 v = reinterpret_cast<const int4*>(qb)[j];
+            c[4 * j] = v.x; c[4 * j + 1] = v.y; c[4 * j + 2] = v.z; c[4 * j + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < V; ++j) c[j] = qb[j];
+    }
+    const int left = (lane + 31) & 31, right = (lane + 1) & 31;
+    const int64_t g0 = (int64_t)lane * V;
+    for (int64_t s = 0; s < nsteps; ++s) {
+        int32_t p[V], m[V];
+        eval_maps<RULE, V>(c, p, m, r);
+        int32_t pl = __shfl_sync(FULL, p[V - 1], left);    // periodic wrap inside the warp
+        int32_t mr = __shfl_sync(FULL, m[0], right);
+        step_cells<RULE, V, WALL>(c, p, m, pl, mr, g0, N);
+    }
+    if (V >= 4) {
+#pragma unroll
+        for (int j = 0; j < V / 4; ++j)
+            reinterpret_cast<int4*>(qb)[j] = make_int4(c[4 * j], c[4 * j + 1], c[4 * j + 2],
+                                                       c[4 * j + 3]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < V; ++j) qb[j] = c[j];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K4: one problem per CTA, state and maps in shared memory
+template <int RULE>
+__global__ void __launch_bounds__(1024) k_cta_ensemble(int32_t* __restrict__ q, int64_t n,
+                                                       int64_t nsteps, int bmode, DevRule r)
+{
+    extern __shared__ int32_t sm[];
+    int32_t* Q = sm;
+    int32_t* P = sm + n;
+    int32_t* M = sm + 2 * n;
+    int32_t* qb = q + (int64_t)blockIdx.x * n;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) Q[i] = qb[i];
+    __syncthreads();
+    for (int64_t s = 0; s < nsteps; ++s) {
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) phi_pm<RULE>(Q[i], P[i], M[i], r);
+        __syncthreads();
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            int64_t il = i - 1, ir = i + 1;
+            int32_t Fl, Fr;
+            if (bmode == BM_PERIODIC) {
+                if (il < 0) il += n;
+                if (ir >= n) ir -= n;
+                Fl = P[il] + M[i];
+                Fr = P[i] + M[ir];
+            } else {
+                Fl = (i == 0) ? P[0] + M[0] : P[il] + M[i];
+                Fr = (i == n - 1) ? P[i] + M[i] : P[i] + M[ir];
+            }
+            Q[i] = Q[i] - (Fr - Fl);
+        }
+        __syncthreads();
+    }
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) qb[i] = Q[i];
+}
+
+// ---------------------------------------------------------------------------
+template <int RULE>
+__global__ void k_transfer(const int32_t* __restrict__ q, int32_t* __restrict__ pp,
+                           int32_t* __restrict__ pm, int64_t n, DevRule r)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t p, m;
+        phi_pm<RULE>(q[i], p, m, r);
+        pp[i] = p;
+        pm[i] = m;
+    }
+}
+
+template <typename T>
+__global__ void k_minmax(const T* __restrict__ q, int64_t n, long long* out)
+{
+    long long lo = LLONG_MAX, hi = LLONG_MIN;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        long long v = (long long)q[i];
+        lo = v < lo ? v : lo;
+        hi = v > hi ? v : hi;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        long long a = __shfl_xor_sync(FULL, lo, o), b = __shfl_xor_sync(FULL, hi, o);
+        lo = a < lo ? a : lo;
+        hi = b > hi ? b : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(out, lo);
+        atomicMax(out + 1, hi);
+    }
+}
+
+template <typename T>
+__global__ void k_observe(const T* __restrict__ q, double delta, double* __restrict__ u, int64_t n)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        u[i] = __dmul_rn(delta, (double)q[i]);          // u = fl(delta q)
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+static int grid_for(int64_t work, int threads, int cap)
+{
+    int64_t g = (work + threads - 1) / threads;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+template <int RULE, int V>
+static cudaError_t blocked_v(const BlockedArgs& a, const DevRule& r, cudaStream_t st, int cap)
+{
+    const int threads = 256;
+    int64_t warps = a.nwin * a.batch;
+    int g = grid_for(warps * 32, threads, cap);
+    k_blocked<RULE, V><<<g, threads, 0, st>>>(a, r);
+    return cudaGetLastError();
+}
+
+template <int RULE>
+static cudaError_t blocked_rule(int V, const BlockedArgs& a, const DevRule& r, cudaStream_t st,
+                                int cap)
+{
+    switch (V) {
+        case 8: return blocked_v<RULE, 8>(a, r, st, cap);
+        case 16: return blocked_v<RULE, 16>(a, r, st, cap);
+        case 32: return blocked_v<RULE, 32>(a, r, st, cap);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+bool blocked_has_V(int V) { return V == 8 || V == 16 || V == 32; }
+int blocked_max_V() { return 32; }
+
+cudaError_t launch_blocked(int rule, int V, const BlockedArgs& a, const DevRule& r,
+                           cudaStream_t st, int grid_cap)
+{
+    switch (rule) {
+        case R_LIN_HALF: return blocked_rule<R_LIN_HALF>(V, a, r, st, grid_cap);
+        case R_EO_FAST: return blocked_rule<R_EO_FAST>(V, a, r, st, grid_cap);
+        case R_GENERIC: return blocked_rule<R_GENERIC>(V, a, r, st, grid_cap);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_naive(int rule, const int32_t* src, int32_t* dst, int64_t n, int64_t batch,
+                         int bmode, const DevRule& r, cudaStream_t st)
+{
+    const int threads = 256;
+    int g = grid_for(n * batch, threads, 148 * 32);
+    switch (rule) {
+        case R_LIN_HALF: k_naive<R_LIN_HALF><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
+        case R_EO_FAST: k_naive<R_EO_FAST><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
+        case R_GENERIC: k_naive<R_GENERIC><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+template <int RULE, int V>
+static cudaError_t warp_v(int32_t* q, int64_t batch, int64_t nsteps, int bmode, const DevRule& r,
+                          cudaStream_t st)
+{
+    const int threads = 128;
+    int64_t g = (batch * 32 + threads - 1) / threads;
+    if (bmode == BM_TRANSMISSIVE)
+        k_warp_ensemble<RULE, V, true><<<(unsigned)g, threads, 0, st>>>(q, batch, nsteps, r);
+    else
+        k_warp_ensemble<RULE, V, false><<<(unsigned)g, threads, 0, st>>>(q, batch, nsteps, r);
+    return cudaGetLastError();
+}
+
+template <int RULE>
+static cudaError_t warp_rule(int V, int32_t* q, int64_t batch, int64_t nsteps, int bmode,
+                             const DevRule& r, cudaStream_t st)
+{
+    switch (V) {
+        case 1: return warp_v<RULE, 1>(q, batch, nsteps, bmode, r, st);
+        case 2: return warp_v<RULE, 2>(q, batch, nsteps, bmode, r, st);
+        case 4: return warp_v<RULE, 4>(q, batch, nsteps, bmode, r, st);
+        case 8: return warp_v<RULE, 8>(q, batch, nsteps, bmode, r, st);
+        case 16: return warp_v<RULE, 16>(q, batch, nsteps, bmode, r, st);
+        case 32: return warp_v<RULE, 32>(q, batch, nsteps, bmode, r, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+bool warp_ensemble_has_V(int V) { return V == 1 || V == 2 || V == 4 || V == 8 || V == 16 || V == 32; }
+
+cudaError_t launch_warp_ensemble(int rule, int V, int32_t* q, int64_t batch, int64_t nsteps,
+                                 int bmode, const DevRule& r, cudaStream_t st)
+{
+    switch (rule) {
+        case R_LIN_HALF: return warp_rule<R_LIN_HALF>(V, q, batch, nsteps, bmode, r, st);
+        case R_EO_FAST: return warp_rule<R_EO_FAST>(V, q, batch, nsteps, bmode, r, st);
+        case R_GENERIC: return warp_rule<R_GENERIC>(V, q, batch, nsteps, bmode, r, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <int RULE>
+static cudaError_t cta_rule(int32_t* q, int64_t n, int64_t batch, int64_t nsteps, int bmode,
+                            const DevRule& r, cudaStream_t st)
+{
+    size_t smem = (size_t)n * 3 * sizeof(int32_t);
+    cudaError_t e = cudaFuncSetAttribute(k_cta_ensemble<RULE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int threads = n >= 1024 ? 1024 : (int)((n + 31) / 32 * 32);
+    k_cta_ensemble<RULE><<<(unsigned)batch, threads, smem, st>>>(q, n, nsteps, bmode, r);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cta_ensemble(int rule, int32_t* q, int64_t n, int64_t batch, int64_t nsteps,
+                                int bmode, const DevRule& r, cudaStream_t st)
+{
+    switch (rule) {
+        case R_LIN_HALF: return cta_rule<R_LIN_HALF>(q, n, batch, nsteps, bmode, r, st);
+        case R_EO_FAST: return cta_rule<R_EO_FAST>(q, n, batch, nsteps, bmode, r, st);
+        case R_GENERIC: return cta_rule<R_GENERIC>(q, n, batch, nsteps, bmode, r, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_transfer(int rule, const int32_t* q, int32_t* pp, int32_t* pm, int64_t n,
+                            const DevRule& r, cudaStream_t st)
+{
+    int g = grid_for(n, 256, 148 * 16);
+    switch (rule) {
+        case R_LIN_HALF: k_transfer<R_LIN_HALF><<<g, 256, 0, st>>>(q, pp, pm, n, r); break;
+        case R_EO_FAST: k_transfer<R_EO_FAST><<<g, 256, 0, st>>>(q, pp, pm, n, r); break;
+        case R_GENERIC: k_transfer<R_GENERIC><<<g, 256, 0, st>>>(q, pp, pm, n, r); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_minmax(const void* q, int dtype, int64_t n, long long* out2, cudaStream_t st)
+{
+    int g = grid_for(n, 256, 148 * 8);
+    if (dtype == 0)
+        k_minmax<int32_t><<<g, 256, 0, st>>>((const int32_t*)q, n, out2);
+    else
+        k_minmax<int64_t><<<g, 256, 0, st>>>((const int64_t*)q, n, out2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_observe(const void* q, int dtype, double delta, double* u, int64_t n,
+                           cudaStream_t st)
+{
+    int g = grid_for(n, 256, 148 * 16);
+    if (dtype == 0)
+        k_observe<int32_t><<<g, 256, 0, st>>>((const int32_t*)q, delta, u, n);
+    else
+        k_observe<int64_t><<<g, 256, 0, st>>>((const int64_t*)q, delta, u, n);
+    return cudaGetLastError();
+}
+
+}  // namespace fqnm

@@ -1,0 +1,358 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle,
+element by element, bit-exact on the integer state (BJ north_star target).
+
+Sizes: small/ragged cases span several tiles; the BASELINE configs run at
+their full sizes in the launch configuration bench.py uses, checked on
+light-cone windows (after S steps cell i depends only on [i-S, i+S], so the
+oracle on a window of the initial data reproduces the window exactly) plus
+full-domain invariants (exact conservation, maximum principle, TVD).
+"""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def F():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2604_06947_b200 as F
+    F._load()
+    return F
+
+
+def to_dev(q, dtype=torch.int32):
+    return torch.tensor(np.asarray(q), dtype=dtype, device=DEV)
+
+
+def host(t):
+    return t.cpu().numpy().astype(np.int64)
+
+
+def tv_periodic(t):
+    t64 = t.to(torch.int64)
+    return int((t64 - torch.roll(t64, 1)).abs().sum())
+
+
+# ---------------------------------------------------------------------------
+# maps: the kernels' own map code, exhaustively over admissible ranges
+@pytest.mark.parametrize("kind,delta,lam,param", [
+    (W.LINEAR, "1e-4", Fraction(1, 2), 1),
+    (W.BURGERS_EO, "1e-5", Fraction(4, 15), 1),                  # cfg2
+    (W.BURGERS_EO, "1e-6", Fraction(2, 5) / Fraction("1e-6") / 345000, 1),   # cfg4-like
+    (W.BURGERS_EO, "1e-6", Fraction(2, 5) / Fraction("1e-6") / 1_200_000, 1),
+    (W.LINEAR, "1e-3", Fraction(7, 9), 1),
+    (W.LINEAR, "1e-3", Fraction(1, 3), -1),
+    (W.BURGERS_LF, "1e-3", Fraction(1, 2), 1),
+])
+def test_device_maps_exhaustive(F, kind, delta, lam, param):
+    plan = F.fqnm_plan_ex(1 << 20, float(Fraction(delta)), float(lam), kind,
+                          flux_param=float(param))
+    info = plan.info()
+    lo, hi = max(info["q_lo"], -4_000_000), min(info["q_hi"], 4_000_000)
+    q = torch.arange(lo, hi + 1, dtype=torch.int32, device=DEV)
+    p, m = F.fqnm_transfer_device(plan, q)
+    r = oracle.Rule(kind, delta, lam, Fraction(param))
+    qh = np.arange(lo, hi + 1, dtype=np.int64)
+    assert np.array_equal(host(p), r.phi_plus(qh))
+    assert np.array_equal(host(m), r.phi_minus(qh))
+    for qq in (lo, -1, 0, 1, hi):
+        assert F.fqnm_transfer(plan, qq) == (int(r.phi_plus(qq)[0]), int(r.phi_minus(qq)[0]))
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configs
+def test_cfg1_full(F):
+    w = W.cfg("cfg1")
+    q0 = W.q0_cfg1()
+    plan = F.fqnm_plan(w.n, float(w.delta), W.dt_dx_double(w), F.LINEAR, F.PERIODIC)
+    q = to_dev(q0)
+    F.fqnm_step(plan, q, w.steps)
+    ref = oracle.Rule(W.LINEAR, w.delta, W.dt_dx(w)).run(q0, w.steps)
+    assert np.array_equal(host(q), ref)
+    u = F.fqnm_observe(plan, q).cpu().numpy()
+    assert np.array_equal(u, oracle.observe(ref, 1e-4))
+
+
+def test_cfg2_full(F):
+    w = W.cfg("cfg2")
+    q0 = W.q0_cfg2()
+    qmax = int(np.abs(q0).max())
+    assert qmax == 150000
+    plan = F.fqnm_plan(w.n, float(w.delta), W.dt_dx_double(w, qmax), F.BURGERS_EO, F.PERIODIC)
+    q = to_dev(q0)
+    F.fqnm_step(plan, q, w.steps)
+    ref = oracle.Rule(W.BURGERS_EO, w.delta, W.dt_dx(w, qmax)).run(q0, w.steps)
+    assert np.array_equal(host(q), ref)
+
+
+def _windows(n, rng, extra=()):
+    ws = [(0, 4096), (n - 4096, n), (n // 2 - 2048, n // 2 + 2048)] + list(extra)
+    for a in rng.integers(0, n - 4096, 5):
+        ws.append((int(a), int(a) + 4096))
+    return ws
+
+
+def _check_windows(q_gpu, q0_at, rule, n, S, left, right, windows, boundary=W.PERIODIC):
+    qg = q_gpu
+    for a, b in windows:
+        lo = a - (S if left else 0)
+        hi = b + (S if right else 0)
+        idx = np.arange(lo, hi)
+        qin = q0_at(idx % n)
+        out = rule.run(qin, S, boundary)
+        got = qg[a:b].cpu().numpy().astype(np.int64)
+        assert np.array_equal(out[a - lo:a - lo + (b - a)], got), f"window [{a},{b})"
+
+
+def test_cfg3_full_size_windows(F):
+    w = W.cfg("cfg3")
+    q0 = W.q0_cfg3()
+    plan = F.fqnm_plan(w.n, float(w.delta), W.dt_dx_double(w), F.LINEAR, F.PERIODIC)
+    assert plan.info()["kernel"] == 2
+    q = to_dev(q0)
+    s0, tv0, mn, mx = int(q.to(torch.int64).sum()), tv_periodic(q), int(q.min()), int(q.max())
+    F.fqnm_step(plan, q, w.steps)
+    assert int(q.to(torch.int64).sum()) == s0
+    assert int(q.min()) >= mn and int(q.max()) <= mx and tv_periodic(q) <= tv0
+    rule = oracle.Rule(W.LINEAR, w.delta, W.dt_dx(w))
+    rng = np.random.default_rng(31)
+    _check_windows(q, lambda idx: q0[idx], rule, w.n, w.steps, True, False,
+                   _windows(w.n, rng)[:6])
+
+
+def test_cfg4_full_size_windows(F):
+    """BJ.cfg4 at its full size N = 2^31 (8 GiB state), 1000 steps, 1 GPU."""
+    w = W.cfg("cfg4")
+    n = w.n
+    q = W.q0_cfg4(n=n, device=DEV)
+    qmax = int(q.abs().max())
+    s0 = int(q.sum(dtype=torch.int64))
+    mn, mx = int(q.min()), int(q.max())
+    plan = F.fqnm_plan(n, 1e-6, W.dt_dx_double(w, qmax), F.BURGERS_EO, F.PERIODIC)
+    info = plan.info()
+    assert (info["kappa_num"], info["kappa_den"]) == (1, 5 * qmax)
+    F.fqnm_step(plan, q, w.steps)
+    torch.cuda.synchronize()
+    assert int(q.sum(dtype=torch.int64)) == s0
+    assert int(q.min()) >= mn and int(q.max()) <= mx
+    rule = oracle.Rule(W.BURGERS_EO, w.delta, W.dt_dx(w, qmax))
+    rng = np.random.default_rng(41)
+    _check_windows(q, lambda idx: W.q0_cfg4_at(idx, n=n, device=DEV), rule, n, w.steps,
+                   True, True, _windows(n, rng)[:8])
+    del q
+    torch.cuda.empty_cache()
+
+
+def test_ens1_sampled(F):
+    w = W.cfg("ens1")
+    B = w.batch
+    q0 = W.q0_ensemble(B)
+    plan = F.fqnm_plan_ex(w.n, float(w.delta), W.dt_dx_double(w), F.LINEAR, batch=B)
+    assert plan.info()["kernel"] == 3
+    q = to_dev(q0)
+    F.fqnm_step(plan, q, w.steps)
+    rule = oracle.Rule(W.LINEAR, w.delta, W.dt_dx(w))
+    rng = np.random.default_rng(51)
+    pick = np.unique(np.concatenate([[0, B - 1], rng.integers(0, B, 30)]))
+    ref = rule.run(q0[pick], w.steps)
+    assert np.array_equal(host(q[pick]), ref)
+    assert np.array_equal(host(q).sum(axis=1), q0.sum(axis=1))
+
+
+def test_cfg5_sod_full_t_small_n(F):
+    """Sod to t = 0.2 at N = 1024 (607 steps) through the Euler kernel, full parity."""
+    n = 1024
+    nsteps, lam = W.sod_steps_and_dt_dx(n)
+    q0 = W.sod_q0(n)
+    plan = F.fqnm_plan(n, 1e-7, lam, F.EULER_ROE, F.TRANSMISSIVE)
+    q = to_dev(q0, torch.int64)
+    F.fqnm_step(plan, q, nsteps)
+    ref = oracle.euler_run(q0, nsteps, 1e-7, lam)
+    assert np.array_equal(q.cpu().numpy(), ref)
+
+
+def test_cfg5_full_size_windows(F):
+    """BJ.cfg5 at N = 2^26 (3 x int64), 200 steps at the config's dt/dx; windows at both
+    walls, the diaphragm and random places."""
+    n = W.cfg("cfg5").n
+    S = 200
+    _, lam = W.sod_steps_and_dt_dx(n)
+    q0 = W.sod_q0(n)
+    plan = F.fqnm_plan(n, 1e-7, lam, F.EULER_ROE, F.TRANSMISSIVE)
+    q = to_dev(q0, torch.int64)
+    F.fqnm_step(plan, q, S)
+    qh = q.cpu().numpy()
+    sums = q0.sum(axis=1)
+    assert qh[0].sum() == sums[0] and qh[2].sum() == sums[2]   # waves far from the walls
+    for a, b in [(0, 2048), (n - 2048, n), (n // 2 - 1024, n // 2 + 1024), (12345, 14345)]:
+        lo, hi = max(0, a - S), min(n, b + S)
+        ref = oracle.euler_run(np.ascontiguousarray(q0[:, lo:hi]), S, 1e-7, lam)
+        assert np.array_equal(qh[:, a:b], ref[:, a - lo:b - lo]), (a, b)
+
+
+def test_roe_transfer_device_random_states(F):
+    rng = np.random.default_rng(61)
+    n = 4096
+    def states():
+        rho = rng.uniform(0.1, 2.0, n); p = rng.uniform(0.1, 2.0, n)
+        u = rng.uniform(-2, 2, n) * np.sqrt(1.4 * p / rho)
+        E = p / 0.4 + 0.5 * rho * u * u
+        return np.stack([np.rint(rho / 1e-7), np.rint(rho * u / 1e-7), np.rint(E / 1e-7)]).astype(np.int64)
+    qL, qR = states(), states()
+    qR[:, :100] = qL[:, :100]                      # equal states
+    plan = F.fqnm_plan(64, 1e-7, 0.3, F.EULER_ROE, F.TRANSMISSIVE)
+    T = F.fqnm_roe_transfer_device(plan, to_dev(qL, torch.int64), to_dev(qR, torch.int64)).cpu().numpy()
+    for i in range(n):
+        assert np.array_equal(T[:, i], oracle.roe_transfer(qL[:, i], qR[:, i], 1e-7, 0.3)), i
+
+
+# ---------------------------------------------------------------------------
+# families, boundaries, ragged sizes, k/V choices, degenerate cases
+CASES = [  # (kind, delta, lam, param, data amplitude, offset)
+    (W.LINEAR, "1e-4", Fraction(1, 2), 1, 5000, 0),
+    (W.BURGERS_EO, "1e-5", Fraction(4, 15), 1, 100000, 20000),
+    (W.BURGERS_LF, "1e-3", Fraction(1, 2), 1, 900, 0),
+    (W.LINEAR, "1e-3", Fraction(1, 3), -1, 3000, 100),
+]
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+@pytest.mark.parametrize("boundary", [W.PERIODIC, W.TRANSMISSIVE])
+@pytest.mark.parametrize("n", [2, 3, 33, 127, 1000, 1024, 4099, 20000, 65536 + 513])
+def test_all_families_match_oracle(F, case, boundary, n):
+    kind, delta, lam, param, amp, off = CASES[case]
+    rng = np.random.default_rng(1000 + 7 * n + case)
+    q0 = np.clip(W.smooth_random(rng, n, amp, off) + rng.integers(-amp // 20, amp // 20 + 1, n),
+                 -amp, amp + off)
+    rule = oracle.Rule(kind, delta, lam, Fraction(param))
+    for nsteps in (0, 1, 7, 40):
+        ref = rule.run(q0, nsteps, boundary)
+        fams = [0, 1]
+        if n >= 64:
+            fams.append(2)
+        if n <= 16384:
+            fams.append(4)
+        if n % 32 == 0 and n // 32 in (1, 2, 4, 8, 16, 32):
+            fams.append(3)
+        for fam in fams:
+            plan = F.fqnm_plan_ex(n, float(Fraction(delta)), float(lam), kind, boundary,
+                                  flux_param=float(param))
+            if fam:
+                F.fqnm_debug_override(plan, fam)
+            q = to_dev(q0)
+            F.fqnm_step(plan, q, nsteps)
+            assert np.array_equal(host(q), ref), (fam, nsteps)
+
+
+@pytest.mark.parametrize("V,k", [(8, 1), (8, 3), (8, 8), (16, 4), (16, 13), (16, 32), (32, 7),
+                                 (32, 64), (16, 64)])
+@pytest.mark.parametrize("case", [0, 1])
+def test_blocked_k_and_v(F, V, k, case):
+    kind, delta, lam, param, amp, off = CASES[case]
+    n = 50000 + 3
+    rng = np.random.default_rng(77 + V + k)
+    q0 = W.smooth_random(rng, n, amp, off)
+    rule = oracle.Rule(kind, delta, lam, Fraction(param))
+    ref = rule.run(q0, 100)
+    plan = F.fqnm_plan_ex(n, float(Fraction(delta)), float(lam), kind)
+    try:
+        F.fqnm_debug_override(plan, 2, 0, V)
+        F.fqnm_debug_override(plan, 0, k, 0)
+    except F.FqnmError:
+        pytest.skip("k too large for V with this dependence")
+    q = to_dev(q0)
+    F.fqnm_step(plan, q, 100)
+    assert np.array_equal(host(q), ref)
+
+
+def test_batched_blocked_and_cta(F):
+    kind, delta, lam, param, amp, off = CASES[1]
+    rng = np.random.default_rng(5)
+    for n, B in [(3000, 7), (70001, 3)]:
+        q0 = np.stack([W.smooth_random(rng, n, amp, off) for _ in range(B)])
+        rule = oracle.Rule(kind, delta, lam)
+        ref = rule.run(q0, 33)
+        plan = F.fqnm_plan_ex(n, float(Fraction(delta)), float(lam), kind, batch=B)
+        q = to_dev(q0)
+        F.fqnm_step(plan, q, 33)
+        assert np.array_equal(host(q), ref)
+
+
+def test_split_domain_virtual_ranks(F):
+    """The halo-exchange path (FQNM_HALO plans + fqnm_step_block) on P virtual
+    subdomains of one GPU equals the single-domain result bit for bit."""
+    from paper_2604_06947_b200 import halo
+    kind, delta, lam, param, amp, off = CASES[1]
+    n = 200003
+    rng = np.random.default_rng(9)
+    q0 = W.smooth_random(rng, n, amp, off)
+    ref = oracle.Rule(kind, delta, lam).run(q0, 75)
+    for P, H in [(1, 16), (2, 16), (3, 8), (4, 32), (5, 4)]:
+        parts = [halo.partition(n, P, r) for r in range(P)]
+        plans = [F.fqnm_plan_ex(nl, float(Fraction(delta)), float(lam), kind, F.HALO, halo=H,
+                                n_global=n, offset=off_) for off_, nl in parts]
+        sd = halo.SplitDomain([nl for _, nl in parts], H, halo.LocalTransport(),
+                              [p.step_block for p in plans],
+                              lambda m: torch.zeros(m, dtype=torch.int32, device=DEV))
+        sd.load([to_dev(q0[o:o + nl]) for o, nl in parts])
+        sd.step(75)
+        got = np.concatenate([host(sd.owned(i)) for i in range(P)])
+        assert np.array_equal(got, ref), (P, H)
+
+
+def test_range_check_and_errors(F):
+    plan = F.fqnm_plan(65536, 1e-5, float(Fraction(4, 15)), F.BURGERS_EO, F.PERIODIC)
+    hi = plan.info()["q_hi"]
+    q = torch.zeros(65536, dtype=torch.int32, device=DEV)
+    q[123] = hi + 1
+    before = q.clone()
+    with pytest.raises(F.FqnmError) as e:
+        F.fqnm_step(plan, q, 3)
+    assert e.value.status == 3 and torch.equal(q, before)
+    with pytest.raises(F.FqnmError):
+        F.fqnm_step(plan, q, -1)
+    with pytest.raises(TypeError):
+        F.fqnm_step(plan, q.cpu(), 1)
+    with pytest.raises(TypeError):
+        F.fqnm_step(plan, q.to(torch.int64), 1)
+
+
+def test_step_host_equals_device_and_composition(F):
+    kind, delta, lam, param, amp, off = CASES[1]
+    n = 300007
+    rng = np.random.default_rng(3)
+    q0 = W.smooth_random(rng, n, amp, off)
+    plan = F.fqnm_plan_ex(n, float(Fraction(delta)), float(lam), kind)
+    qd = to_dev(q0)
+    F.fqnm_step(plan, qd, 50)
+    qh = torch.tensor(q0, dtype=torch.int32).pin_memory()
+    F.fqnm_step_host(plan, qh, 50)
+    assert torch.equal(qh, qd.cpu())
+    q2 = to_dev(q0)
+    F.fqnm_step(plan, q2, 20)
+    F.fqnm_step(plan, q2, 30)
+    assert torch.equal(q2, qd)                      # step(a+b) = step(b) o step(a)
+    q3 = to_dev(q0)
+    F.fqnm_step(plan, q3, 50)
+    assert torch.equal(q3, qd)                      # deterministic
+
+
+def test_profile_hooks(F):
+    plan = F.fqnm_plan(1 << 20, 1e-6, 0.5, F.LINEAR, F.PERIODIC)
+    q = to_dev(W.q0_cfg3(1 << 20))
+    F.fqnm_profile_enable(plan, True)
+    before = plan.launches()
+    F.fqnm_step(plan, q, 100)
+    ms, nl = F.fqnm_profile_read(plan)
+    assert nl >= 1 and ms > 0
+    assert plan.launches() - before >= nl

@@ -172,13 +172,24 @@ def cfg4_modes(seed: int = 0, nmodes: int = 64):
     return amp, phase
 
 
+def u0_cfg4_at(i, n: int, amp, phase):
+    """u0 of BJ.cfg4 at integer cell indices i (float64 torch tensor of indices)."""
+    import torch
+    x = (i + 0.5) / float(n)
+    u = torch.full_like(x, 0.2)
+    for k in range(len(amp)):
+        u += float(amp[k]) * torch.sin((2.0 * math.pi * (k + 1)) * x + float(phase[k]))
+    return u
+
+
 def q0_cfg4(n: int = 1 << 31, delta: float = 1e-6, seed: int = 0, nmodes: int = 64,
             device=None, offset: int = 0, count: Optional[int] = None,
             out=None, chunk: int = 1 << 25):
     """BJ.cfg4: u0 = 0.2 + sum_k a_k sin(2 pi k x + theta_k), summed in k order.
 
     Generated in float64 with torch (on `device`, chunked) into an int32
-    tensor `out` (allocated if None).  Returns the int32 tensor."""
+    tensor `out` (allocated if None).  Elementwise, so any sub-range (or
+    `q0_cfg4_at`) reproduces the same integers bit for bit."""
     import torch
     amp, phase = cfg4_modes(seed, nmodes)
     if count is None:
@@ -189,12 +200,17 @@ def q0_cfg4(n: int = 1 << 31, delta: float = 1e-6, seed: int = 0, nmodes: int = 
     for s in range(0, count, chunk):
         e = min(count, s + chunk)
         i = torch.arange(offset + s, offset + e, dtype=torch.float64, device=dev)
-        x = (i + 0.5) / float(n)
-        u = torch.full_like(x, 0.2)
-        for k in range(nmodes):
-            u += float(amp[k]) * torch.sin((2.0 * math.pi * (k + 1)) * x + float(phase[k]))
-        out[s:e] = quantise(u, delta).to(torch.int32)
+        out[s:e] = quantise(u0_cfg4_at(i, n, amp, phase), delta).to(torch.int32)
     return out
+
+
+def q0_cfg4_at(idx, n: int = 1 << 31, delta: float = 1e-6, seed: int = 0, nmodes: int = 64,
+               device=None):
+    """q0 of BJ.cfg4 at arbitrary (e.g. wrapped window) indices; int64 numpy array."""
+    import torch
+    amp, phase = cfg4_modes(seed, nmodes)
+    i = torch.as_tensor(np.asarray(idx) % n, dtype=torch.float64, device=device)
+    return quantise(u0_cfg4_at(i, n, amp, phase), delta).cpu().numpy()
 
 
 def q0_ensemble(batch: int, n: int = 1024, delta: float = 1e-4, first: int = 0,
