@@ -37,7 +37,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def lib_path() -> str:
-    return os.path.join(_HERE, "libfqnm.so")
+    # FQNM_LIBPATH: alternative in-tree build (tools/tune.py variant sweeps only)
+    return os.environ.get("FQNM_LIBPATH") or os.path.join(_HERE, "libfqnm.so")
 
 
 class FqnmError(RuntimeError):

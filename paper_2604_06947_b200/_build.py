@@ -37,8 +37,9 @@ def _stale(obj: str, src: str) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> str:
-    objdir = os.path.join(HERE, "build")
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False,
+          defines=(), lib: str = LIB, objdir: str = "") -> str:
+    objdir = objdir or os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     rebuilt = False
@@ -47,18 +48,18 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
         obj = os.path.join(objdir, unit.replace(".cu", ".o"))
         objs.append(obj)
         if force or _stale(obj, src):
-            cmd = [NVCC, *ARCH, *COMMON, *extra, "-c", src, "-o", obj]
+            cmd = [NVCC, *ARCH, *COMMON, *extra, *[f"-D{x}" for x in defines], "-c", src, "-o", obj]
             if ptxas_v:
                 cmd[1:1] = ["-Xptxas", "-v"]
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
             subprocess.check_call(cmd)
             rebuilt = True
-    if rebuilt or force or not os.path.exists(LIB):
-        tmp = LIB + f".{os.getpid()}.tmp"
+    if rebuilt or force or not os.path.exists(lib):
+        tmp = lib + f".{os.getpid()}.tmp"
         subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static"])
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -152,6 +152,7 @@ struct fqnm_plan {
     int family = 0;
     int V = 0;
     int k = 0;
+    int minb = 0;         // K2 register cap variant (0 = default)
     // Euler constants
     double s_e = 0, g1_e = 0;
     // memory
@@ -277,11 +278,11 @@ static int build_rule(fqnm_plan_t* p)
     int64_t a_fast = 0;
     if (kind == FQNM_BURGERS_EO && d.rounding == FQNM_ROUND_HALF_AWAY && P >= 1 &&
         P < (1 << 29) && Q < (1 << 29)) {
-        // largest a with a < 2^23 and P a^2 / Q <= 2^22 - 8
-        double am = std::sqrt((std::ldexp(1.0, 22) - 8.0) * (double)Q / (double)P);
-        a_fast = (int64_t)am;
-        while (a_fast > 0 && (i128)P * a_fast * a_fast > ((i128)((1 << 22) - 8)) * Q) --a_fast;
-        if (a_fast > (1 << 23) - 1) a_fast = (1 << 23) - 1;
+        // maps.cuh eo_g: exact for |q| < 2^22 and P q^2 / Q <= 2^20
+        double am = std::sqrt(std::ldexp(1.0, 20) * (double)Q / (double)P);
+        a_fast = (int64_t)am + 1;
+        while (a_fast > 0 && (i128)P * a_fast * a_fast > ((i128)1 << 20) * Q) --a_fast;
+        if (a_fast > (1 << 22) - 1) a_fast = (1 << 22) - 1;
         eo_fast_ok = a_fast > 0;
     }
     int64_t lo = d.q_lo, hi = d.q_hi;
@@ -344,11 +345,17 @@ static int build_rule(fqnm_plan_t* p)
     if (map_is_zero(p->hp)) r.suppp = SUPP_NONE;
     if (map_is_zero(p->hm)) r.suppm = SUPP_NONE;
     r.rounding = d.rounding;
+    r.one = 1;
+    r.mone = -1;
     if (p->rule == R_EO_FAST) {
-        r.eo_twoP = (int32_t)(2 * P);
-        r.eo_Q = (int32_t)Q;
+        r.eo_ntwoP = (int32_t)(-2 * P);
         r.eo_twoQ = (int32_t)(2 * Q);
-        r.eo_cf = (float)((double)P / (double)Q);
+        r.eo_c1 = (int32_t)(uint32_t)((uint64_t)(Q - 1) - (uint64_t)(2 * Q) * 0x4B400000ull);
+        // largest float <= kappa (1 - 2^-21): a strict relative underestimate of kappa
+        const double target = ((double)P / (double)Q) * (1.0 - std::ldexp(1.0, -21));
+        float cf = (float)target;
+        while ((double)cf > target) cf = std::nextafterf(cf, 0.0f);
+        r.eo_cf = cf;
     }
     return FQNM_OK;
 }
@@ -376,8 +383,8 @@ static int choose_kernel(fqnm_plan_t* p)
     }
     if (p->family == 2) {
         const bool two = p->dep_left && p->dep_right;
-        if (p->rule == R_LIN_HALF) { p->V = 16; p->k = 32; }
-        else if (p->rule == R_EO_FAST) { p->V = 16; p->k = 16; }
+        if (p->rule == R_LIN_HALF) { p->V = 32; p->k = 64; }
+        else if (p->rule == R_EO_FAST) { p->V = 32; p->k = 24; p->minb = 2; }
         else { p->V = 8; p->k = two ? 8 : 16; }
         if (d.k > 0) p->k = d.k;
         if (d.boundary == FQNM_HALO && p->k > d.halo) p->k = (int)d.halo;
@@ -591,7 +598,7 @@ static int launch_block(fqnm_plan_t* p, const int32_t* src, int32_t* dst, int ks
     const int64_t S = 32 * p->V - a.KL - a.KR;
     if (S < 4) return fail(FQNM_ERR_ARG, "k = %d too large for V = %d", ksteps, p->V);
     a.nwin = (d.n_local + S - 1) / S;
-    PROF_LAUNCH(launch_blocked(p->rule, p->V, a, p->dr, p->st, 148 * 32));
+    PROF_LAUNCH(launch_blocked(p->rule, p->V, p->minb, a, p->dr, p->st, 148 * 32));
     return FQNM_OK;
 }
 
@@ -789,6 +796,10 @@ extern "C" int fqnm_debug_override(fqnm_plan_t* p, int32_t kernel, int32_t k, in
         if (V && !euler_has_V(V)) return fail(FQNM_ERR_UNSUPPORTED, "Euler V must be 1, 2 or 4");
         if (V) p->V = V;
         return FQNM_OK;
+    }
+    if (kernel >= 100) {               // K2 with a register-cap variant: 2 + 100 * minb
+        p->minb = kernel / 100;
+        kernel = kernel % 100;
     }
     if (kernel) {
         if (d.boundary == FQNM_HALO && kernel != 2) return fail(FQNM_ERR_UNSUPPORTED, "split domains use K2");

@@ -24,12 +24,14 @@ struct DevRule {
     int64_t c2m, c1m, denm;
     int32_t suppp, suppm;
     int32_t rounding;
-    // EO fast path constants
-    int32_t eo_twoP;      // 2P
-    int32_t eo_Q;         // Q
+    // EO fast path constants (maps.cuh eo_g)
+    int32_t eo_ntwoP;     // -2P
+    int32_t eo_c1;        // Q - 1 - 2Q * 0x4B400000  (mod 2^32)
     int32_t eo_twoQ;      // 2Q
-    float eo_cf;          // fl32(P/Q)
-    int32_t pad;
+    float eo_cf;          // largest float <= (P/Q)(1 - 2^-21)
+    int32_t one;          // runtime 1 and -1: let the linear kernel issue IMADs (FMA pipe)
+    int32_t mone;
+    int32_t pad2;
 };
 
 enum Bmode : int32_t { BM_PERIODIC = 0, BM_TRANSMISSIVE = 1, BM_HALO = 2 };
@@ -57,7 +59,7 @@ struct EulerArgs {
 };
 
 // kernel launchers (kernels_scalar.cu / kernels_euler.cu); return cudaError_t
-cudaError_t launch_blocked(int rule, int V, const BlockedArgs& a, const DevRule& r,
+cudaError_t launch_blocked(int rule, int V, int minb, const BlockedArgs& a, const DevRule& r,
                            cudaStream_t st, int grid_cap);
 cudaError_t launch_naive(int rule, const int32_t* src, int32_t* dst, int64_t n, int64_t batch,
                          int bmode, const DevRule& r, cudaStream_t st);

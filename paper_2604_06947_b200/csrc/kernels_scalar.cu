@@ -28,21 +28,23 @@ namespace fqnm {
 static constexpr unsigned FULL = 0xffffffffu;
 
 // ---------------------------------------------------------------------------
-// one explicit step of V register-resident cells of a lane.
+// one explicit step of V register-resident cells of a lane, from (g, m) with
+// g = phi+ + phi-, m = phi-:  F_{j+1/2} = phi+(q_j) + phi-(q_{j+1}) = g_j - m_j + m_{j+1}.
 //   pl, mr: phi+ of the cell left of q[0], phi- of the cell right of q[V-1]
-//   WALL:   transmissive ghost rule (interface -1/2 and N-1/2 use the edge cell)
-template <int RULE, int V, bool WALL>
-__device__ __forceinline__ void step_cells(int32_t (&q)[V], const int32_t (&p)[V],
+//   WALL:   transmissive ghost rule (interface -1/2 and N-1/2 use the edge cell:
+//           F = phi+(q_e) + phi-(q_e) = g_e)
+template <int V, bool WALL>
+__device__ __forceinline__ void step_cells(int32_t (&q)[V], const int32_t (&g)[V],
                                            const int32_t (&m)[V], int32_t pl, int32_t mr,
                                            int64_t g0, int64_t n)
 {
     int32_t Tl = pl + m[0];                 // F_{j-1/2} for j = 0
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-        int32_t Tr = (j + 1 < V) ? p[j] + m[j + 1] : p[V - 1] + mr;   // F_{j+1/2}
+        int32_t Tr = g[j] - m[j] + ((j + 1 < V) ? m[j + 1] : mr);   // F_{j+1/2}
         if (WALL) {
-            if (g0 + j == 0) Tl = p[j] + m[j];          // F_{-1/2} with ghost q_{-1} = q_0
-            if (g0 + j == n - 1) Tr = p[j] + m[j];      // F_{N-1/2} with ghost q_N = q_{N-1}
+            if (g0 + j == 0) Tl = g[j];                 // F_{-1/2} with ghost q_{-1} = q_0
+            if (g0 + j == n - 1) Tr = g[j];             // F_{N-1/2} with ghost q_N = q_{N-1}
         }
         q[j] = q[j] + Tl - Tr;
         Tl = Tr;
@@ -50,28 +52,61 @@ __device__ __forceinline__ void step_cells(int32_t (&q)[V], const int32_t (&p)[V
 }
 
 template <int RULE, int V>
-__device__ __forceinline__ void eval_maps(const int32_t (&q)[V], int32_t (&p)[V],
+__device__ __forceinline__ void eval_maps(const int32_t (&q)[V], int32_t (&g)[V],
                                           int32_t (&m)[V], const DevRule& r)
 {
 #pragma unroll
-    for (int j = 0; j < V; ++j) phi_pm<RULE>(q[j], p[j], m[j], r);
+    for (int j = 0; j < V; ++j) phi_gm<RULE>(q[j], g[j], m[j], r);
 }
 
 // ---------------------------------------------------------------------------
+// One explicit step of the lane's V cells.  NB = 0: neighbours by shfl.up/down
+// (window edges produce garbage that the caller cuts off); NB = 1: periodic
+// wrap inside the warp (K3, the warp holds a whole problem).
+template <int RULE, int V, bool WALL, int NB>
+__device__ __forceinline__ void one_step(int32_t (&q)[V], const DevRule& r, int lane, int64_t g0,
+                                         int64_t n)
+{
+    if (RULE == R_LIN_HALF && !WALL) {
+        // kappa = 1/2: q'_j = trunc(q_j/2) + phi+(q_{j-1}), phi+ = q - trunc(q/2).
+        // The runtime r.one turns the two adds into IMADs (FMA pipe) so the
+        // ALU pipe only carries the halving (LEA.HI + SHF): 2 ALU + 2 FMA ops.
+        int32_t h[V], p[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            h[j] = q[j] / 2;
+            p[j] = h[j] * r.mone + q[j];
+        }
+        const int32_t pl = NB == 0 ? __shfl_up_sync(FULL, p[V - 1], 1)
+                                   : __shfl_sync(FULL, p[V - 1], (lane + 31) & 31);
+        q[0] = pl * r.one + h[0];
+#pragma unroll
+        for (int j = 1; j < V; ++j) q[j] = p[j - 1] * r.one + h[j];
+    } else {
+        int32_t g[V], m[V];
+        eval_maps<RULE, V>(q, g, m, r);
+        const int32_t pv = g[V - 1] - m[V - 1];
+        const int32_t pl = NB == 0 ? __shfl_up_sync(FULL, pv, 1)
+                                   : __shfl_sync(FULL, pv, (lane + 31) & 31);
+        const int32_t mr = NB == 0 ? __shfl_down_sync(FULL, m[0], 1)
+                                   : __shfl_sync(FULL, m[0], (lane + 1) & 31);
+        step_cells<V, WALL>(q, g, m, pl, mr, g0, n);
+    }
+}
+
 // K2: temporally blocked stencil
 template <int RULE, int V, bool WALL>
 __device__ __forceinline__ void run_window_steps(int32_t (&q)[V], int ksteps, const DevRule& r,
                                                  int64_t g0, int64_t n)
 {
-    for (int s = 0; s < ksteps; ++s) {
-        int32_t p[V], m[V];
-        eval_maps<RULE, V>(q, p, m, r);
-        // lane 0 / lane 31 receive their own values: the garbage this creates
-        // moves inward one cell per step and is cut off by KL/KR at the store.
-        int32_t pl = __shfl_up_sync(FULL, p[V - 1], 1);
-        int32_t mr = __shfl_down_sync(FULL, m[0], 1);
-        step_cells<RULE, V, WALL>(q, p, m, pl, mr, g0, n);
+    const int lane = threadIdx.x & 31;
+    int s = 0;
+    // unrolled by two: no register renaming moves between steps
+    for (; s + 2 <= ksteps; s += 2) {
+        one_step<RULE, V, WALL, 0>(q, r, lane, g0, n);
+        one_step<RULE, V, WALL, 0>(q, r, lane, g0, n);
     }
+    if (s < ksteps) one_step<RULE, V, WALL, 0>(q, r, lane, g0, n);
 }
 
 __device__ __forceinline__ int64_t wrap_index(int64_t i, int64_t n, int bmode, int64_t halo)
@@ -87,8 +122,8 @@ __device__ __forceinline__ int64_t wrap_index(int64_t i, int64_t n, int bmode, i
     return i + halo;
 }
 
-template <int RULE, int V>
-__global__ void __launch_bounds__(256) k_blocked(BlockedArgs a, DevRule r)
+template <int RULE, int V, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_blocked(BlockedArgs a, DevRule r)
 {
     static_assert(V % 4 == 0, "V must be a multiple of 4 (int4 vectors)");
     constexpr int W = 32 * V;
@@ -109,8 +144,9 @@ __global__ void __launch_bounds__(256) k_blocked(BlockedArgs a, DevRule r)
         const int64_t ws = w * S - a.KL;               // first cell of the window
         const int64_t g0 = ws + lane * V;              // first cell of this lane
         int32_t q[V];
-        const bool fast = (a.bmode == BM_HALO) ? (ws + W <= n + a.halo)
-                                               : (ws >= 0 && ws + W <= n);
+        const bool aligned = ((b * pstride + base_off) & 3) == 0;   // int4 access possible
+        const bool fast = aligned && ((a.bmode == BM_HALO) ? (ws + W <= n + a.halo)
+                                                            : (ws >= 0 && ws + W <= n));
         if (fast) {
             const int4* s4 = reinterpret_cast<const int4*>(src + base_off + g0);
 #pragma unroll
@@ -134,7 +170,7 @@ __global__ void __launch_bounds__(256) k_blocked(BlockedArgs a, DevRule r)
             const int pos = lane * V + 4 * j;
             if (pos >= lo && pos < hi) {
                 const int64_t gi = ws + pos;
-                if (gi + 4 <= n) {
+                if (aligned && gi + 4 <= n) {
                     int4 v = make_int4(q[4 * j], q[4 * j + 1], q[4 * j + 2], q[4 * j + 3]);
                     *reinterpret_cast<int4*>(dst + base_off + gi) = v;
                 } else {
@@ -197,15 +233,13 @@ __global__ void __launch_bounds__(128) k_warp_ensemble(int32_t* __restrict__ q, 
 #pragma unroll
         for (int j = 0; j < V; ++j) c[j] = qb[j];
     }
-    const int left = (lane + 31) & 31, right = (lane + 1) & 31;
     const int64_t g0 = (int64_t)lane * V;
-    for (int64_t s = 0; s < nsteps; ++s) {
-        int32_t p[V], m[V];
-        eval_maps<RULE, V>(c, p, m, r);
-        int32_t pl = __shfl_sync(FULL, p[V - 1], left);    // periodic wrap inside the warp
-        int32_t mr = __shfl_sync(FULL, m[0], right);
-        step_cells<RULE, V, WALL>(c, p, m, pl, mr, g0, N);
+    int64_t s = 0;
+    for (; s + 2 <= nsteps; s += 2) {
+        one_step<RULE, V, WALL, 1>(c, r, lane, g0, N);
+        one_step<RULE, V, WALL, 1>(c, r, lane, g0, N);
     }
+    if (s < nsteps) one_step<RULE, V, WALL, 1>(c, r, lane, g0, N);
     if (V >= 4) {
 #pragma unroll
         for (int j = 0; j < V / 4; ++j)
@@ -306,24 +340,31 @@ static int grid_for(int64_t work, int threads, int cap)
     return (int)g;
 }
 
-template <int RULE, int V>
+template <int RULE, int V, int MINB>
 static cudaError_t blocked_v(const BlockedArgs& a, const DevRule& r, cudaStream_t st, int cap)
 {
     const int threads = 256;
     int64_t warps = a.nwin * a.batch;
     int g = grid_for(warps * 32, threads, cap);
-    k_blocked<RULE, V><<<g, threads, 0, st>>>(a, r);
+    k_blocked<RULE, V, MINB><<<g, threads, 0, st>>>(a, r);
     return cudaGetLastError();
 }
 
+// minb: __launch_bounds__ min blocks per SM (register cap), 0 = default
 template <int RULE>
-static cudaError_t blocked_rule(int V, const BlockedArgs& a, const DevRule& r, cudaStream_t st,
-                                int cap)
+static cudaError_t blocked_rule(int V, int minb, const BlockedArgs& a, const DevRule& r,
+                                cudaStream_t st, int cap)
 {
+    if (RULE == R_EO_FAST && minb) {
+        if (V == 16 && minb == 3) return blocked_v<RULE, 16, 3>(a, r, st, cap);
+        if (V == 16 && minb == 4) return blocked_v<RULE, 16, 4>(a, r, st, cap);
+        if (V == 32 && minb == 2) return blocked_v<RULE, 32, 2>(a, r, st, cap);
+        if (V == 8 && minb == 4) return blocked_v<RULE, 8, 4>(a, r, st, cap);
+    }
     switch (V) {
-        case 8: return blocked_v<RULE, 8>(a, r, st, cap);
-        case 16: return blocked_v<RULE, 16>(a, r, st, cap);
-        case 32: return blocked_v<RULE, 32>(a, r, st, cap);
+        case 8: return blocked_v<RULE, 8, 1>(a, r, st, cap);
+        case 16: return blocked_v<RULE, 16, 1>(a, r, st, cap);
+        case 32: return blocked_v<RULE, 32, 1>(a, r, st, cap);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -331,13 +372,13 @@ static cudaError_t blocked_rule(int V, const BlockedArgs& a, const DevRule& r, c
 bool blocked_has_V(int V) { return V == 8 || V == 16 || V == 32; }
 int blocked_max_V() { return 32; }
 
-cudaError_t launch_blocked(int rule, int V, const BlockedArgs& a, const DevRule& r,
+cudaError_t launch_blocked(int rule, int V, int minb, const BlockedArgs& a, const DevRule& r,
                            cudaStream_t st, int grid_cap)
 {
     switch (rule) {
-        case R_LIN_HALF: return blocked_rule<R_LIN_HALF>(V, a, r, st, grid_cap);
-        case R_EO_FAST: return blocked_rule<R_EO_FAST>(V, a, r, st, grid_cap);
-        case R_GENERIC: return blocked_rule<R_GENERIC>(V, a, r, st, grid_cap);
+        case R_LIN_HALF: return blocked_rule<R_LIN_HALF>(V, minb, a, r, st, grid_cap);
+        case R_EO_FAST: return blocked_rule<R_EO_FAST>(V, minb, a, r, st, grid_cap);
+        case R_GENERIC: return blocked_rule<R_GENERIC>(V, minb, a, r, st, grid_cap);
         default: return cudaErrorInvalidValue;
     }
 }

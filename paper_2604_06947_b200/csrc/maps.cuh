@@ -9,6 +9,12 @@
 #include <cstdint>
 #include "fqnm_internal.h"
 
+// EO pipe-balance variant (tools/tune_variants.sh): 2 = conversion by IMAD and
+// phi- by LOP3 (measured fastest on B200), 1 = both LOP3, 0 = phi- by IMAD.
+#ifndef FQNM_EO_VARIANT
+#define FQNM_EO_VARIANT 2
+#endif
+
 namespace fqnm {
 
 // round(num/den) for den > 0 in int64 (headroom validated by the planner)
@@ -43,42 +49,83 @@ __device__ __forceinline__ int32_t generic_phi(int32_t q, int64_t c2, int64_t c1
     return (int32_t)round_div_i64(num, den, rounding);
 }
 
-// EO Burgers magnitude g(a) = floor((2P a^2 + Q) / (2Q)), a = |q| < 2^23.
-// 1. est = nearest integer to fl(fl(a*a) * fl(P/Q)) via the 1.5*2^23 magic add
-//    (one rounding inside the FMA); |est - g| <= 1 while kappa a^2 < 2^22.
-// 2. rem = 2P a^2 + Q - 2Q est is computed modulo 2^32 and is exact because
-//    -2Q <= rem < 4Q < 2^31 (Q < 2^29); one correction step in each direction.
-__device__ __forceinline__ int32_t eo_g(int32_t q, const DevRule& r)
+// EO Burgers magnitude g(q) = floor((2P q^2 + Q) / (2Q)) = RHA(kappa q^2),
+// for |q| < 2^22 and kappa q^2 <= 2^20 (proved at plan time):
+// 1. qf = float(q) exactly via the 1.5*2^23 magic (IADD + FADD);
+//    est = rint(fl(qf*qf) * cf) with cf <= kappa (1 - 2^-21) rounded down, done
+//    by one FFMA into the 1.5*2^23 magic: the relative underestimate keeps
+//    est in {g - 1, g} (never above g, at most one below).
+// 2. u = 2Q - 1 - r with r = 2P q^2 + Q - 2Q est, evaluated modulo 2^32 (exact:
+//    0 <= r < 4Q < 2^31); est is one short exactly when r >= 2Q, i.e. u < 0.
+//    Constants: eo_c1 = Q - 1 - 2Q*0x4B400000 (mod 2^32), eo_ntwoP = -2P, eo_twoQ = 2Q.
+__device__ __forceinline__ uint32_t lop3_6c(uint32_t a, uint32_t b, uint32_t c)
 {
-    uint32_t a = (uint32_t)(q < 0 ? -q : q);
-    float af = __int_as_float((int32_t)(0x4B000000u | a)) - 8388608.0f;   // exact, a < 2^23
-    float s = __fmul_rn(af, af);
-    float t = __fmaf_rn(s, r.eo_cf, 12582912.0f);
-    int32_t est = __float_as_int(t) - 0x4B400000;
-    uint32_t a2 = a * a;
-    int32_t rem = (int32_t)(a2 * (uint32_t)r.eo_twoP + (uint32_t)r.eo_Q
-                            - (uint32_t)est * (uint32_t)r.eo_twoQ);
-    est += (rem >> 31);                                    // rem < 0   -> est - 1
-    est += (int32_t)((uint32_t)(r.eo_twoQ - 1 - rem) >> 31);   // rem >= 2Q -> est + 1
-    return est;
+    // d = c ? (a ^ b) : b   (LUT 0x6C with a = 0xF0, b = 0xCC, c = 0xAA)
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0x6C;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+__device__ __forceinline__ int32_t imad(int32_t a, int32_t b, int32_t c)
+{
+    // a*b + c on the FMA pipe (ptxas keeps an IMAD when b is not a known constant)
+    int32_t d;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+// Pipe balance per cell, variant 2: 3 FP32 (FADD, FMUL, FFMA),
+// 5 IMAD (conversion, q^2, 2 x remainder, -K), 5 ALU (LEA.HI, SHF, LOP3, and the
+// step's 2 x IADD3) -> 13 instructions, issue-bound, neither integer pipe saturated.
+__device__ __forceinline__ void eo_gm(int32_t q, int32_t& g, int32_t& m, const DevRule& r)
+{
+    // 0x4B400000 + q for |q| < 2^22 as one LOP3: bits 0..22 of q with bit 22
+    // flipped, exponent/sign bits of 1.5*2^23 above
+#if FQNM_EO_VARIANT == 2
+    const uint32_t x = (uint32_t)imad(q, r.one, 0x4B400000);
+#else
+    const uint32_t x = lop3_6c((uint32_t)q, 0x4B400000u, 0x007FFFFFu);
+#endif
+    const float qf = __int_as_float((int32_t)x) - 12582912.0f;          // exact
+    const float s = __fmul_rn(qf, qf);
+    const float t = __fmaf_rn(s, r.eo_cf, 12582912.0f);                 // 0x4B400000 + est
+    const int32_t bits = __float_as_int(t);
+    const int32_t q2 = imad(q, q, 0);                                    // q^2 mod 2^32
+    int32_t u = imad(q2, r.eo_ntwoP, r.eo_c1);
+    u = imad(bits, r.eo_twoQ, u);                                        // 2Q - 1 - r
+    const int32_t gb = bits + (int32_t)((uint32_t)u >> 31);              // LEA.HI
+    g = imad(gb, r.one, (int32_t)0xB4C00000);                            // - 0x4B400000
+#if FQNM_EO_VARIANT == 0
+    m = imad(g, (int32_t)((uint32_t)q >> 31), 0);                        // phi-(q) = [q<0] g
+#else
+    m = g & (q >> 31);
+#endif
+}
+
+// (g, m) with g = phi+(q) + phi-(q) and m = phi-(q); phi+(q) = g - m.
+// The step uses F_{j+1/2} = phi+(q_j) + phi-(q_{j+1}) = g_j - m_j + m_{j+1} (one IADD3).
+template <int RULE>
+__device__ __forceinline__ void phi_gm(int32_t q, int32_t& g, int32_t& m, const DevRule& r)
+{
+    if (RULE == R_LIN_HALF) {
+        // RHA(q/2) = q - trunc(q/2) for every signed q (C division truncates)
+        g = q - q / 2;
+        m = 0;
+    } else if (RULE == R_EO_FAST) {
+        eo_gm(q, g, m, r);               // phi-(q) = g for q < 0, phi+(q) = g for q > 0, g(0) = 0
+    } else {
+        const int32_t p = generic_phi(q, r.c2p, r.c1p, r.denp, r.suppp, r.rounding);
+        m = generic_phi(q, r.c2m, r.c1m, r.denm, r.suppm, r.rounding);
+        g = p + m;
+    }
 }
 
 template <int RULE>
 __device__ __forceinline__ void phi_pm(int32_t q, int32_t& p, int32_t& m, const DevRule& r)
 {
-    if (RULE == R_LIN_HALF) {
-        // RHA(q/2) = q - trunc(q/2) for every signed q (C division truncates)
-        p = q - q / 2;
-        m = 0;
-    } else if (RULE == R_EO_FAST) {
-        int32_t g = eo_g(q, r);
-        int32_t neg = q >> 31;          // -1 when q < 0
-        m = g & neg;                     // phi-(q) = g for q < 0
-        p = g - m;                       // phi+(q) = g for q > 0 (g(0) = 0)
-    } else {
-        p = generic_phi(q, r.c2p, r.c1p, r.denp, r.suppp, r.rounding);
-        m = generic_phi(q, r.c2m, r.c1m, r.denm, r.suppm, r.rounding);
-    }
+    int32_t g;
+    phi_gm<RULE>(q, g, m, r);
+    p = g - m;
 }
 
 }  // namespace fqnm
