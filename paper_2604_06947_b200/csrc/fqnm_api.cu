@@ -383,7 +383,7 @@ static int choose_kernel(fqnm_plan_t* p)
     }
     if (p->family == 2) {
         const bool two = p->dep_left && p->dep_right;
-        if (p->rule == R_LIN_HALF) { p->V = 32; p->k = 64; }
+        if (p->rule == R_LIN_HALF) { p->V = 32; p->k = 64; p->minb = 2; }
         else if (p->rule == R_EO_FAST) { p->V = 32; p->k = 24; p->minb = 2; }
         else { p->V = 8; p->k = two ? 8 : 16; }
         if (d.k > 0) p->k = d.k;

@@ -122,64 +122,78 @@ __device__ __forceinline__ int64_t wrap_index(int64_t i, int64_t n, int bmode, i
     return i + halo;
 }
 
+// Slow window (periodic wrap, transmissive walls, ragged tails, misaligned
+// batches): scalar loads through wrap_index, guarded scalar stores.  Kept out of
+// line so the hot path's register allocation is not shaped by it.
+template <int RULE, int V>
+__device__ __noinline__ void slow_window(const BlockedArgs& a, const DevRule& r, int64_t b,
+                                         int64_t ws, int lane)
+{
+    constexpr int W = 32 * V;
+    const int64_t n = a.n;
+    const int64_t pstride = (a.bmode == BM_HALO) ? n + 2 * a.halo : n;
+    const int32_t* src = a.src + b * pstride;
+    int32_t* dst = a.dst + b * pstride + ((a.bmode == BM_HALO) ? a.halo : 0);
+    const int64_t g0 = ws + lane * V;
+    int32_t q[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) q[j] = src[wrap_index(g0 + j, n, a.bmode, a.halo)];
+    if (a.bmode == BM_TRANSMISSIVE)
+        run_window_steps<RULE, V, true>(q, a.ksteps, r, g0, n);
+    else
+        run_window_steps<RULE, V, false>(q, a.ksteps, r, g0, n);
+    const int lo = a.KL, hi = W - a.KR;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        const int pos = lane * V + j;
+        const int64_t gi = g0 + j;
+        if (pos >= lo && pos < hi && gi >= 0 && gi < n) dst[gi] = q[j];
+    }
+}
+
 template <int RULE, int V, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_blocked(BlockedArgs a, DevRule r)
 {
     static_assert(V % 4 == 0, "V must be a multiple of 4 (int4 vectors)");
     constexpr int W = 32 * V;
     const int lane = threadIdx.x & 31;
-    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t S = W - a.KL - a.KR;
+    const int S = W - a.KL - a.KR;
+    const int lo = a.KL, hi = W - a.KR;
     const int64_t n = a.n;
-    const int64_t total = a.nwin * a.batch;
-    const int64_t base_off = (a.bmode == BM_HALO) ? a.halo : 0;
-    const int64_t pstride = (a.bmode == BM_HALO) ? n + 2 * a.halo : n;
-
-    for (int64_t wid = gw; wid < total; wid += nwarps) {
-        const int64_t b = wid / a.nwin;
-        const int64_t w = wid - b * a.nwin;
-        const int32_t* src = a.src + b * pstride;
-        int32_t* dst = a.dst + b * pstride;
-        const int64_t ws = w * S - a.KL;               // first cell of the window
-        const int64_t g0 = ws + lane * V;              // first cell of this lane
-        int32_t q[V];
-        const bool aligned = ((b * pstride + base_off) & 3) == 0;   // int4 access possible
-        const bool fast = aligned && ((a.bmode == BM_HALO) ? (ws + W <= n + a.halo)
-                                                            : (ws >= 0 && ws + W <= n));
+    const bool halo = a.bmode == BM_HALO;
+    const int64_t pstride = halo ? n + 2 * a.halo : n;
+    const int64_t lowest = halo ? -a.halo : 0;
+    // window iteration without 64-bit division: (b, w) advanced by nwarps
+    int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t b = 0;
+    while (w >= a.nwin && b < a.batch) { w -= a.nwin; ++b; }
+    while (b < a.batch) {
+        const int64_t ws = w * S - a.KL;                        // first cell of the window
+        const int64_t boff = b * pstride + (halo ? a.halo : 0);
+        const bool fast = ((boff & 3) == 0) && ws >= lowest && ws + W <= n;
         if (fast) {
-            const int4* s4 = reinterpret_cast<const int4*>(src + base_off + g0);
+            const int4* s4 = reinterpret_cast<const int4*>(a.src + boff + ws) + lane * (V / 4);
+            int4* d4 = reinterpret_cast<int4*>(a.dst + boff + ws) + lane * (V / 4);
+            int32_t q[V];
 #pragma unroll
             for (int j = 0; j < V / 4; ++j) {
                 int4 v = __ldg(s4 + j);
                 q[4 * j] = v.x; q[4 * j + 1] = v.y; q[4 * j + 2] = v.z; q[4 * j + 3] = v.w;
             }
-            run_window_steps<RULE, V, false>(q, a.ksteps, r, g0, n);
-        } else {
+            run_window_steps<RULE, V, false>(q, a.ksteps, r, 0, 0);
+            // store the cells whose dependence cone stayed inside the window
 #pragma unroll
-            for (int j = 0; j < V; ++j) q[j] = src[wrap_index(g0 + j, n, a.bmode, a.halo)];
-            if (a.bmode == BM_TRANSMISSIVE)
-                run_window_steps<RULE, V, true>(q, a.ksteps, r, g0, n);
-            else
-                run_window_steps<RULE, V, false>(q, a.ksteps, r, g0, n);
-        }
-        // store the cells whose dependence cone stayed inside the window
-        const int lo = a.KL, hi = W - a.KR;
-#pragma unroll
-        for (int j = 0; j < V / 4; ++j) {
-            const int pos = lane * V + 4 * j;
-            if (pos >= lo && pos < hi) {
-                const int64_t gi = ws + pos;
-                if (aligned && gi + 4 <= n) {
-                    int4 v = make_int4(q[4 * j], q[4 * j + 1], q[4 * j + 2], q[4 * j + 3]);
-                    *reinterpret_cast<int4*>(dst + base_off + gi) = v;
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        if (gi + e < n && gi + e >= 0) dst[base_off + gi + e] = q[4 * j + e];
-                }
+            for (int j = 0; j < V / 4; ++j) {
+                const int pos = lane * V + 4 * j;
+                if (pos >= lo && pos < hi)
+                    d4[j] = make_int4(q[4 * j], q[4 * j + 1], q[4 * j + 2], q[4 * j + 3]);
             }
+        } else {
+            slow_window<RULE, V>(a, r, b, ws, lane);
         }
+        w += nwarps;
+        while (w >= a.nwin && b < a.batch) { w -= a.nwin; ++b; }
     }
 }
 
@@ -355,7 +369,7 @@ template <int RULE>
 static cudaError_t blocked_rule(int V, int minb, const BlockedArgs& a, const DevRule& r,
                                 cudaStream_t st, int cap)
 {
-    if (RULE == R_EO_FAST && minb) {
+    if (minb) {
         if (V == 16 && minb == 3) return blocked_v<RULE, 16, 3>(a, r, st, cap);
         if (V == 16 && minb == 4) return blocked_v<RULE, 16, 4>(a, r, st, cap);
         if (V == 32 && minb == 2) return blocked_v<RULE, 32, 2>(a, r, st, cap);
