@@ -198,9 +198,11 @@ void or_observe(double delta, const int64_t* q, double* u, int64_t n)
 }
 
 /* ---- 5. Euler system: quantised Roe transfer ------------------------------ */
-/* Every statement below is one IEEE binary64 operation, in the order of
- * SURVEY §8(c)-C2 (reading R-ROE).  Compiled with
- * -ffp-contract=off, so no FMA contraction or reassociation happens. */
+/* Every statement below is one IEEE binary64 operation (+ - * / sqrt, all
+ * correctly rounded), in the order of DESIGN.md reading R-ROE-2 (SURVEY
+ * §8(c)-C2 with the divisions by rho, d and a^2 re-pinned as one reciprocal
+ * each, multiplied in; the paper does not fix the arithmetic).
+ * Compiled with -ffp-contract=off, so no FMA contraction or reassociation. */
 
 typedef struct {
     double rho, m, E, u, p, H, r, f0, f1, f2;
@@ -211,13 +213,14 @@ static void or_roe_side(double delta, double g1, const int64_t qc[3], or_side* s
     double rho = delta * (double)qc[0];
     double m = delta * (double)qc[1];
     double E = delta * (double)qc[2];
-    double u = m / rho;
+    double irho = 1.0 / rho;
+    double u = m * irho;
     double mu = m * u;
     double half_mu = 0.5 * mu;
     double e_int = E - half_mu;
     double p = g1 * e_int;
     double Ep = E + p;
-    double H = Ep / rho;
+    double H = Ep * irho;
     double r = sqrt(rho);
     s->rho = rho; s->m = m; s->E = E; s->u = u; s->p = p; s->H = H; s->r = r;
     s->f0 = m;
@@ -254,10 +257,11 @@ void or_roe_transfer(double delta, double s, double g1, const int64_t qL[3],
     or_roe_side(delta, g1, qL, &L);
     or_roe_side(delta, g1, qR, &R);
     double d = L.r + R.r;
+    double id = 1.0 / d;
     double ru_l = L.r * L.u, ru_r = R.r * R.u;
-    double ut = (ru_l + ru_r) / d;
+    double ut = (ru_l + ru_r) * id;
     double rh_l = L.r * L.H, rh_r = R.r * R.H;
-    double Ht = (rh_l + rh_r) / d;
+    double Ht = (rh_l + rh_r) * id;
     double rhot = L.r * R.r;
     double uu = ut * ut;
     double half_uu = 0.5 * uu;
@@ -268,10 +272,11 @@ void or_roe_transfer(double delta, double s, double g1, const int64_t qL[3],
     double dp = R.p - L.p;
     double ra = rhot * at;
     double t = ra * du;
-    double two_a2 = 2.0 * a2;
-    double al1 = (dp - t) / two_a2;
-    double al3 = (dp + t) / two_a2;
-    double dpa = dp / a2;
+    double ia2 = 1.0 / a2;
+    double h_ia2 = 0.5 * ia2;
+    double al1 = (dp - t) * h_ia2;
+    double al3 = (dp + t) * h_ia2;
+    double dpa = dp * ia2;
     double al2 = drho - dpa;
     double l1 = ut - at;
     double l3 = ut + at;

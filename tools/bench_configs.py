@@ -1,0 +1,73 @@
+"""Time every BASELINE.json configuration through the C ABI on one GPU (CUDA
+events, after a warm-up run) and report GCUPS; bench.py's headline is cfg4.
+usage: python tools/bench_configs.py [cfg ...]"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+import torch
+import paper_2604_06947_b200 as F
+import workloads as W
+
+
+def timed(plan, q0, steps, reps=3):
+    q = q0.clone()
+    F.fqnm_step(plan, q, steps)                      # warm-up
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(reps):
+        q.copy_(q0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        F.fqnm_step(plan, q, steps)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    return best, q
+
+
+def main():
+    names = sys.argv[1:] or ["cfg1", "cfg2", "cfg3", "ens1", "cfg5"]
+    for name in names:
+        w = W.cfg(name)
+        if name == "cfg1":
+            q0 = torch.tensor(W.q0_cfg1(), dtype=torch.int32, device="cuda")
+            plan = F.fqnm_plan(w.n, 1e-4, W.dt_dx_double(w), F.LINEAR, F.PERIODIC)
+            steps, cells = w.steps, w.n
+        elif name == "cfg2":
+            q0 = torch.tensor(W.q0_cfg2(), dtype=torch.int32, device="cuda")
+            plan = F.fqnm_plan(w.n, 1e-5, W.dt_dx_double(w, 150000), F.BURGERS_EO, F.PERIODIC)
+            steps, cells = w.steps, w.n
+        elif name == "cfg3":
+            q0 = torch.tensor(W.q0_cfg3(), dtype=torch.int32, device="cuda")
+            plan = F.fqnm_plan(w.n, 1e-6, W.dt_dx_double(w), F.LINEAR, F.PERIODIC)
+            steps, cells = w.steps, w.n
+        elif name == "ens1":
+            q0 = torch.tensor(W.q0_ensemble(w.batch), dtype=torch.int32, device="cuda")
+            plan = F.fqnm_plan_ex(w.n, 1e-4, W.dt_dx_double(w), F.LINEAR, batch=w.batch)
+            steps, cells = w.steps, w.n * w.batch
+        elif name == "cfg5":
+            _, lam = W.sod_steps_and_dt_dx(w.n)
+            q0 = torch.tensor(W.sod_q0(w.n), dtype=torch.int64, device="cuda")
+            plan = F.fqnm_plan(w.n, 1e-7, lam, F.EULER_ROE, F.TRANSMISSIVE)
+            if os.environ.get("EULER_V"):
+                F.fqnm_debug_override(plan, 0, 0, int(os.environ["EULER_V"]))
+            steps, cells = int(os.environ.get("CFG5_STEPS", 2000)), w.n
+        else:
+            raise SystemExit(f"unknown config {name}")
+        ms, q = timed(plan, q0, steps, reps=1 if name == "cfg5" else 3)
+        info = plan.info()
+        print(json.dumps({"config": name, "cells": cells, "steps": steps, "ms": ms,
+                          "GCUPS": cells * steps / ms / 1e6, "kernel": info["kernel"],
+                          "V": info["cells_per_thread"], "k": info["k"]}), flush=True)
+        del q, q0, plan
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
