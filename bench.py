@@ -144,7 +144,7 @@ def run_reference(args):
     q = W.q0_cfg4(n=w.n, count=n_sample).numpy().astype(np.int64)
     qmax = 345000                      # sample only; kappa as for a typical cfg4 Q_max
     rule = oracle.Rule(oracle.BURGERS_EO, w.delta, W.dt_dx(w, qmax))
-    steps_per = 40
+    steps_per = 1000                   # the time steps of one cfg4 bench step
     for _ in range(args.warmup):
         q = rule.run(q, 1)
     times = []

@@ -162,6 +162,10 @@ struct fqnm_plan {
     long long* h_minmax = nullptr;
     void* e2e_dev = nullptr;
     size_t e2e_bytes = 0;
+    int32_t* edges = nullptr;           // K6 resident stepper: halo edges + block-tag flags
+    unsigned int* flags = nullptr;
+    int res_P = 0;
+    uint32_t tag_base = 0;
     cudaStream_t st = nullptr;
     int64_t launches = 0;
     // profiling (fqnm_profile_enable)
@@ -172,6 +176,11 @@ struct fqnm_plan {
 
 static void fill_info(const fqnm_plan_t* p, fqnm_plan_info* info);
 static int plan_build(fqnm_plan_t** out, const fqnm_plan_desc* din, bool allocate);
+
+// K6 geometry: V = 8 (W = 256 cells per warp), H = round4(k) halo cells per side,
+// at most 1184 warps (one 256-thread CTA per SM: always co-resident)
+static const int RESIDENT_MAX_WARPS = 148 * 8;
+static const int64_t RESIDENT_MAX_CELLS = (int64_t)RESIDENT_MAX_WARPS * (256 - 2 * 16);
 
 static size_t elem_size(const fqnm_plan_desc& d) { return d.dtype == FQNM_I64 ? 8 : 4; }
 
@@ -361,6 +370,8 @@ static int build_rule(fqnm_plan_t* p)
 }
 
 // ---------------------------------------------------------------------------
+static int resident_geometry(const fqnm_plan_t* p, int k, int* P, int* base, int* rem, int* H);
+
 static int choose_kernel(fqnm_plan_t* p)
 {
     const fqnm_plan_desc& d = p->d;
@@ -378,6 +389,20 @@ static int choose_kernel(fqnm_plan_t* p)
         p->V = (int)(n / 32);
     } else if (n <= 16384) {
         p->family = 4;
+    } else if (d.batch == 1 && n <= RESIDENT_MAX_CELLS) {
+        p->family = 6;                  // one mid-size problem: whole domain resident on chip
+        p->V = 8;
+        p->k = d.k;
+        if (p->k <= 0) {
+            // deepest halo (fewest L2 exchanges) whose warps still all fit: measured on
+            // cfg2, time per run falls ~1/k up to k = 80 (profiles/r01_summary.md)
+            static const int ks[] = {80, 64, 48, 32, 16};
+            for (int kk : ks) {
+                int P, base, rem, H;
+                p->k = kk;
+                if (resident_geometry(p, kk, &P, &base, &rem, &H) == FQNM_OK) break;
+            }
+        }
     } else {
         p->family = 2;
     }
@@ -393,6 +418,44 @@ static int choose_kernel(fqnm_plan_t* p)
 }
 
 static int round4(int x) { return (x + 3) & ~3; }
+
+
+static int resident_geometry(const fqnm_plan_t* p, int k, int* P, int* base, int* rem, int* H)
+{
+    const int W = 32 * p->V;
+    *H = round4(k);
+    const int S = W - 2 * *H;
+    if (S < *H || S < 4) return FQNM_ERR_ARG;
+    const int64_t n = p->d.n_local;
+    int64_t P64 = (n + S - 1) / S;
+    if (P64 > RESIDENT_MAX_WARPS) return FQNM_ERR_UNSUPPORTED;
+    *P = (int)P64;
+    *base = (int)(n / P64);
+    *rem = (int)(n % P64);
+    if (*base < *H) return FQNM_ERR_ARG;
+    return FQNM_OK;
+}
+
+static int resident_alloc(fqnm_plan_t* p)
+{
+    int P, base, rem, H;
+    int rc = resident_geometry(p, p->k, &P, &base, &rem, &H);
+    if (rc != FQNM_OK)
+        return fail(rc, "resident stepper geometry invalid for n = %lld", (long long)p->d.n_local);
+    const int Hmax = 124;                    // largest halo any allowed k needs
+    // edges sized for the smallest S (largest P) any allowed k produces
+    const int64_t n = p->d.n_local;
+    int64_t Pmax = (n + 4 - 1) / 4;
+    if (Pmax > RESIDENT_MAX_WARPS) Pmax = RESIDENT_MAX_WARPS;
+    if (!p->edges) CUDA_TRY(cudaMalloc(&p->edges, sizeof(int32_t) * 2 * Pmax * 2 * (size_t)Hmax));
+    if (!p->flags) {
+        CUDA_TRY(cudaMalloc(&p->flags, sizeof(unsigned int) * Pmax));
+        CUDA_TRY(cudaMemset(p->flags, 0, sizeof(unsigned int) * Pmax));   // tags start at 1
+        p->tag_base = 1;
+    }
+    p->res_P = (int)Pmax;
+    return FQNM_OK;
+}
 
 // largest steps per block the geometry of V admits
 static int max_block_steps(const fqnm_plan_t* p, int V)
@@ -457,7 +520,11 @@ static int plan_build(fqnm_plan_t** out, const fqnm_plan_desc* din, bool allocat
     }
     // device buffers
     cudaError_t e;
-    if (p->family == 2 || p->family == 1 || p->family == 5) {
+    if (p->family == 6) {
+        int rc6 = resident_alloc(p);
+        if (rc6 != FQNM_OK) { fqnm_destroy(p); return rc6; }
+    }
+    if (p->family == 2 || p->family == 1 || p->family == 5 || p->family == 6) {
         if (d.boundary != FQNM_HALO) {
             p->scratch_bytes = state_elems(p->d) * elem_size(p->d);
             e = cudaMalloc(&p->scratch, p->scratch_bytes);
@@ -513,6 +580,8 @@ extern "C" void fqnm_destroy(fqnm_plan_t* p)
     if (p->d_minmax) cudaFree(p->d_minmax);
     if (p->h_minmax) cudaFreeHost(p->h_minmax);
     if (p->e2e_dev) cudaFree(p->e2e_dev);
+    if (p->edges) cudaFree(p->edges);
+    if (p->flags) cudaFree(p->flags);
     for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
     delete p;
 }
@@ -623,6 +692,26 @@ extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
     }
     if (p->family == 4) {
         PROF_LAUNCH(launch_cta_ensemble(p->rule, (int32_t*)q, n, d.batch, nsteps, bm, p->dr, p->st));
+        return FQNM_OK;
+    }
+    if (p->family == 6) {
+        ResidentArgsHost h;
+        int P, base, rem, H;
+        if ((rc = resident_geometry(p, p->k, &P, &base, &rem, &H)) != FQNM_OK)
+            return fail(rc, "resident stepper: invalid k = %d for n = %lld", p->k, (long long)n);
+        if (P > p->res_P) return fail(FQNM_ERR_ARG, "resident stepper: edge buffers too small");
+        h.src = (const int32_t*)q;
+        h.dst = (int32_t*)p->scratch;
+        h.edges = p->edges;
+        h.flags = p->flags;
+        h.tag_base = p->tag_base;
+        h.n = n;
+        h.nsteps = nsteps;
+        h.P = P; h.base = base; h.rem = rem; h.H = H; h.k = p->k < H ? p->k : H;
+        p->tag_base += (uint32_t)((nsteps + h.k - 1) / h.k) + 1;    // fresh tags for the next call
+        h.bmode = bm;
+        PROF_LAUNCH(launch_resident(p->rule, p->V, h, p->dr, p->st));
+        CUDA_TRY(cudaMemcpyAsync(q, p->scratch, bytes, cudaMemcpyDeviceToDevice, p->st));
         return FQNM_OK;
     }
     // ping-pong families
@@ -809,6 +898,20 @@ extern "C" int fqnm_debug_override(fqnm_plan_t* p, int32_t kernel, int32_t k, in
             p->V = (int)(d.n_local / 32);
         } else if (kernel == 4) {
             if (d.n_local > 16384) return fail(FQNM_ERR_UNSUPPORTED, "CTA ensemble needs n <= 16384");
+        } else if (kernel == 6) {
+            if (d.batch != 1 || d.boundary == FQNM_HALO)
+                return fail(FQNM_ERR_UNSUPPORTED, "resident stepper needs one problem, no split");
+            int P, base, rem, H;
+            const int saveV = p->V, savek = p->k;
+            p->V = (V == 4 || V == 8) ? V : 8;
+            p->k = p->k > 0 && p->k <= 124 ? p->k : 16;
+            int rc6 = resident_geometry(p, p->k, &P, &base, &rem, &H);
+            if (rc6 != FQNM_OK) { p->V = saveV; p->k = savek; return fail(rc6, "resident stepper: n not supported"); }
+            if ((rc6 = resident_alloc(p)) != FQNM_OK) return rc6;
+            if (!p->scratch) {
+                p->scratch_bytes = state_elems(d) * elem_size(d);
+                CUDA_TRY(cudaMalloc(&p->scratch, p->scratch_bytes));
+            }
         } else if (kernel == 1 || kernel == 2) {
             if (!p->scratch && d.boundary != FQNM_HALO) {
                 p->scratch_bytes = state_elems(d) * elem_size(d);
@@ -822,9 +925,19 @@ extern "C" int fqnm_debug_override(fqnm_plan_t* p, int32_t kernel, int32_t k, in
         }
         p->family = kernel;
     }
+    if (V && p->family == 6) {
+        V = 0;                           // consumed above
+    }
     if (V) {
         if (p->family != 2 || !blocked_has_V(V)) return fail(FQNM_ERR_UNSUPPORTED, "V override needs K2 and V in {8,16,32}");
         p->V = V;
+    }
+    if (k && p->family == 6) {
+        int P, base, rem, H;
+        if (k > 124 || resident_geometry(p, k, &P, &base, &rem, &H) != FQNM_OK || P > p->res_P)
+            return fail(FQNM_ERR_ARG, "k = %d not valid for the resident stepper", k);
+        p->k = k;
+        return FQNM_OK;
     }
     if (k) {
         if (p->family != 2) return fail(FQNM_ERR_UNSUPPORTED, "k override needs K2");

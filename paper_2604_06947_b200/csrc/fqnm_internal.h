@@ -58,9 +58,23 @@ struct EulerArgs {
     int32_t bmode;
 };
 
+struct ResidentArgsHost {
+    const int32_t* src;
+    int32_t* dst;
+    int32_t* edges;              // halo edges [2][P][2][H]
+    unsigned int* flags;         // [P] block tags
+    int64_t n, nsteps;
+    int32_t P, base, rem, H, k, bmode;
+    uint32_t tag_base;           // tags strictly increase across calls of one plan
+};
+
+int resident_capacity_warps(int rule, int V);   // 0 if unavailable (no GPU)
+
 // kernel launchers (kernels_scalar.cu / kernels_euler.cu); return cudaError_t
 cudaError_t launch_blocked(int rule, int V, int minb, const BlockedArgs& a, const DevRule& r,
                            cudaStream_t st, int grid_cap);
+cudaError_t launch_resident(int rule, int V, const ResidentArgsHost& h, const DevRule& r,
+                            cudaStream_t st);
 cudaError_t launch_naive(int rule, const int32_t* src, int32_t* dst, int64_t n, int64_t batch,
                          int bmode, const DevRule& r, cudaStream_t st);
 cudaError_t launch_warp_ensemble(int rule, int V, int32_t* q, int64_t batch, int64_t nsteps,

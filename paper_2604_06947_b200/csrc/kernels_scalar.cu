@@ -23,6 +23,10 @@
 #include "fqnm_internal.h"
 #include "maps.cuh"
 
+#ifndef FQNM_RES_FENCE
+#define FQNM_RES_FENCE 0
+#endif
+
 namespace fqnm {
 
 static constexpr unsigned FULL = 0xffffffffu;
@@ -222,6 +226,103 @@ __global__ void k_naive(const int32_t* __restrict__ src, int32_t* __restrict__ d
         phi_pm<RULE>(s[ir], pr, mr, r);
         const int32_t Fr = pc + mr, Fl = pl + mc;
         dst[b * n + i] = s[i] - (Fr - Fl);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K6: resident stepper for one mid-size problem (e.g. BJ.cfg2, N = 65536).
+// The domain is split over P warps; warp w owns S_w cells, held with H halo
+// cells on each side in a register window of 32*V cells, for ALL nsteps.
+// After every block of k <= H steps each warp publishes its H edge cells to
+// global memory (double-buffered by block parity: a neighbour can be at most
+// one block ahead), raises its flag (release) and waits for both neighbours'
+// flags (acquire) before reloading its halos through L2 - no grid-wide
+// barrier, no relaunch.  All warps must be co-resident: the launcher uses a
+// cooperative launch.  Flags carry tag_base + block, strictly increasing across
+// calls, so they never need resetting.
+struct ResidentArgs {
+    const int32_t* src;
+    int32_t* dst;
+    int32_t* edges;           // [2 parities][P][2 sides][H]
+    unsigned int* flags;      // [P]
+    int64_t n;
+    int64_t nsteps;
+    int32_t P, base, rem, H, k, bmode;   // warp w owns base + (w < rem) cells
+    uint32_t tag_base;
+};
+
+template <int RULE, int V>
+__global__ void __launch_bounds__(256) k_resident(ResidentArgs a, DevRule r)
+{
+    const int lane = threadIdx.x & 31;
+    const int w = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (w >= a.P) return;                              // whole warps only
+    const int H = a.H;
+    const int64_t own0 = (int64_t)w * a.base + (w < a.rem ? w : a.rem);   // first owned cell
+    const int Sw = a.base + (w < a.rem ? 1 : 0);
+    const int64_t ws = own0 - H;                       // window start (global index)
+    const bool wall = a.bmode == BM_TRANSMISSIVE;
+    const int wl = (w + a.P - 1) % a.P, wr = (w + 1) % a.P;
+    int32_t q[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        const int pos = lane * V + j;
+        int64_t gi = ws + pos;
+        if (pos >= H + Sw + H) gi = own0;              // beyond the window's use: any valid state
+        if (wall) gi = gi < 0 ? 0 : (gi >= a.n ? a.n - 1 : gi);
+        else gi = ((gi % a.n) + a.n) % a.n;
+        q[j] = a.src[gi];
+    }
+    int64_t done = 0;
+    uint32_t blk = 0;
+    while (done < a.nsteps) {
+        const int kb = (int)((a.nsteps - done) < a.k ? (a.nsteps - done) : a.k);
+        if (wall)
+            run_window_steps<RULE, V, true>(q, kb, r, ws + (int64_t)lane * V, a.n);
+        else
+            run_window_steps<RULE, V, false>(q, kb, r, 0, 0);
+        done += kb;
+        if (done >= a.nsteps) break;
+        ++blk;
+        const uint32_t tag = a.tag_base + blk;
+        // publish the edges: left = positions [H, 2H), right = [Sw, Sw + H)
+        int32_t* e = a.edges + ((size_t)(blk & 1) * a.P + w) * 2 * H;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const int pos = lane * V + j;
+            if (pos >= H && pos < 2 * H) e[pos - H] = q[j];
+            if (pos >= Sw && pos < Sw + H) e[H + pos - Sw] = q[j];
+        }
+        __syncwarp();
+        if (lane == 0) {
+#if FQNM_RES_FENCE == 0
+            __threadfence();
+#else
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(a.flags + w), "r"(tag) : "memory");
+            unsigned int f;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(a.flags + wl) : "memory");
+            } while ((int)(f - tag) < 0);
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(a.flags + wr) : "memory");
+            } while ((int)(f - tag) < 0);
+        }
+        __syncwarp();
+        const int32_t* el = a.edges + ((size_t)(blk & 1) * a.P + wl) * 2 * H + H;   // left nbr's right edge
+        const int32_t* er = a.edges + ((size_t)(blk & 1) * a.P + wr) * 2 * H;       // right nbr's left edge
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const int pos = lane * V + j;
+            if (pos < H) q[j] = __ldcg(el + pos);
+            else if (pos >= H + Sw && pos < H + Sw + H) q[j] = __ldcg(er + pos - H - Sw);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        const int pos = lane * V + j;
+        if (pos >= H && pos < H + Sw) a.dst[ws + pos] = q[j];
     }
 }
 
@@ -435,6 +536,58 @@ static cudaError_t warp_rule(int V, int32_t* q, int64_t batch, int64_t nsteps, i
         case 8: return warp_v<RULE, 8>(q, batch, nsteps, bmode, r, st);
         case 16: return warp_v<RULE, 16>(q, batch, nsteps, bmode, r, st);
         case 32: return warp_v<RULE, 32>(q, batch, nsteps, bmode, r, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <int RULE, int V>
+static cudaError_t resident_v(const ResidentArgsHost& h, const DevRule& r, cudaStream_t st)
+{
+    ResidentArgs a;
+    a.src = h.src; a.dst = h.dst; a.edges = h.edges; a.flags = h.flags; a.n = h.n;
+    a.tag_base = h.tag_base;
+    a.nsteps = h.nsteps; a.P = h.P; a.base = h.base; a.rem = h.rem; a.H = h.H; a.k = h.k;
+    a.bmode = h.bmode;
+    const int threads = 256;
+    const int blocks = (h.P * 32 + threads - 1) / threads;
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<RULE, V>,
+                                                                  threads, 0);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    if (blocks > per_sm * sms) return cudaErrorCooperativeLaunchTooLarge;
+    void* args[] = {&a, const_cast<DevRule*>(&r)};
+    return cudaLaunchCooperativeKernel((const void*)k_resident<RULE, V>, blocks, threads, args, 0, st);
+}
+
+int resident_capacity_warps(int rule, int V)
+{
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaError_t e;
+    if (V == 8) {
+        e = rule == R_LIN_HALF ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_LIN_HALF, 8>, 256, 0)
+          : rule == R_EO_FAST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_EO_FAST, 8>, 256, 0)
+          : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_GENERIC, 8>, 256, 0);
+    } else {
+        e = rule == R_LIN_HALF ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_LIN_HALF, 4>, 256, 0)
+          : rule == R_EO_FAST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_EO_FAST, 4>, 256, 0)
+          : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_GENERIC, 4>, 256, 0);
+    }
+    if (e != cudaSuccess) return 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+    return per_sm * sms * 8;
+}
+
+cudaError_t launch_resident(int rule, int V, const ResidentArgsHost& h, const DevRule& r,
+                            cudaStream_t st)
+{
+    if (V != 8 && V != 4) return cudaErrorInvalidValue;
+    switch (rule) {
+        case R_LIN_HALF: return V == 8 ? resident_v<R_LIN_HALF, 8>(h, r, st) : resident_v<R_LIN_HALF, 4>(h, r, st);
+        case R_EO_FAST: return V == 8 ? resident_v<R_EO_FAST, 8>(h, r, st) : resident_v<R_EO_FAST, 4>(h, r, st);
+        case R_GENERIC: return V == 8 ? resident_v<R_GENERIC, 8>(h, r, st) : resident_v<R_GENERIC, 4>(h, r, st);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -75,6 +75,8 @@ def test_rule_and_kernel_selection(F):
     assert info["kernel"] == 3 and info["cells_per_thread"] == 32
     info = F.fqnm_plan_validate(1000, 1e-4, 0.5, F.LINEAR)
     assert info["kernel"] == 4
+    info = F.fqnm_plan_validate(65536, 1e-5, 4 / 15, F.BURGERS_EO)      # cfg2: resident stepper
+    assert info["kernel"] == 6
     info = F.fqnm_plan_validate(1 << 26, 1e-7, 0.3, F.EULER_ROE, F.TRANSMISSIVE)
     assert info["kernel"] == 5 and info["s_euler"] == 0.3 / 1e-7 and info["g1_euler"] == 1.4 - 1.0
 

@@ -239,7 +239,7 @@ def test_all_families_match_oracle(F, case, boundary, n):
         ref = rule.run(q0, nsteps, boundary)
         fams = [0, 1]
         if n >= 64:
-            fams.append(2)
+            fams += [2, 6]
         if n <= 16384:
             fams.append(4)
         if n % 32 == 0 and n // 32 in (1, 2, 4, 8, 16, 32):
@@ -273,6 +273,29 @@ def test_blocked_k_and_v(F, V, k, case):
     q = to_dev(q0)
     F.fqnm_step(plan, q, 100)
     assert np.array_equal(host(q), ref)
+
+
+@pytest.mark.parametrize("k", [1, 5, 16, 40, 124])
+@pytest.mark.parametrize("boundary", [W.PERIODIC, W.TRANSMISSIVE])
+def test_resident_stepper_k(F, k, boundary):
+    """K6 (whole problem resident, halo exchange through L2 with flags) for
+    several block lengths; nsteps not a multiple of k."""
+    kind, delta, lam, param, amp, off = CASES[1]
+    for n in (65536, 70001, 250000):
+        rng = np.random.default_rng(n + k)
+        q0 = W.smooth_random(rng, n, amp, off)
+        ref = oracle.Rule(kind, delta, lam).run(q0, 301, boundary)
+        plan = F.fqnm_plan_ex(n, float(Fraction(delta)), float(lam), kind, boundary)
+        F.fqnm_debug_override(plan, 6)
+        try:
+            F.fqnm_debug_override(plan, 0, k, 0)
+        except F.FqnmError:
+            assert n * 2 * (k + 3) // 4 * 4 > 148 * 8 * 64      # only when the warps would not fit
+            continue
+        assert plan.info()["kernel"] == 6
+        q = to_dev(q0)
+        F.fqnm_step(plan, q, 301)
+        assert np.array_equal(host(q), ref), n
 
 
 def test_batched_blocked_and_cta(F):

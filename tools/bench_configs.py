@@ -42,6 +42,9 @@ def main():
         elif name == "cfg2":
             q0 = torch.tensor(W.q0_cfg2(), dtype=torch.int32, device="cuda")
             plan = F.fqnm_plan(w.n, 1e-5, W.dt_dx_double(w, 150000), F.BURGERS_EO, F.PERIODIC)
+            if os.environ.get("CFG2_K") or os.environ.get("CFG2_V"):
+                F.fqnm_debug_override(plan, 6, int(os.environ.get("CFG2_K", 16)),
+                                      int(os.environ.get("CFG2_V", 8)))
             steps, cells = w.steps, w.n
         elif name == "cfg3":
             q0 = torch.tensor(W.q0_cfg3(), dtype=torch.int32, device="cuda")
