@@ -99,6 +99,20 @@ class Clocks:
         return out
 
 
+def ncu_traffic(n_local: int):
+    """Per-launch DRAM bytes of the dominant kernel from the latest committed
+    `ncu --set full` capture (profiles/*_bench_kernel_ncu.json, written by
+    tools/ncu_traffic.py), scaled to this run's cells per launch."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_bench_kernel_ncu.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as f:
+        cap = json.load(f)
+    scale = n_local / float(1 << 31)           # the capture is of the N = 2^31 bench launch
+    return cap["dram_bytes_per_launch"] * scale, os.path.relpath(files[-1], ROOT)
+
+
 def init_dist():
     import torch
     import torch.distributed as dist
@@ -281,12 +295,20 @@ def main():
         "ops_alg_per_cell_update": OPS_ALG["burgers_eo"],
         "peak_basis": "148 SMs x 128 int lanes/clk x sm_max_mhz (%s)" % peak_src,
         "traffic": None,
+        "traffic_source": None,
+        "algorithmic_bytes_per_launch": hbm_bytes_per_launch,
         "kernel_ms_per_launch": per_launch_ms, "kernel_launches": kern_launches,
         "kernel_share_of_step": kern_ms / ms if ms > 0 else None,
         "hbm_achieved_gbs": hbm_bytes_per_launch / (per_launch_ms / 1e3) / 1e9,
         "hbm_peak_gbs": float(peaks.get("hbm_gbs", 6650.0)),
         "k": info["k"], "V": info["cells_per_thread"],
     }
+
+    tr, tr_src = ncu_traffic(n_local)
+    if tr is not None:
+        roofline["traffic"] = tr
+        roofline["traffic_source"] = tr_src
+        roofline["traffic_over_algorithmic"] = tr / hbm_bytes_per_launch
 
     # ---- end-to-end through the public API with host buffers (H2D + steps + D2H) ----
     e2e = None
