@@ -86,6 +86,11 @@ def lib():
                                     ctypes.c_int64, P64, P64]
         L.or_run_euler.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                    ctypes.c_int64, P64, ctypes.c_int64, ctypes.c_int]
+        L.or_step_euler_density.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                            ctypes.c_double, ctypes.c_int64, P64, P64]
+        L.or_run_euler_density.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                           ctypes.c_double, ctypes.c_int64, P64, ctypes.c_int64,
+                                           ctypes.c_int]
         L.or_round_rational.restype = ctypes.c_int64
         L.or_round_rational.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64,
                                         ctypes.c_int]
@@ -199,6 +204,38 @@ def euler_run(q, nsteps: int, delta: float, dt_dx: float, gamma: float = 1.4,
     q = np.array(q, dtype=np.int64, copy=True, order="C")
     s, g1 = euler_constants(delta, dt_dx, gamma)
     lib().or_run_euler(delta, s, g1, q.shape[1], _p64(q), nsteps, nthreads)
+    return q
+
+
+def pack_mixed(q_rho, m, E) -> np.ndarray:
+    """[3][N] int64 buffer of the density-only variant: q_rho, then the float64 bit
+    patterns of m and E."""
+    out = np.empty((3, len(q_rho)), dtype=np.int64)
+    out[0] = q_rho
+    out[1] = np.asarray(m, dtype=np.float64).view(np.int64)
+    out[2] = np.asarray(E, dtype=np.float64).view(np.int64)
+    return out
+
+
+def unpack_mixed(q):
+    q = np.ascontiguousarray(q, dtype=np.int64)
+    return q[0].copy(), q[1].view(np.float64).copy(), q[2].view(np.float64).copy()
+
+
+def euler_density_step(q, delta: float, dt_dx: float, gamma: float = 1.4) -> np.ndarray:
+    q = np.ascontiguousarray(q, dtype=np.int64)
+    s, g1 = euler_constants(delta, dt_dx, gamma)
+    out = np.empty_like(q)
+    lib().or_step_euler_density(delta, s, dt_dx, g1, q.shape[1], _p64(q), _p64(out))
+    return out
+
+
+def euler_density_run(q, nsteps: int, delta: float, dt_dx: float, gamma: float = 1.4,
+                      nthreads: int = 0) -> np.ndarray:
+    """Density-only quantised Euler (the paper's Sod prototype)."""
+    q = np.array(q, dtype=np.int64, copy=True, order="C")
+    s, g1 = euler_constants(delta, dt_dx, gamma)
+    lib().or_run_euler_density(delta, s, dt_dx, g1, q.shape[1], _p64(q), nsteps, nthreads)
     return q
 
 

@@ -208,11 +208,8 @@ typedef struct {
     double rho, m, E, u, p, H, r, f0, f1, f2;
 } or_side;
 
-static void or_roe_side(double delta, double g1, const int64_t qc[3], or_side* s)
+static void or_roe_side_d(double g1, double rho, double m, double E, or_side* s)
 {
-    double rho = delta * (double)qc[0];
-    double m = delta * (double)qc[1];
-    double E = delta * (double)qc[2];
     double irho = 1.0 / rho;
     double u = m * irho;
     double mu = m * u;
@@ -226,6 +223,11 @@ static void or_roe_side(double delta, double g1, const int64_t qc[3], or_side* s
     s->f0 = m;
     s->f1 = mu + p;
     s->f2 = u * Ep;
+}
+
+static void or_roe_side(double delta, double g1, const int64_t qc[3], or_side* s)
+{
+    or_roe_side_d(g1, delta * (double)qc[0], delta * (double)qc[1], delta * (double)qc[2], s);
 }
 
 /* round-half-away-from-zero of a double (reading A1): exact because
@@ -249,13 +251,10 @@ static double or_harten(double l, double eps)
     return num / den;
 }
 
-/* T^c(qL, qR) = RHA(fl(F^c_Roe(delta qL, delta qR) * s)), s = fl(dt/dx / delta). */
-void or_roe_transfer(double delta, double s, double g1, const int64_t qL[3],
-                     const int64_t qR[3], int64_t T[3])
+/* Roe flux F^c(L, R) of two physical states (R-ROE-2 operation order). */
+static void or_roe_flux(double g1, const or_side* Lp, const or_side* Rp, double F[3])
 {
-    or_side L, R;
-    or_roe_side(delta, g1, qL, &L);
-    or_roe_side(delta, g1, qR, &R);
+    or_side L = *Lp, R = *Rp;
     double d = L.r + R.r;
     double id = 1.0 / d;
     double ru_l = L.r * L.u, ru_r = R.r * R.u;
@@ -296,8 +295,21 @@ void or_roe_transfer(double delta, double s, double g1, const int64_t qL[3],
         double w2 = c2 * r2[c];
         double D = (w1 + w3) + w2;
         double avg = 0.5 * (fL[c] + fR[c]);
-        double F = avg - 0.5 * D;
-        double x = F * s;
+        F[c] = avg - 0.5 * D;
+    }
+}
+
+/* T^c(qL, qR) = RHA(fl(F^c_Roe(delta qL, delta qR) * s)), s = fl(dt/dx / delta). */
+void or_roe_transfer(double delta, double s, double g1, const int64_t qL[3],
+                     const int64_t qR[3], int64_t T[3])
+{
+    or_side L, R;
+    double F[3];
+    or_roe_side(delta, g1, qL, &L);
+    or_roe_side(delta, g1, qR, &R);
+    or_roe_flux(g1, &L, &R, F);
+    for (int c = 0; c < 3; ++c) {
+        double x = F[c] * s;
         T[c] = or_rha_double(x);
     }
 }
@@ -320,6 +332,63 @@ void or_step_euler(double delta, double s, double g1, int64_t N,
         for (int c = 0; c < 3; ++c)
             out[c * N + i] = qi[c] - (Tr[c] - Tl[c]);
     }
+}
+
+/* Density-only quantisation (the paper's Sod prototype; DESIGN.md
+ * reading A9-D): cell state (q_rho int64, m double, E double) in SoA [3][N]
+ * (components 1 and 2 stored as IEEE doubles).  rho = delta q_rho enters the
+ * same Roe flux; the density moves by integer transfers T = RHA(fl(F^rho s)),
+ * momentum and energy by the classical float64 update
+ * m' = fl(m - fl(lam fl(F^m_{i+1/2} - F^m_{i-1/2}))) (likewise E), transmissive. */
+static void or_side_mixed(double delta, double g1, const int64_t* q, int64_t N, int64_t i,
+                          or_side* s)
+{
+    double m, E;
+    memcpy(&m, &q[N + i], 8);
+    memcpy(&E, &q[2 * N + i], 8);
+    or_roe_side_d(g1, delta * (double)q[i], m, E, s);
+}
+
+void or_step_euler_density(double delta, double s, double lam, double g1, int64_t N,
+                           const int64_t* q, int64_t* out)
+{
+    #pragma omp parallel for schedule(static) if (N >= 32768)
+    for (int64_t i = 0; i < N; ++i) {
+        int64_t im = i > 0 ? i - 1 : 0;
+        int64_t ip = i < N - 1 ? i + 1 : N - 1;
+        or_side Sm, Si, Sp;
+        or_side_mixed(delta, g1, q, N, im, &Sm);
+        or_side_mixed(delta, g1, q, N, i, &Si);
+        or_side_mixed(delta, g1, q, N, ip, &Sp);
+        double Fl[3], Fr[3];
+        or_roe_flux(g1, &Sm, &Si, Fl);
+        or_roe_flux(g1, &Si, &Sp, Fr);
+        int64_t Tl = or_rha_double(Fl[0] * s), Tr = or_rha_double(Fr[0] * s);
+        out[i] = q[i] - (Tr - Tl);
+        double m, E;
+        memcpy(&m, &q[N + i], 8);
+        memcpy(&E, &q[2 * N + i], 8);
+        double dm = Fr[1] - Fl[1];
+        double dE = Fr[2] - Fl[2];
+        double m2 = m - lam * dm;
+        double E2 = E - lam * dE;
+        memcpy(&out[N + i], &m2, 8);
+        memcpy(&out[2 * N + i], &E2, 8);
+    }
+}
+
+void or_run_euler_density(double delta, double s, double lam, double g1, int64_t N, int64_t* q,
+                          int64_t nsteps, int nthreads)
+{
+    set_threads(nthreads);
+    int64_t* a = q;
+    int64_t* b = (int64_t*)malloc(sizeof(int64_t) * 3 * (size_t)N);
+    for (int64_t k = 0; k < nsteps; ++k) {
+        or_step_euler_density(delta, s, lam, g1, N, a, b);
+        int64_t* t = a; a = b; b = t;
+    }
+    if (a != q) { memcpy(q, a, sizeof(int64_t) * 3 * (size_t)N); b = a; }
+    free(b);
 }
 
 void or_run_euler(double delta, double s, double g1, int64_t N, int64_t* q,

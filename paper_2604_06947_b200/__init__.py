@@ -22,11 +22,11 @@ __all__ = [
     "fqnm_observe", "fqnm_step_host", "fqnm_get_info", "fqnm_transfer", "fqnm_transfer_device",
     "fqnm_roe_transfer_device", "fqnm_debug_override", "fqnm_launch_count", "fqnm_destroy",
     "fqnm_plan_validate", "fqnm_profile_enable", "fqnm_profile_read",
-    "LINEAR", "BURGERS_EO", "BURGERS_LF", "EULER_ROE", "PERIODIC", "TRANSMISSIVE", "HALO",
+    "LINEAR", "BURGERS_EO", "BURGERS_LF", "EULER_ROE", "EULER_ROE_DENSITY", "PERIODIC", "TRANSMISSIVE", "HALO",
     "I32", "I64", "ROUND_HALF_AWAY", "ROUND_FLOOR", "ROUND_HALF_EVEN", "lib_path",
 ]
 
-LINEAR, BURGERS_EO, BURGERS_LF, EULER_ROE = 0, 1, 2, 3
+LINEAR, BURGERS_EO, BURGERS_LF, EULER_ROE, EULER_ROE_DENSITY = 0, 1, 2, 3, 4
 PERIODIC, TRANSMISSIVE, HALO = 0, 1, 2
 I32, I64 = 0, 1
 ROUND_HALF_AWAY, ROUND_FLOOR, ROUND_HALF_EVEN = 0, 1, 2
@@ -205,9 +205,9 @@ def fqnm_plan(N: int, delta: float, dt_dx: float, flux_kind: int = LINEAR,
     L.fqnm_desc_init(ctypes.byref(d))
     d.n_local = d.n_global = N
     d.delta, d.dt_dx, d.flux_kind, d.boundary = delta, dt_dx, flux_kind, boundary
-    if flux_kind == EULER_ROE:
+    if flux_kind in (EULER_ROE, EULER_ROE_DENSITY):
         d.nvar, d.dtype = 3, I64
-    d.check_range = 1 if flux_kind != EULER_ROE else 0
+    d.check_range = 1 if flux_kind not in (EULER_ROE, EULER_ROE_DENSITY) else 0
     return Plan(h, d)
 
 
@@ -220,7 +220,7 @@ def make_desc(n_local: int, delta: float, dt_dx: float, flux_kind: int = LINEAR,
     L = _load()
     d = PlanDesc()
     L.fqnm_desc_init(ctypes.byref(d))
-    euler = flux_kind == EULER_ROE
+    euler = flux_kind in (EULER_ROE, EULER_ROE_DENSITY)
     d.n_local = n_local
     d.n_global = n_global or n_local
     d.offset = offset

@@ -485,7 +485,7 @@ static int plan_build(fqnm_plan_t** out, const fqnm_plan_desc* din, bool allocat
     p->d.n_global = d.n_global ? d.n_global : d.n_local;
     p->st = (cudaStream_t)d.stream;
     int rc;
-    if (d.flux_kind == FQNM_EULER_ROE) {
+    if (d.flux_kind == FQNM_EULER_ROE || d.flux_kind == FQNM_EULER_ROE_DENSITY) {
         if (d.nvar != 3 || d.dtype != FQNM_I64) {
             delete p;
             return fail(FQNM_ERR_ARG, "Euler plans need nvar = 3 and dtype = FQNM_I64");
@@ -563,7 +563,7 @@ extern "C" int fqnm_plan(fqnm_plan_t** out, int64_t N, double delta, double dt_d
     d.check_range = 1;
     if (boundary != FQNM_PERIODIC && boundary != FQNM_TRANSMISSIVE)
         return fail(FQNM_ERR_ARG, "fqnm_plan: boundary must be PERIODIC or TRANSMISSIVE");
-    if (flux_kind == FQNM_EULER_ROE) {
+    if (flux_kind == FQNM_EULER_ROE || flux_kind == FQNM_EULER_ROE_DENSITY) {
         d.nvar = 3;
         d.dtype = FQNM_I64;
         d.flux_param = 1.4;
@@ -732,6 +732,8 @@ extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
                 a.delta = d.delta;
                 a.s = p->s_e;
                 a.g1 = p->g1_e;
+                a.lam = d.dt_dx;
+                a.mode = d.flux_kind == FQNM_EULER_ROE_DENSITY ? 1 : 0;
                 a.bmode = bm;
                 PROF_LAUNCH(launch_euler(p->V, a, p->st));
             }
@@ -767,6 +769,19 @@ extern "C" int fqnm_step_block(fqnm_plan_t* p, const void* src, void* dst, int32
 extern "C" int fqnm_observe(const fqnm_plan_t* p, const void* q, double* u)
 {
     if (!p || !q || !u) return fail(FQNM_ERR_ARG, "null argument");
+    if (p->d.flux_kind == FQNM_EULER_ROE_DENSITY) {
+        // density: u = delta q; momentum and energy are already float64 (bit copy)
+        const int64_t n = p->d.n_local;
+        for (int64_t b = 0; b < p->d.batch; ++b) {
+            const int64_t* qb = (const int64_t*)q + b * 3 * n;
+            double* ub = u + b * 3 * n;
+            CUDA_TRY(launch_observe(qb, FQNM_I64, p->d.delta, ub, n, p->st));
+            const_cast<fqnm_plan_t*>(p)->launches++;
+            CUDA_TRY(cudaMemcpyAsync(ub + n, qb + n, 2 * n * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, p->st));
+        }
+        return FQNM_OK;
+    }
     CUDA_TRY(launch_observe(q, p->d.dtype, p->d.delta, u, (int64_t)state_elems(p->d), p->st));
     const_cast<fqnm_plan_t*>(p)->launches++;
     return FQNM_OK;

@@ -55,7 +55,9 @@ struct EulerArgs {
     int64_t batch;
     int64_t nwin;
     double delta, s, g1;
+    double lam;         // dt/dx (density-only variant: float update of m and E)
     int32_t bmode;
+    int32_t mode;       // 0: all components quanta, 1: density-only quantisation
 };
 
 struct ResidentArgsHost {

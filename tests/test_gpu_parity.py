@@ -379,3 +379,42 @@ def test_profile_hooks(F):
     ms, nl = F.fqnm_profile_read(plan)
     assert nl >= 1 and ms > 0
     assert plan.launches() - before >= nl
+
+
+# ---------------------------------------------------------------------------
+# density-only quantisation (the paper's Sod prototype; NEXT-f2)
+def _sod_mixed(n, delta=1e-7):
+    q = W.sod_q0(n, Fraction(str(delta)))
+    E = np.where(np.arange(n) < n // 2, 1.0 / 0.4, 0.1 / 0.4)
+    return oracle.pack_mixed(q[0], np.zeros(n), E)
+
+
+def test_density_only_sod_full_and_observe(F):
+    n = 1024
+    nsteps, lam = W.sod_steps_and_dt_dx(n)
+    q0 = _sod_mixed(n)
+    plan = F.fqnm_plan(n, 1e-7, lam, F.EULER_ROE_DENSITY, F.TRANSMISSIVE)
+    q = to_dev(q0, torch.int64)
+    F.fqnm_step(plan, q, nsteps)
+    ref = oracle.euler_density_run(q0, nsteps, 1e-7, lam)
+    assert np.array_equal(q.cpu().numpy(), ref)
+    u = F.fqnm_observe(plan, q).cpu().numpy().reshape(3, n)
+    r, m, E = oracle.unpack_mixed(ref)
+    assert np.array_equal(u[0], oracle.observe(r, 1e-7))
+    assert np.array_equal(u[1], m) and np.array_equal(u[2], E)
+
+
+def test_density_only_full_size_windows(F):
+    n = W.cfg("cfg5").n
+    S = 150
+    _, lam = W.sod_steps_and_dt_dx(n)
+    q0 = _sod_mixed(n)
+    plan = F.fqnm_plan(n, 1e-7, lam, F.EULER_ROE_DENSITY, F.TRANSMISSIVE)
+    q = to_dev(q0, torch.int64)
+    F.fqnm_step(plan, q, S)
+    qh = q.cpu().numpy()
+    assert qh[0].sum() == q0[0].sum()
+    for a, b in [(0, 2048), (n - 2048, n), (n // 2 - 1024, n // 2 + 1024)]:
+        lo, hi = max(0, a - S), min(n, b + S)
+        ref = oracle.euler_density_run(np.ascontiguousarray(q0[:, lo:hi]), S, 1e-7, lam)
+        assert np.array_equal(qh[:, a:b], ref[:, a - lo:b - lo]), (a, b)
