@@ -192,6 +192,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1: fused peer-memory halo exchange inside the kernel (p2p) "
+                         "or torch.distributed NCCL send/recv between launches")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -203,6 +206,7 @@ def main():
     import workloads as W
 
     rank, world, local = init_dist()
+    halo_mode = "none"
     dev = torch.device("cuda", local)
     w = W.cfg("cfg4")
     N = args.n
@@ -229,17 +233,37 @@ def main():
     else:
         probe = F.fqnm_plan_validate(N, 1e-6, dt_dx, F.BURGERS_EO)
         k = probe["k"]
-        plan = F.fqnm_plan_ex(n_local, 1e-6, dt_dx, F.BURGERS_EO, F.HALO, halo=k, n_global=N,
-                              offset=off)
+        halo_mode = args.halo
+        ring = None
+        if halo_mode == "p2p":
+            ring, why = halo.P2PRing.distributed(
+                lambda: F.fqnm_plan_ex(n_local, 1e-6, dt_dx, F.BURGERS_EO, F.HALO, halo=k,
+                                       n_global=N, offset=off, p2p=True), None, dev)
+            if ring is None:                         # no peer access somewhere: NCCL for all
+                if rank == 0:
+                    print(f"[bench] p2p halo unavailable ({why}); using nccl", file=sys.stderr)
+                halo_mode = "nccl"
+            else:
+                plan = ring.plans[0]
+                ring.load([q])
+        if halo_mode == "nccl":
+            plan = F.fqnm_plan_ex(n_local, 1e-6, dt_dx, F.BURGERS_EO, F.HALO, halo=k,
+                                  n_global=N, offset=off)
+            sd = halo.SplitDomain([n_local], k, halo.DistTransport(), [plan.step_block],
+                                  lambda m: torch.zeros(m, dtype=torch.int32, device=dev))
+            sd.load([q])
         info = plan.info()
-        sd = halo.SplitDomain([n_local], k, halo.DistTransport(), [plan.step_block],
-                              lambda m: torch.zeros(m, dtype=torch.int32, device=dev))
-        sd.load([q])
         del q
         torch.cuda.empty_cache()
 
+        def owned():
+            return ring.owned(0) if ring is not None else sd.owned(0)
+
         def do_step():
-            sd.step(T)
+            if ring is not None:
+                ring.step(T)
+            else:
+                sd.step(T)
         stepper_plans = [plan]
 
     # ---- warm-up ----
@@ -327,13 +351,13 @@ def main():
                    "h2d_bytes_per_step": 4 * N, "d2h_bytes_per_step": 4 * N}
         else:
             qh = torch.empty(n_local, dtype=torch.int32, pin_memory=True)
-            qh.copy_(sd.owned(0).cpu())
+            qh.copy_(owned().cpu())
             dist.barrier()
             t0 = time.perf_counter()
             for _ in range(args.steps):
-                sd.owned(0).copy_(qh, non_blocking=True)
-                sd.step(T)
-                qh.copy_(sd.owned(0), non_blocking=True)
+                owned().copy_(qh, non_blocking=True)
+                do_step()
+                qh.copy_(owned(), non_blocking=True)
                 torch.cuda.synchronize()
             e2e_s = time.perf_counter() - t0
             tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
@@ -379,7 +403,8 @@ def main():
                        "flux": "burgers_eo", "delta": 1e-6, "courant": 0.4, "kappa": [
                            info["kappa_num"], info["kappa_den"]], "k": info["k"],
                        "l2": "inputs larger than L2 (state %.1f GiB > 126 MB)" % (4 * N / 2**30),
-                       "parallelism": "domain split x%d" % world if world > 1 else "single domain"},
+                       "parallelism": ("domain split x%d, %s halo" % (world, halo_mode))
+                       if world > 1 else "single domain"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": launches, "parity": parity,
         }

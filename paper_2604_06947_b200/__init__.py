@@ -21,7 +21,9 @@ __all__ = [
     "FqnmError", "Plan", "fqnm_plan", "fqnm_plan_ex", "fqnm_step", "fqnm_step_block",
     "fqnm_observe", "fqnm_step_host", "fqnm_get_info", "fqnm_transfer", "fqnm_transfer_device",
     "fqnm_roe_transfer_device", "fqnm_debug_override", "fqnm_launch_count", "fqnm_destroy",
-    "fqnm_plan_validate", "fqnm_profile_enable", "fqnm_profile_read",
+    "fqnm_plan_validate", "fqnm_profile_enable", "fqnm_profile_read", "fqnm_halo_buffers",
+    "fqnm_halo_connect", "fqnm_halo_owned", "fqnm_step_group", "fqnm_ipc_export",
+    "fqnm_ipc_open", "fqnm_ipc_close", "owned_tensor",
     "LINEAR", "BURGERS_EO", "BURGERS_LF", "EULER_ROE", "EULER_ROE_DENSITY", "PERIODIC", "TRANSMISSIVE", "HALO",
     "I32", "I64", "ROUND_HALF_AWAY", "ROUND_FLOOR", "ROUND_HALF_EVEN", "lib_path",
 ]
@@ -56,7 +58,7 @@ class PlanDesc(ctypes.Structure):
         ("kappa_num", ctypes.c_int64), ("kappa_den", ctypes.c_int64),
         ("boundary", ctypes.c_int32), ("k", ctypes.c_int32),
         ("q_lo", ctypes.c_int64), ("q_hi", ctypes.c_int64), ("halo", ctypes.c_int64),
-        ("check_range", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+        ("check_range", ctypes.c_int32), ("p2p", ctypes.c_int32),
         ("stream", ctypes.c_void_p),
     ]
 
@@ -106,6 +108,13 @@ def _load():
     L.fqnm_plan_validate.argtypes = [ctypes.POINTER(PlanDesc), ctypes.POINTER(PlanInfo)]
     L.fqnm_profile_enable.argtypes = [vp, ctypes.c_int]
     L.fqnm_profile_read.argtypes = [vp, ctypes.POINTER(dbl), ctypes.POINTER(i64)]
+    L.fqnm_halo_buffers.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)]
+    L.fqnm_halo_connect.argtypes = [vp, vp, vp, vp, i64, vp, vp, vp, i64]
+    L.fqnm_halo_owned.argtypes = [vp, ctypes.POINTER(vp)]
+    L.fqnm_step_group.argtypes = [ctypes.POINTER(vp), ctypes.c_int, i64]
+    L.fqnm_ipc_export.argtypes = [vp, ctypes.c_char_p]
+    L.fqnm_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
+    L.fqnm_ipc_close.argtypes = [vp]
     L.fqnm_launch_count.argtypes = [vp]
     L.fqnm_launch_count.restype = i64
     L.fqnm_last_error.restype = ctypes.c_char_p
@@ -216,7 +225,7 @@ def make_desc(n_local: int, delta: float, dt_dx: float, flux_kind: int = LINEAR,
               dtype: Optional[int] = None, flux_param: float = 0.0, kappa=None,
               rounding: int = ROUND_HALF_AWAY, q_range=None, k: int = 0, halo: int = 0,
               n_global: int = 0, offset: int = 0, check_range: bool = False,
-              stream=None) -> PlanDesc:
+              stream=None, p2p: bool = False) -> PlanDesc:
     L = _load()
     d = PlanDesc()
     L.fqnm_desc_init(ctypes.byref(d))
@@ -238,6 +247,7 @@ def make_desc(n_local: int, delta: float, dt_dx: float, flux_kind: int = LINEAR,
         d.q_lo, d.q_hi = int(q_range[0]), int(q_range[1])
     d.halo = int(halo)
     d.check_range = 1 if check_range else 0
+    d.p2p = 1 if p2p else 0
     d.stream = stream
     return d
 
@@ -272,8 +282,13 @@ def fqnm_profile_read(plan: Plan):
 
 
 def fqnm_step(plan: Plan, q, nsteps: int):
-    """q <- q^{n+nsteps} in place (device tensor of the plan's dtype/layout)."""
+    """q <- q^{n+nsteps} in place (device tensor of the plan's dtype/layout).
+    p2p split plans: q is None (the state lives in the plan's buffers)."""
     L = _load()
+    if q is None:
+        _check(L.fqnm_set_stream(plan.handle, _stream_ptr()))
+        _check(L.fqnm_step(plan.handle, None, int(nsteps)))
+        return None
     ptr = _dev_ptr(q, plan.dtype, "q")
     if q.numel() != _numel(plan):
         raise ValueError(f"q has {q.numel()} elements, plan expects {_numel(plan)}")
@@ -369,6 +384,74 @@ def fqnm_roe_transfer_device(plan: Plan, qL, qR):
 
 def fqnm_debug_override(plan: Plan, kernel: int = 0, k: int = 0, cells_per_thread: int = 0):
     _check(_load().fqnm_debug_override(plan.handle, int(kernel), int(k), int(cells_per_thread)))
+
+
+# ---- fused peer-memory halo exchange --------------------------------------
+def fqnm_halo_buffers(plan: Plan):
+    """(buf0, buf1, flags) device pointers (ints) owned by a p2p split plan."""
+    b0, b1, fl = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    _check(_load().fqnm_halo_buffers(plan.handle, ctypes.byref(b0), ctypes.byref(b1),
+                                     ctypes.byref(fl)))
+    return b0.value, b1.value, fl.value
+
+
+def fqnm_halo_connect(plan: Plan, left, left_n: int, right, right_n: int):
+    """left/right = (buf0, buf1, flags) device pointers of the ring neighbours."""
+    _check(_load().fqnm_halo_connect(plan.handle, ctypes.c_void_p(left[0]), ctypes.c_void_p(left[1]),
+                                     ctypes.c_void_p(left[2]), int(left_n),
+                                     ctypes.c_void_p(right[0]), ctypes.c_void_p(right[1]),
+                                     ctypes.c_void_p(right[2]), int(right_n)))
+
+
+def fqnm_halo_owned(plan: Plan) -> int:
+    """Device pointer (int) to the owned cells of the plan's current buffer."""
+    o = ctypes.c_void_p()
+    _check(_load().fqnm_halo_owned(plan.handle, ctypes.byref(o)))
+    return o.value
+
+
+def fqnm_step_group(plans, nsteps: int):
+    """Step p2p plans of one device together (virtual ranks)."""
+    arr = (ctypes.c_void_p * len(plans))(*[p.handle for p in plans])
+    for p in plans:
+        _check(_load().fqnm_set_stream(p.handle, _stream_ptr()))
+    _check(_load().fqnm_step_group(arr, len(plans), int(nsteps)))
+
+
+def fqnm_ipc_export(ptr: int) -> bytes:
+    buf = ctypes.create_string_buffer(64)
+    _check(_load().fqnm_ipc_export(ctypes.c_void_p(ptr), buf))
+    return buf.raw
+
+
+def fqnm_ipc_open(handle: bytes) -> int:
+    o = ctypes.c_void_p()
+    _check(_load().fqnm_ipc_open(ctypes.c_char_p(handle), ctypes.byref(o)))
+    return o.value
+
+
+def fqnm_ipc_close(ptr: int):
+    _check(_load().fqnm_ipc_close(ctypes.c_void_p(ptr)))
+
+
+def owned_tensor(plan: Plan):
+    """torch view (int32, CUDA) of a p2p plan's owned cells (current buffer)."""
+    import torch
+    ptr = fqnm_halo_owned(plan)
+    n = plan.desc.n_local
+    dev = torch.cuda.current_device()
+    # wrap the raw device pointer through a zero-copy DLPack-free path
+    return _wrap_device(ptr, n, torch.int32, dev)
+
+
+def _wrap_device(ptr: int, n: int, dtype, device: int):
+    import torch
+
+    class _CAI:
+        def __init__(self):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4", "data": (ptr, False),
+                                             "version": 3, "strides": None}
+    return torch.as_tensor(_CAI(), device=f"cuda:{device}")
 
 
 def fqnm_launch_count(plan: Plan) -> int:

@@ -166,6 +166,17 @@ struct fqnm_plan {
     unsigned int* flags = nullptr;
     int res_P = 0;
     uint32_t tag_base = 0;
+    // fused peer-memory halo exchange (HALO + p2p)
+    void* hbuf[2] = {nullptr, nullptr};
+    unsigned int* hflags = nullptr;
+    int hcur = 0;
+    bool hconnected = false;
+    void* lbuf[2] = {nullptr, nullptr};
+    void* rbuf[2] = {nullptr, nullptr};
+    unsigned int* lflags = nullptr;
+    unsigned int* rflags = nullptr;
+    int64_t ln = 0, rn = 0;
+    uint32_t htag = 1;
     cudaStream_t st = nullptr;
     int64_t launches = 0;
     // profiling (fqnm_profile_enable)
@@ -520,6 +531,21 @@ static int plan_build(fqnm_plan_t** out, const fqnm_plan_desc* din, bool allocat
     }
     // device buffers
     cudaError_t e;
+    if (d.boundary == FQNM_HALO && d.p2p) {
+        const size_t bytes = state_elems(p->d) * elem_size(p->d);
+        for (int i = 0; i < 2; ++i) {
+            if ((e = cudaMalloc(&p->hbuf[i], bytes)) != cudaSuccess) {
+                fqnm_destroy(p);
+                return fail(FQNM_ERR_NOMEM, "cudaMalloc halo buffer: %s", cudaGetErrorString(e));
+            }
+            cudaMemset(p->hbuf[i], 0, bytes);
+        }
+        if ((e = cudaMalloc(&p->hflags, 2 * sizeof(unsigned int))) != cudaSuccess) {
+            fqnm_destroy(p);
+            return fail(FQNM_ERR_NOMEM, "cudaMalloc halo flags: %s", cudaGetErrorString(e));
+        }
+        cudaMemset(p->hflags, 0, 2 * sizeof(unsigned int));
+    }
     if (p->family == 6) {
         int rc6 = resident_alloc(p);
         if (rc6 != FQNM_OK) { fqnm_destroy(p); return rc6; }
@@ -582,6 +608,9 @@ extern "C" void fqnm_destroy(fqnm_plan_t* p)
     if (p->e2e_dev) cudaFree(p->e2e_dev);
     if (p->edges) cudaFree(p->edges);
     if (p->flags) cudaFree(p->flags);
+    for (int i = 0; i < 2; ++i)
+        if (p->hbuf[i]) cudaFree(p->hbuf[i]);
+    if (p->hflags) cudaFree(p->hflags);
     for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
     delete p;
 }
@@ -655,6 +684,7 @@ static int launch_block(fqnm_plan_t* p, const int32_t* src, int32_t* dst, int ks
 {
     const fqnm_plan_desc& d = p->d;
     BlockedArgs a;
+    std::memset(&a, 0, sizeof a);
     a.src = src;
     a.dst = dst;
     a.n = d.n_local;
@@ -671,8 +701,14 @@ static int launch_block(fqnm_plan_t* p, const int32_t* src, int32_t* dst, int ks
     return FQNM_OK;
 }
 
+static int halo_step_blocks(fqnm_plan_t* const* plans, int nplans, int64_t nsteps);
+
 extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
 {
+    if (p && p->d.boundary == FQNM_HALO && p->d.p2p) {
+        if (nsteps < 0) return fail(FQNM_ERR_ARG, "nsteps must be >= 0");
+        return halo_step_blocks(&p, 1, nsteps);
+    }
     if (!p || !q) return fail(FQNM_ERR_ARG, "null argument");
     if (nsteps < 0) return fail(FQNM_ERR_ARG, "nsteps must be >= 0");
     if (!aligned16(q)) return fail(FQNM_ERR_ARG, "q must be 16-byte aligned");
@@ -752,6 +788,138 @@ extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
         }
     }
     if (cur != 0) CUDA_TRY(cudaMemcpyAsync(q, bufs[cur], bytes, cudaMemcpyDeviceToDevice, p->st));
+    return FQNM_OK;
+}
+
+static void halo_args(fqnm_plan_t* p, BlockedArgs& a, int ksteps, uint32_t tag)
+{
+    const fqnm_plan_desc& d = p->d;
+    a.src = (const int32_t*)p->hbuf[p->hcur];
+    a.dst = (int32_t*)p->hbuf[p->hcur ^ 1];
+    a.n = d.n_local;
+    a.batch = 1;
+    a.halo = d.halo;
+    a.ksteps = ksteps;
+    a.KL = p->dep_left ? round4(ksteps) : 0;
+    a.KR = p->dep_right ? round4(ksteps) : 0;
+    a.bmode = BM_HALO;
+    const int64_t S = 32 * p->V - a.KL - a.KR;
+    a.nwin = (d.n_local + S - 1) / S;
+    a.p2p = 1;
+    a.tag = tag;
+    a.peer_left_dst = (int32_t*)p->lbuf[p->hcur ^ 1];
+    a.peer_right_dst = (int32_t*)p->rbuf[p->hcur ^ 1];
+    a.left_n = p->ln;
+    a.right_n = p->rn;
+    a.self_flags = p->hflags;
+    a.peer_left_flags = p->lflags;
+    a.peer_right_flags = p->rflags;
+}
+
+// Prime (every rank pushes the edges of its current buffer, tag t0), then the
+// blocks: block b waits for t0 + b and pushes t0 + b + 1.  With several plans
+// (virtual ranks on one device) the launches are interleaved rank by rank.
+static int halo_step_blocks(fqnm_plan_t* const* plans, int nplans, int64_t nsteps)
+{
+    for (int i = 0; i < nplans; ++i) {
+        fqnm_plan_t* p = plans[i];
+        if (!p || !(p->d.boundary == FQNM_HALO && p->d.p2p))
+            return fail(FQNM_ERR_ARG, "fqnm_step_group needs p2p split-domain plans");
+        if (!p->hconnected) return fail(FQNM_ERR_ARG, "p2p plan not connected (fqnm_halo_connect)");
+        if (p->d.n_local < 32 * p->V) return fail(FQNM_ERR_UNSUPPORTED, "p2p needs n_local >= one window");
+    }
+    if (nsteps == 0) return FQNM_OK;
+    fqnm_plan_t* p0 = plans[0];
+    const int k = p0->k;
+    const int64_t nb = (nsteps + k - 1) / k;
+    const uint32_t t0 = p0->htag;
+    for (int i = 0; i < nplans; ++i) {
+        fqnm_plan_t* p = plans[i];
+        if (p->k != k || p->htag != t0) return fail(FQNM_ERR_ARG, "p2p plans out of step");
+        BlockedArgs a;
+        halo_args(p, a, k, t0);
+        a.peer_left_dst = (int32_t*)p->lbuf[p->hcur];     // prime: neighbours' current buffers
+        a.peer_right_dst = (int32_t*)p->rbuf[p->hcur];
+        CUDA_TRY(launch_halo_prime(a, p->st));
+        p->launches++;
+    }
+    int64_t done = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        const int ks = (int)((nsteps - done) < k ? (nsteps - done) : k);
+        for (int i = 0; i < nplans; ++i) {
+            fqnm_plan_t* p = plans[i];
+            BlockedArgs a;
+            halo_args(p, a, ks, t0 + (uint32_t)b);
+            PROF_LAUNCH(launch_blocked(p->rule, p->V, p->minb, a, p->dr, p->st, 148 * 32));
+            p->hcur ^= 1;
+        }
+        done += ks;
+    }
+    for (int i = 0; i < nplans; ++i) plans[i]->htag = t0 + (uint32_t)nb + 1;
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_step_group(fqnm_plan_t* const* plans, int nplans, int64_t nsteps)
+{
+    if (!plans || nplans < 1) return fail(FQNM_ERR_ARG, "null argument");
+    if (nsteps < 0) return fail(FQNM_ERR_ARG, "nsteps must be >= 0");
+    return halo_step_blocks(plans, nplans, nsteps);
+}
+
+extern "C" int fqnm_halo_buffers(const fqnm_plan_t* p, void** buf0, void** buf1, unsigned int** flags)
+{
+    if (!p || !buf0 || !buf1 || !flags) return fail(FQNM_ERR_ARG, "null argument");
+    if (!p->hbuf[0]) return fail(FQNM_ERR_ARG, "not a p2p split-domain plan");
+    *buf0 = p->hbuf[0];
+    *buf1 = p->hbuf[1];
+    *flags = p->hflags;
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_halo_connect(fqnm_plan_t* p, void* left_buf0, void* left_buf1,
+                                 unsigned int* left_flags, int64_t left_n, void* right_buf0,
+                                 void* right_buf1, unsigned int* right_flags, int64_t right_n)
+{
+    if (!p || !left_buf0 || !left_buf1 || !left_flags || !right_buf0 || !right_buf1 || !right_flags)
+        return fail(FQNM_ERR_ARG, "null argument");
+    if (!p->hbuf[0]) return fail(FQNM_ERR_ARG, "not a p2p split-domain plan");
+    if (left_n < p->d.halo || right_n < p->d.halo) return fail(FQNM_ERR_ARG, "neighbour smaller than the halo");
+    p->lbuf[0] = left_buf0; p->lbuf[1] = left_buf1; p->lflags = left_flags; p->ln = left_n;
+    p->rbuf[0] = right_buf0; p->rbuf[1] = right_buf1; p->rflags = right_flags; p->rn = right_n;
+    p->hconnected = true;
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_halo_owned(const fqnm_plan_t* p, void** owned)
+{
+    if (!p || !owned) return fail(FQNM_ERR_ARG, "null argument");
+    if (!p->hbuf[0]) return fail(FQNM_ERR_ARG, "not a p2p split-domain plan");
+    *owned = (int32_t*)p->hbuf[p->hcur] + p->d.halo;
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_ipc_export(const void* dev_ptr, void* handle64)
+{
+    if (!dev_ptr || !handle64) return fail(FQNM_ERR_ARG, "null argument");
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+    std::memcpy(handle64, &h, sizeof h);
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_ipc_open(const void* handle64, void** dev_ptr)
+{
+    if (!dev_ptr || !handle64) return fail(FQNM_ERR_ARG, "null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof h);
+    CUDA_TRY(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_ipc_close(void* dev_ptr)
+{
+    if (!dev_ptr) return fail(FQNM_ERR_ARG, "null argument");
+    CUDA_TRY(cudaIpcCloseMemHandle(dev_ptr));
     return FQNM_OK;
 }
 

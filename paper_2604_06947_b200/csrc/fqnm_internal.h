@@ -46,6 +46,17 @@ struct BlockedArgs {
     int32_t ksteps;
     int32_t KL, KR;     // garbage-shrink per side (multiples of 4)
     int32_t bmode;
+    // fused peer-memory halo exchange (HALO plans with p2p): window 0 and the last
+    // window push their H edge cells straight into the neighbours' next buffers
+    // over NVLink and release a tag; the windows that read halos acquire it first
+    int32_t p2p;
+    uint32_t tag;                  // tag this block's halos carry / this block pushes + 1
+    int32_t* peer_left_dst;        // left neighbour's next ext buffer
+    int32_t* peer_right_dst;       // right neighbour's next ext buffer
+    int64_t left_n, right_n;       // neighbours' owned cells
+    unsigned int* self_flags;      // [0]: left-halo tag, [1]: right-halo tag (written by peers)
+    unsigned int* peer_left_flags;
+    unsigned int* peer_right_flags;
 };
 
 struct EulerArgs {
@@ -77,6 +88,7 @@ cudaError_t launch_blocked(int rule, int V, int minb, const BlockedArgs& a, cons
                            cudaStream_t st, int grid_cap);
 cudaError_t launch_resident(int rule, int V, const ResidentArgsHost& h, const DevRule& r,
                             cudaStream_t st);
+cudaError_t launch_halo_prime(const BlockedArgs& a, cudaStream_t st);
 cudaError_t launch_naive(int rule, const int32_t* src, int32_t* dst, int64_t n, int64_t batch,
                          int bmode, const DevRule& r, cudaStream_t st);
 cudaError_t launch_warp_ensemble(int rule, int V, int32_t* q, int64_t batch, int64_t nsteps,

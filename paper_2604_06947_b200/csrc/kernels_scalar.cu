@@ -30,6 +30,9 @@
 namespace fqnm {
 
 static constexpr unsigned FULL = 0xffffffffu;
+// spin budget before declaring a peer/neighbour dead: trap (a clean launch
+// failure the host sees) instead of hanging the GPU (~20 s at 2 GHz)
+static constexpr long long SPIN_TRAP_CYCLES = 40000000000ll;
 
 // ---------------------------------------------------------------------------
 // one explicit step of V register-resident cells of a lane, from (g, m) with
@@ -126,6 +129,59 @@ __device__ __forceinline__ int64_t wrap_index(int64_t i, int64_t n, int bmode, i
     return i + halo;
 }
 
+// ---- fused peer-memory halo exchange (split domains over NVLink) ----------
+__device__ __forceinline__ void p2p_wait(const unsigned int* flag, uint32_t tag)
+{
+    unsigned int f;
+    const long long t0 = clock64();
+    for (;;) {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(f) : "l"(flag) : "memory");
+        if ((int)(f - tag) >= 0) break;
+        if (clock64() - t0 > SPIN_TRAP_CYCLES) __trap();
+    }
+}
+
+__device__ __forceinline__ void p2p_signal(unsigned int* flag, uint32_t tag)
+{
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(flag), "r"(tag) : "memory");
+}
+
+// push the H edge cells of `ext` (layout [H | n | H]) that `owned0` / the window
+// covers into the neighbours' buffers and release `tag` on their flags
+__device__ __noinline__ void p2p_push(const BlockedArgs& a, const int32_t* ext, bool left_edge,
+                                      bool right_edge, uint32_t tag, int32_t* peer_l,
+                                      int32_t* peer_r, int lane)
+{
+    const int64_t H = a.halo, n = a.n;
+    if (left_edge) {            // my [0, H) -> left neighbour's right halo [H + left_n, ...)
+        for (int64_t i = lane; i < H; i += 32) peer_l[H + a.left_n + i] = ext[H + i];
+        __threadfence_system();
+        __syncwarp();
+        if (lane == 0) p2p_signal(a.peer_left_flags + 1, tag);
+    }
+    if (right_edge) {           // my [n - H, n) -> right neighbour's left halo [0, H)
+        for (int64_t i = lane; i < H; i += 32) peer_r[i] = ext[n + i];
+        __threadfence_system();
+        __syncwarp();
+        if (lane == 0) p2p_signal(a.peer_right_flags + 0, tag);
+    }
+    __syncwarp();
+}
+
+// initial halos of a split run: every rank pushes the edges of its current buffer
+__global__ void k_halo_prime(BlockedArgs a)
+{
+    const int lane = threadIdx.x & 31;
+    p2p_push(a, a.src, true, true, a.tag, a.peer_left_dst, a.peer_right_dst, lane);
+}
+
+cudaError_t launch_halo_prime(const BlockedArgs& a, cudaStream_t st)
+{
+    k_halo_prime<<<1, 32, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
 // Slow window (periodic wrap, transmissive walls, ragged tails, misaligned
 // batches): scalar loads through wrap_index, guarded scalar stores.  Kept out of
 // line so the hot path's register allocation is not shaped by it.
@@ -173,9 +229,18 @@ __global__ void __launch_bounds__(256, MINB) k_blocked(BlockedArgs a, DevRule r)
     int64_t b = 0;
     while (w >= a.nwin && b < a.batch) { w -= a.nwin; ++b; }
     while (b < a.batch) {
-        const int64_t ws = w * S - a.KL;                        // first cell of the window
+        int64_t owned0 = w * S;
+        if (a.p2p && owned0 + S > n && n >= S) owned0 = n - S;  // last window ends at n
+        const int64_t ws = owned0 - a.KL;                       // first cell of the window
         const int64_t boff = b * pstride + (halo ? a.halo : 0);
         const bool fast = ((boff & 3) == 0) && ws >= lowest && ws + W <= n;
+        if (a.p2p && (ws < 0 || ws + W > n)) {                  // reads halos: wait for them
+            if (lane == 0) {
+                if (ws < 0) p2p_wait(a.self_flags + 0, a.tag);
+                if (ws + W > n) p2p_wait(a.self_flags + 1, a.tag);
+            }
+            __syncwarp();
+        }
         if (fast) {
             const int4* s4 = reinterpret_cast<const int4*>(a.src + boff + ws) + lane * (V / 4);
             int4* d4 = reinterpret_cast<int4*>(a.dst + boff + ws) + lane * (V / 4);
@@ -195,6 +260,11 @@ __global__ void __launch_bounds__(256, MINB) k_blocked(BlockedArgs a, DevRule r)
             }
         } else {
             slow_window<RULE, V>(a, r, b, ws, lane);
+        }
+        if (a.p2p && (owned0 == 0 || owned0 + S >= n)) {
+            __syncwarp();
+            p2p_push(a, a.dst, owned0 == 0, owned0 + S >= n, a.tag + 1, a.peer_left_dst,
+                     a.peer_right_dst, lane);
         }
         w += nwarps;
         while (w >= a.nwin && b < a.batch) { w -= a.nwin; ++b; }
@@ -302,11 +372,14 @@ __global__ void __launch_bounds__(256) k_resident(ResidentArgs a, DevRule r)
 #endif
             asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(a.flags + w), "r"(tag) : "memory");
             unsigned int f;
+            const long long t0 = clock64();
             do {
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(a.flags + wl) : "memory");
+                if (clock64() - t0 > SPIN_TRAP_CYCLES) __trap();
             } while ((int)(f - tag) < 0);
             do {
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(a.flags + wr) : "memory");
+                if (clock64() - t0 > SPIN_TRAP_CYCLES) __trap();
             } while ((int)(f - tag) < 0);
         }
         __syncwarp();

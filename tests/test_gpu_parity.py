@@ -418,3 +418,29 @@ def test_density_only_full_size_windows(F):
         lo, hi = max(0, a - S), min(n, b + S)
         ref = oracle.euler_density_run(np.ascontiguousarray(q0[:, lo:hi]), S, 1e-7, lam)
         assert np.array_equal(qh[:, a:b], ref[:, a - lo:b - lo]), (a, b)
+
+
+def test_split_domain_fused_p2p_virtual_ranks(F):
+    """Fused peer-memory halo exchange (the stepping kernel writes the edges into
+    the neighbours' buffers and releases a tag) on P virtual ranks of one GPU:
+    bit-identical to the single domain, across several calls."""
+    from paper_2604_06947_b200 import halo
+    kind, delta, lam, param, amp, off = CASES[1]
+    n = 200003
+    rng = np.random.default_rng(19)
+    q0 = W.smooth_random(rng, n, amp, off)
+    rule = oracle.Rule(kind, delta, lam)
+    ref = rule.run(q0, 75)
+    ref2 = rule.run(ref, 31)
+    for P, H in [(1, 24), (2, 24), (3, 8), (5, 16)]:
+        parts = [halo.partition(n, P, r) for r in range(P)]
+        plans = [F.fqnm_plan_ex(nl, float(Fraction(delta)), float(lam), kind, F.HALO, halo=H,
+                                n_global=n, offset=o, p2p=True) for o, nl in parts]
+        ring = halo.P2PRing.virtual(plans)
+        ring.load([to_dev(q0[o:o + nl]) for o, nl in parts])
+        ring.step(75)
+        got = np.concatenate([host(ring.owned(i)) for i in range(P)])
+        assert np.array_equal(got, ref), (P, H)
+        ring.step(31)                                   # second call: tags continue
+        got = np.concatenate([host(ring.owned(i)) for i in range(P)])
+        assert np.array_equal(got, ref2), (P, H)

@@ -109,3 +109,27 @@ def test_local_transport_virtual_ranks_cpu():
         sd.step(29)
         got = torch.cat([sd.owned(i) for i in range(P)]).numpy().astype(np.int64)
         assert np.array_equal(got, ref)
+
+
+def _p2p_fallback_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        def factory():
+            if rank == 1:
+                raise RuntimeError("no peer access on rank 1")
+            raise RuntimeError("no GPU in the CPU test")
+        ring, why = halo.P2PRing.distributed(factory, None, "cpu")
+        out[rank] = 1 if (ring is None and "rank 1" in why) else 0
+    finally:
+        dist.destroy_process_group()
+
+
+def test_p2p_setup_failure_is_collective():
+    """If the fused peer-memory setup fails on any rank, every rank falls back
+    (returns None) instead of waiting in a collective the failed rank skipped."""
+    out = torch.zeros(2, dtype=torch.int32).share_memory_()
+    mp.start_processes(_p2p_fallback_worker, args=(2, _free_port(), out), nprocs=2, join=True,
+                       start_method="fork")
+    assert out.tolist() == [1, 1]
