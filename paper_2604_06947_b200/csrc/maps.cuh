@@ -9,10 +9,11 @@
 #include <cstdint>
 #include "fqnm_internal.h"
 
-// EO pipe-balance variant (tools/tune_variants.sh): 2 = conversion by IMAD and
-// phi- by LOP3 (measured fastest on B200), 1 = both LOP3, 0 = phi- by IMAD.
+// EO pipe-balance variant (tools/tune_variants.sh, profiles/r01_tune_eo_variants*.jsonl):
+// 3 = conversion by I2FP and phi- by LOP3 (12.2 instr/cell, measured fastest on B200),
+// 2 = conversion by IMAD + FADD, 1 = conversion by LOP3 + FADD, 0/4 = phi- by IMAD.
 #ifndef FQNM_EO_VARIANT
-#define FQNM_EO_VARIANT 2
+#define FQNM_EO_VARIANT 3
 #endif
 
 namespace fqnm {
@@ -74,19 +75,21 @@ __device__ __forceinline__ int32_t imad(int32_t a, int32_t b, int32_t c)
     return d;
 }
 
-// Pipe balance per cell, variant 2: 3 FP32 (FADD, FMUL, FFMA),
-// 5 IMAD (conversion, q^2, 2 x remainder, -K), 5 ALU (LEA.HI, SHF, LOP3, and the
-// step's 2 x IADD3) -> 13 instructions, issue-bound, neither integer pipe saturated.
+// Per cell, variant 3: I2FP, FMUL, FFMA, 4 IMAD (q^2, 2 x remainder,
+// -K), LEA.HI, SHF, LOP3 and the step's 2 x IADD3 -> 12 SASS instructions.
 __device__ __forceinline__ void eo_gm(int32_t q, int32_t& g, int32_t& m, const DevRule& r)
 {
     // 0x4B400000 + q for |q| < 2^22 as one LOP3: bits 0..22 of q with bit 22
     // flipped, exponent/sign bits of 1.5*2^23 above
-#if FQNM_EO_VARIANT == 2
+#if FQNM_EO_VARIANT >= 3
+    const float qf = __int2float_rn(q);                                  // exact, |q| < 2^24
+#elif FQNM_EO_VARIANT == 2
     const uint32_t x = (uint32_t)imad(q, r.one, 0x4B400000);
+    const float qf = __int_as_float((int32_t)x) - 12582912.0f;          // exact
 #else
     const uint32_t x = lop3_6c((uint32_t)q, 0x4B400000u, 0x007FFFFFu);
-#endif
     const float qf = __int_as_float((int32_t)x) - 12582912.0f;          // exact
+#endif
     const float s = __fmul_rn(qf, qf);
     const float t = __fmaf_rn(s, r.eo_cf, 12582912.0f);                 // 0x4B400000 + est
     const int32_t bits = __float_as_int(t);
@@ -95,7 +98,7 @@ __device__ __forceinline__ void eo_gm(int32_t q, int32_t& g, int32_t& m, const D
     u = imad(bits, r.eo_twoQ, u);                                        // 2Q - 1 - r
     const int32_t gb = bits + (int32_t)((uint32_t)u >> 31);              // LEA.HI
     g = imad(gb, r.one, (int32_t)0xB4C00000);                            // - 0x4B400000
-#if FQNM_EO_VARIANT == 0
+#if FQNM_EO_VARIANT == 0 || FQNM_EO_VARIANT == 4
     m = imad(g, (int32_t)((uint32_t)q >> 31), 0);                        // phi-(q) = [q<0] g
 #else
     m = g & (q >> 31);
