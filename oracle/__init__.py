@@ -91,6 +91,10 @@ def lib():
         L.or_run_euler_density.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                            ctypes.c_double, ctypes.c_int64, P64, ctypes.c_int64,
                                            ctypes.c_int]
+        L.or_step_scalar_2d.argtypes = [PM, PM, PM, PM, ctypes.c_int, ctypes.c_int64,
+                                        ctypes.c_int64, P64, P64]
+        L.or_run_scalar_2d.argtypes = [PM, PM, PM, PM, ctypes.c_int, ctypes.c_int64,
+                                       ctypes.c_int64, P64, ctypes.c_int64, ctypes.c_int]
         L.or_round_rational.restype = ctypes.c_int64
         L.or_round_rational.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64,
                                         ctypes.c_int]
@@ -162,6 +166,33 @@ class Rule:
             B, N = q.shape
             lib().or_run_scalar_batch(ctypes.byref(self._mp), ctypes.byref(self._mm), boundary,
                                       B, N, _p64(q), nsteps, nthreads)
+        return q
+
+
+class Rule2D:
+    """Directional composition in 2D (Thm P:364-401): one scalar Rule per direction
+    (same flux kind and delta, dt/dx and dt/dy, per-direction speed param)."""
+
+    def __init__(self, kind: int, delta, dt_dx, dt_dy, param_x=Fraction(1), param_y=Fraction(1),
+                 rounding: int = RHA):
+        self.rx = Rule(kind, delta, dt_dx, param_x, rounding)
+        self.ry = Rule(kind, delta, dt_dy, param_y, rounding)
+
+    def _maps(self):
+        return (ctypes.byref(self.rx._mp), ctypes.byref(self.rx._mm),
+                ctypes.byref(self.ry._mp), ctypes.byref(self.ry._mm))
+
+    def step(self, q, boundary: int = PERIODIC) -> np.ndarray:
+        q = np.ascontiguousarray(q, dtype=np.int64)
+        ny, nx = q.shape
+        out = np.empty_like(q)
+        lib().or_step_scalar_2d(*self._maps(), boundary, nx, ny, _p64(q), _p64(out))
+        return out
+
+    def run(self, q, nsteps: int, boundary: int = PERIODIC, nthreads: int = 0) -> np.ndarray:
+        q = np.array(q, dtype=np.int64, copy=True, order="C")
+        ny, nx = q.shape
+        lib().or_run_scalar_2d(*self._maps(), boundary, nx, ny, _p64(q), nsteps, nthreads)
         return q
 
 

@@ -191,6 +191,56 @@ void or_run_scalar_batch(const or_map* pp, const or_map* pm, int boundary, int64
         run_one(pp, pm, boundary, N, q + b * N, nsteps);
 }
 
+/* ---- 3b. Cartesian extension by directional composition ------------------ */
+/* Thm formal Cartesian dimensional extension, d = 2, unsplit:
+ *   q'_{i,j} = q_{i,j} - (F^x_{i+1/2,j} - F^x_{i-1/2,j}) - (F^y_{i,j+1/2} - F^y_{i,j-1/2}),
+ *   F^x_{i+1/2,j} = phi+_x(q_{i,j}) + phi-_x(q_{i+1,j}),
+ *   F^y_{i,j+1/2} = phi+_y(q_{i,j}) + phi-_y(q_{i,j+1}),
+ * all on q^n.  Layout q[j * nx + i] (x fastest).  Boundaries per direction as
+ * in 1D (periodic wrap or transmissive ghost copies). */
+static int64_t at2(const int64_t* q, int boundary, int64_t nx, int64_t ny, int64_t i, int64_t j)
+{
+    if (boundary == OR_PERIODIC) {
+        i = (i % nx + nx) % nx;
+        j = (j % ny + ny) % ny;
+    } else {
+        i = i < 0 ? 0 : (i >= nx ? nx - 1 : i);
+        j = j < 0 ? 0 : (j >= ny ? ny - 1 : j);
+    }
+    return q[j * nx + i];
+}
+
+void or_step_scalar_2d(const or_map* ppx, const or_map* pmx, const or_map* ppy, const or_map* pmy,
+                       int boundary, int64_t nx, int64_t ny, const int64_t* q, int64_t* out)
+{
+    #pragma omp parallel for schedule(static) if (nx * ny >= 32768)
+    for (int64_t j = 0; j < ny; ++j)
+        for (int64_t i = 0; i < nx; ++i) {
+            int64_t c = q[j * nx + i];
+            int64_t Fxr = or_phi(ppx, c) + or_phi(pmx, at2(q, boundary, nx, ny, i + 1, j));
+            int64_t Fxl = or_phi(ppx, at2(q, boundary, nx, ny, i - 1, j)) + or_phi(pmx, c);
+            int64_t Fyr = or_phi(ppy, c) + or_phi(pmy, at2(q, boundary, nx, ny, i, j + 1));
+            int64_t Fyl = or_phi(ppy, at2(q, boundary, nx, ny, i, j - 1)) + or_phi(pmy, c);
+            out[j * nx + i] = c - (Fxr - Fxl) - (Fyr - Fyl);
+        }
+}
+
+void or_run_scalar_2d(const or_map* ppx, const or_map* pmx, const or_map* ppy, const or_map* pmy,
+                      int boundary, int64_t nx, int64_t ny, int64_t* q, int64_t nsteps,
+                      int nthreads)
+{
+    set_threads(nthreads);
+    const size_t N = (size_t)(nx * ny);
+    int64_t* a = q;
+    int64_t* b = (int64_t*)malloc(sizeof(int64_t) * N);
+    for (int64_t s = 0; s < nsteps; ++s) {
+        or_step_scalar_2d(ppx, pmx, ppy, pmy, boundary, nx, ny, a, b);
+        int64_t* t = a; a = b; b = t;
+    }
+    if (a != q) { memcpy(q, a, sizeof(int64_t) * N); b = a; }
+    free(b);
+}
+
 /* ---- 4. reconstruction ---------------------------------------------------- */
 void or_observe(double delta, const int64_t* q, double* u, int64_t n)
 {

@@ -23,7 +23,7 @@ __all__ = [
     "fqnm_roe_transfer_device", "fqnm_debug_override", "fqnm_launch_count", "fqnm_destroy",
     "fqnm_plan_validate", "fqnm_profile_enable", "fqnm_profile_read", "fqnm_halo_buffers",
     "fqnm_halo_connect", "fqnm_halo_owned", "fqnm_step_group", "fqnm_ipc_export",
-    "fqnm_ipc_open", "fqnm_ipc_close", "owned_tensor",
+    "fqnm_ipc_open", "fqnm_ipc_close", "owned_tensor", "fqnm_plan_2d",
     "LINEAR", "BURGERS_EO", "BURGERS_LF", "EULER_ROE", "EULER_ROE_DENSITY", "PERIODIC", "TRANSMISSIVE", "HALO",
     "I32", "I64", "ROUND_HALF_AWAY", "ROUND_FLOOR", "ROUND_HALF_EVEN", "lib_path",
 ]
@@ -91,6 +91,8 @@ def _load():
     vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
     L.fqnm_plan.argtypes = [ctypes.POINTER(vp), i64, dbl, dbl, ctypes.c_int, ctypes.c_int]
     L.fqnm_plan_ex.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(PlanDesc)]
+    L.fqnm_plan_2d.argtypes = [ctypes.POINTER(vp), i64, i64, dbl, dbl, dbl, ctypes.c_int,
+                               ctypes.c_int, dbl, dbl]
     L.fqnm_desc_init.argtypes = [ctypes.POINTER(PlanDesc)]
     L.fqnm_desc_init.restype = None
     L.fqnm_destroy.argtypes = [vp]
@@ -217,6 +219,23 @@ def fqnm_plan(N: int, delta: float, dt_dx: float, flux_kind: int = LINEAR,
     if flux_kind in (EULER_ROE, EULER_ROE_DENSITY):
         d.nvar, d.dtype = 3, I64
     d.check_range = 1 if flux_kind not in (EULER_ROE, EULER_ROE_DENSITY) else 0
+    return Plan(h, d)
+
+
+def fqnm_plan_2d(nx: int, ny: int, delta: float, dt_dx: float, dt_dy: float,
+                 flux_kind: int = LINEAR, boundary: int = PERIODIC, param_x: float = 0.0,
+                 param_y: float = 0.0) -> Plan:
+    """2D directional-composition plan (include/fqnm.h fqnm_plan_2d); state [ny][nx] int32."""
+    L = _load()
+    h = ctypes.c_void_p()
+    _check(L.fqnm_plan_2d(ctypes.byref(h), int(nx), int(ny), float(delta), float(dt_dx),
+                          float(dt_dy), int(flux_kind), int(boundary), float(param_x),
+                          float(param_y)))
+    d = PlanDesc()
+    L.fqnm_desc_init(ctypes.byref(d))
+    d.n_local = d.n_global = nx * ny
+    d.delta, d.dt_dx, d.flux_kind, d.boundary = delta, dt_dx, flux_kind, boundary
+    d.check_range = 1
     return Plan(h, d)
 
 

@@ -177,6 +177,11 @@ struct fqnm_plan {
     unsigned int* rflags = nullptr;
     int64_t ln = 0, rn = 0;
     uint32_t htag = 1;
+    // 2D plans (family 7): y-direction rule
+    int64_t nx = 0, ny = 0;
+    HostMap hpy, hmy;
+    DevRule dry{};
+    bool same_xy = false;
     cudaStream_t st = nullptr;
     int64_t launches = 0;
     // profiling (fqnm_profile_enable)
@@ -309,16 +314,30 @@ static int build_rule(fqnm_plan_t* p)
     const int64_t i32lo = INT32_MIN + 1, i32hi = INT32_MAX;
     if (kind == FQNM_LINEAR) {
         // D8 holds on all of Z iff |kappa| <= 1 (increments of round(kappa q) are 0/1)
-        if ((P < 0 ? -P : P) > Q)
+        const int64_t aP = P < 0 ? -P : P;
+        if (aP > Q)
             return fail(FQNM_ERR_CFL, "linear |kappa| = %lld/%lld > 1 violates D8", (long long)P,
                         (long long)Q);
-        if (lo == 0 && hi == 0) { lo = i32lo; hi = i32hi; }
+        // R_LIN_FAST domain (maps.cuh lin_phi): |q| < 2^24, |kappa q| <= 2^20, Q < 2^29
+        int64_t a_lin = 0;
+        if (!lin_half && d.rounding == FQNM_ROUND_HALF_AWAY && Q < (1 << 29)) {
+            a_lin = (int64_t)(((i128)1 << 20) * Q / aP);
+            if (a_lin > (1 << 24) - 1) a_lin = (1 << 24) - 1;
+        }
+        const bool derive = (lo == 0 && hi == 0);
+        if (derive) {
+            if (a_lin > 0 && d.check_range) { lo = -a_lin; hi = a_lin; }   // checked at every step
+            else { lo = i32lo; hi = i32hi; }
+        }
         if (lo < i32lo || hi > i32hi) return fail(FQNM_ERR_RANGE, "range exceeds int32 state");
-        if (!lin_half && !(generic_headroom(p->hp, lo < 0 ? -lo : lo) &&
-                           generic_headroom(p->hp, hi) && generic_headroom(p->hm, lo < 0 ? -lo : lo)
-                           && generic_headroom(p->hm, hi)))
-            return fail(FQNM_ERR_RANGE, "int64 headroom exceeded");
-        p->rule = lin_half ? R_LIN_HALF : R_GENERIC;
+        const int64_t amax = (lo < 0 ? -lo : lo) > hi ? (lo < 0 ? -lo : lo) : hi;
+        if (lin_half) p->rule = R_LIN_HALF;
+        else if (a_lin > 0 && amax <= a_lin) p->rule = R_LIN_FAST;
+        else {
+            if (!(generic_headroom(p->hp, amax) && generic_headroom(p->hm, amax)))
+                return fail(FQNM_ERR_RANGE, "int64 headroom exceeded");
+            p->rule = R_GENERIC;
+        }
     } else {
         if (lo == 0 && hi == 0) {
             // derive the largest symmetric range on which D8 holds (and the device path is exact)
@@ -367,6 +386,17 @@ static int build_rule(fqnm_plan_t* p)
     r.rounding = d.rounding;
     r.one = 1;
     r.mone = -1;
+    r.lin_minus = (kind == FQNM_LINEAR && P < 0) ? 1 : 0;
+    if (p->rule == R_LIN_FAST) {
+        const int64_t aP = P < 0 ? -P : P;
+        r.eo_ntwoP = (int32_t)(-2 * aP);
+        r.eo_twoQ = (int32_t)(2 * Q);
+        r.eo_c1 = (int32_t)(uint32_t)((uint64_t)(Q - 1) - (uint64_t)(2 * Q) * 0x4B400000ull);
+        const double target = ((double)aP / (double)Q) * (1.0 - std::ldexp(1.0, -21));
+        float cf = (float)target;
+        while ((double)cf > target) cf = std::nextafterf(cf, 0.0f);
+        r.eo_cf = cf;
+    }
     if (p->rule == R_EO_FAST) {
         r.eo_ntwoP = (int32_t)(-2 * P);
         r.eo_twoQ = (int32_t)(2 * Q);
@@ -598,6 +628,64 @@ extern "C" int fqnm_plan(fqnm_plan_t** out, int64_t N, double delta, double dt_d
     return fqnm_plan_ex(out, &d);
 }
 
+extern "C" int fqnm_plan_2d(fqnm_plan_t** out, int64_t nx, int64_t ny, double delta, double dt_dx,
+                            double dt_dy, int flux_kind, int boundary, double param_x, double param_y)
+{
+    if (!out) return fail(FQNM_ERR_ARG, "null argument");
+    *out = nullptr;
+    if (nx < 2 || ny < 2) return fail(FQNM_ERR_ARG, "nx and ny must be >= 2");
+    if (flux_kind != FQNM_LINEAR && flux_kind != FQNM_BURGERS_EO && flux_kind != FQNM_BURGERS_LF)
+        return fail(FQNM_ERR_UNSUPPORTED, "2D plans support the scalar flux kinds");
+    if (boundary != FQNM_PERIODIC && boundary != FQNM_TRANSMISSIVE)
+        return fail(FQNM_ERR_ARG, "2D plans: boundary must be PERIODIC or TRANSMISSIVE");
+    if (!(std::isfinite(dt_dy) && dt_dy > 0)) return fail(FQNM_ERR_ARG, "dt_dy must be finite and > 0");
+    fqnm_plan_desc d;
+    fqnm_desc_init(&d);
+    d.n_local = nx * ny;
+    d.n_global = nx * ny;
+    d.delta = delta;
+    d.dt_dx = dt_dy;
+    d.flux_kind = flux_kind;
+    d.boundary = boundary;
+    d.flux_param = param_y;
+    d.check_range = 1;
+    // y rule (host-only build)
+    fqnm_plan_t* py = nullptr;
+    int rc = plan_build(&py, &d, false);
+    if (rc != FQNM_OK) return rc;
+    // x rule + the plan
+    d.dt_dx = dt_dx;
+    d.flux_param = param_x;
+    fqnm_plan_t* p = nullptr;
+    rc = plan_build(&p, &d, false);
+    if (rc != FQNM_OK) { delete py; return rc; }
+    p->nx = nx;
+    p->ny = ny;
+    p->hpy = py->hp;
+    p->hmy = py->hm;
+    p->dry = py->dr;
+    p->same_xy = std::memcmp(&p->dr, &py->dr, sizeof(DevRule)) == 0;
+    if (p->rule != py->rule) p->rule = R_GENERIC;          // both directions on the int64 path
+    p->lo = p->lo > py->lo ? p->lo : py->lo;
+    p->hi = p->hi < py->hi ? p->hi : py->hi;
+    p->dep_left = p->dep_left || py->dep_left;
+    p->dep_right = p->dep_right || py->dep_right;
+    delete py;
+    p->family = 7;
+    p->V = 0;
+    p->k = STEP2D_KMAX;
+    p->scratch_bytes = state_elems(p->d) * elem_size(p->d);
+    cudaError_t e;
+    if ((e = cudaMalloc(&p->scratch, p->scratch_bytes)) != cudaSuccess ||
+        (e = cudaMalloc(&p->d_minmax, 2 * sizeof(long long))) != cudaSuccess ||
+        (e = cudaMallocHost(&p->h_minmax, 4 * sizeof(long long))) != cudaSuccess) {
+        fqnm_destroy(p);
+        return fail(FQNM_ERR_NOMEM, "allocating 2D plan buffers: %s", cudaGetErrorString(e));
+    }
+    *out = p;
+    return FQNM_OK;
+}
+
 extern "C" void fqnm_destroy(fqnm_plan_t* p)
 {
     if (!p) return;
@@ -753,6 +841,24 @@ extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
     // ping-pong families
     void* bufs[2] = {q, p->scratch};
     int cur = 0;
+    if (p->family == 7) {
+        int64_t nb = (nsteps + p->k - 1) / p->k;
+        if (nb % 2 == 1 && nsteps >= nb + 1) nb += 1;
+        const int64_t base = nsteps / nb, rem = nsteps % nb;
+        for (int64_t b = 0; b < nb; ++b) {
+            Step2DArgs a;
+            a.src = (const int32_t*)bufs[cur];
+            a.dst = (int32_t*)bufs[cur ^ 1];
+            a.nx = p->nx;
+            a.ny = p->ny;
+            a.ksteps = (int)(base + (b < rem ? 1 : 0));
+            a.bmode = bm;
+            PROF_LAUNCH(launch_step2d(p->rule, p->same_xy, a, p->dr, p->dry, p->st));
+            cur ^= 1;
+        }
+        if (cur != 0) CUDA_TRY(cudaMemcpyAsync(q, bufs[cur], bytes, cudaMemcpyDeviceToDevice, p->st));
+        return FQNM_OK;
+    }
     if (p->family == 1 || p->family == 5) {
         for (int64_t s = 0; s < nsteps; ++s) {
             if (p->family == 1) {
@@ -1114,6 +1220,11 @@ extern "C" int fqnm_debug_override(fqnm_plan_t* p, int32_t kernel, int32_t k, in
     if (V) {
         if (p->family != 2 || !blocked_has_V(V)) return fail(FQNM_ERR_UNSUPPORTED, "V override needs K2 and V in {8,16,32}");
         p->V = V;
+    }
+    if (k && p->family == 7) {
+        if (k > STEP2D_KMAX) return fail(FQNM_ERR_ARG, "2D plans: k <= %d", STEP2D_KMAX);
+        p->k = k;
+        return FQNM_OK;
     }
     if (k && p->family == 6) {
         int P, base, rem, H;

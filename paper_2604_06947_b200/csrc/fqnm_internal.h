@@ -13,7 +13,9 @@ enum RuleKind : int32_t {
     R_LIN_HALF = 1,   // LINEAR a > 0, kappa = 1/2 exactly, RHA: phi+ = q - trunc(q/2), phi- = 0
     R_EO_FAST = 2,    // BURGERS_EO, RHA: g(|q|) = floor((2P q^2 + Q)/(2Q)) by float estimate +
                       // exact 32-bit remainder correction (valid range proven at plan time)
-    R_GENERIC = 3     // any piecewise-quadratic map, exact int64 arithmetic, any rounding
+    R_GENERIC = 3,    // any piecewise-quadratic map, exact int64 arithmetic, any rounding
+    R_LIN_FAST = 4    // LINEAR any |kappa| <= 1, RHA: g(|q|) = floor((2P|q| + Q)/(2Q)) by the
+                      // same estimate + remainder scheme as EO (eo_* constants), sign restored
 };
 
 enum Support : int32_t { SUPP_ALL = 0, SUPP_POS = 1, SUPP_NEG = 2, SUPP_NONE = 3 };
@@ -29,6 +31,7 @@ struct DevRule {
     int32_t eo_c1;        // Q - 1 - 2Q * 0x4B400000  (mod 2^32)
     int32_t eo_twoQ;      // 2Q
     float eo_cf;          // largest float <= (P/Q)(1 - 2^-21)
+    int32_t lin_minus;    // R_LIN_FAST: 0 -> the map is phi+ (a > 0), 1 -> phi- (a < 0)
     int32_t one;          // runtime 1 and -1: let the linear kernel issue IMADs (FMA pipe)
     int32_t mone;
     int32_t pad2;
@@ -82,6 +85,20 @@ struct ResidentArgsHost {
 };
 
 int resident_capacity_warps(int rule, int V);   // 0 if unavailable (no GPU)
+
+// K7: 2D directional composition, smem-tiled with k <= STEP2D_KMAX steps per launch
+#define STEP2D_TX 128
+#define STEP2D_TY 32
+#define STEP2D_KMAX 4
+struct Step2DArgs {
+    const int32_t* src;
+    int32_t* dst;
+    int64_t nx, ny;
+    int32_t ksteps;
+    int32_t bmode;
+};
+cudaError_t launch_step2d(int rule, bool same, const Step2DArgs& a, const DevRule& rx,
+                          const DevRule& ry, cudaStream_t st);
 
 // kernel launchers (kernels_scalar.cu / kernels_euler.cu); return cudaError_t
 cudaError_t launch_blocked(int rule, int V, int minb, const BlockedArgs& a, const DevRule& r,

@@ -400,6 +400,153 @@ __global__ void __launch_bounds__(256) k_resident(ResidentArgs a, DevRule r)
 }
 
 // ---------------------------------------------------------------------------
+// K7: 2D directional composition (Thm formal Cartesian extension):
+//   q'_{i,j} = q - (F^x_{i+1/2,j} - F^x_{i-1/2,j}) - (F^y_{i,j+1/2} - F^y_{i,j-1/2})
+// A CTA (32 x 16 threads) owns a (TX + 2k) x (TY + 2k) region; every thread keeps
+// its fixed cells (x = tx + 32a, y = ty + 16b) in registers for the k steps.
+// Per step each thread reads the neighbours' maps (phi+ of the left/lower cell,
+// phi- of the right/upper cell) from shared memory, updates its cells, and
+// writes the maps of the new values into the other half of a double-buffered
+// map array: one barrier per step.  Garbage from the region edge moves in one
+// cell per step and the inner TX x TY tile is stored after k steps.
+// SAME: identical x and y rules (maps evaluated once).
+template <int RULE, bool SAME, bool WALL>
+__global__ void __launch_bounds__(512) k_step2d(Step2DArgs a, DevRule rx, DevRule ry)
+{
+    extern __shared__ int32_t sm2[];
+    constexpr int TX = STEP2D_TX, TY = STEP2D_TY;
+    constexpr int NA = (TX + 2 * STEP2D_KMAX + 31) / 32;       // cell columns per thread
+    constexpr int NB = (TY + 2 * STEP2D_KMAX + 15) / 16;       // cell rows per thread
+    const int K = a.ksteps;
+    const int RX = TX + 2 * K, RY = TY + 2 * K, R = RX * RY;
+    constexpr int NMAP = SAME ? 2 : 4;                          // Px, Mx (, Py, My)
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int64_t nx = a.nx, ny = a.ny;
+    const int64_t ox = (int64_t)blockIdx.x * TX - K, oy = (int64_t)blockIdx.y * TY - K;
+    int32_t q[NB][NA];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        const int y = ty + 16 * b;
+        int64_t gj = oy + (y < RY ? y : RY - 1);
+        if (WALL) gj = gj < 0 ? 0 : (gj >= ny ? ny - 1 : gj);
+        else gj = (gj % ny + ny) % ny;
+#pragma unroll
+        for (int c = 0; c < NA; ++c) {
+            const int x = tx + 32 * c;
+            int64_t gi = ox + (x < RX ? x : RX - 1);
+            if (WALL) gi = gi < 0 ? 0 : (gi >= nx ? nx - 1 : gi);
+            else gi = (gi % nx + nx) % nx;
+            q[b][c] = a.src[gj * nx + gi];
+        }
+    }
+    // maps of the current values -> buffer 0
+    auto publish = [&](int buf) {
+        int32_t* M0 = sm2 + (size_t)buf * NMAP * R;
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+            for (int c = 0; c < NA; ++c) {
+                const int x = tx + 32 * c, y = ty + 16 * b;
+                if (x < RX && y < RY) {
+                    const int i = y * RX + x;
+                    int32_t g, m;
+                    phi_gm<RULE>(q[b][c], g, m, rx);
+                    M0[i] = g - m;                    // phi+_x
+                    M0[R + i] = m;                    // phi-_x
+                    if (!SAME) {
+                        phi_gm<RULE>(q[b][c], g, m, ry);
+                        M0[2 * R + i] = g - m;        // phi+_y
+                        M0[3 * R + i] = m;            // phi-_y
+                    }
+                }
+            }
+    };
+    publish(0);
+    __syncthreads();
+    for (int s = 0; s < K; ++s) {
+        const int32_t* Mc = sm2 + (size_t)(s & 1) * NMAP * R;
+        const int32_t* PX = Mc;
+        const int32_t* MX = Mc + R;
+        const int32_t* PY = SAME ? PX : Mc + 2 * R;
+        const int32_t* MY = SAME ? MX : Mc + 3 * R;
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+            for (int c = 0; c < NA; ++c) {
+                const int x = tx + 32 * c, y = ty + 16 * b;
+                if (x < RX && y < RY) {
+                    const int i = y * RX + x;
+                    const int il = x > 0 ? i - 1 : i, ir = x < RX - 1 ? i + 1 : i;
+                    const int id = y > 0 ? i - RX : i, iu = y < RY - 1 ? i + RX : i;
+                    int32_t txl = PX[il] + MX[i];
+                    int32_t txr = PX[i] + MX[ir];
+                    int32_t tyl = PY[id] + MY[i];
+                    int32_t tyr = PY[i] + MY[iu];
+                    if (WALL) {                                       // ghost copies (A12)
+                        const int64_t gi = ox + x, gj = oy + y;
+                        if (gi == 0) txl = PX[i] + MX[i];
+                        if (gi == nx - 1) txr = PX[i] + MX[i];
+                        if (gj == 0) tyl = PY[i] + MY[i];
+                        if (gj == ny - 1) tyr = PY[i] + MY[i];
+                    }
+                    q[b][c] = q[b][c] + txl - txr + tyl - tyr;
+                }
+            }
+        if (s + 1 < K) {
+            publish((s + 1) & 1);
+            __syncthreads();
+        }
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int c = 0; c < NA; ++c) {
+            const int x = tx + 32 * c, y = ty + 16 * b;
+            const int64_t gi = ox + x, gj = oy + y;
+            if (x >= K && x < K + TX && y >= K && y < K + TY && gi < nx && gj < ny)
+                a.dst[gj * nx + gi] = q[b][c];
+        }
+}
+
+template <int RULE, bool SAME>
+static cudaError_t step2d_rule(const Step2DArgs& a, const DevRule& rx, const DevRule& ry,
+                               cudaStream_t st)
+{
+    const int K = a.ksteps;
+    const size_t R = (size_t)(STEP2D_TX + 2 * K) * (STEP2D_TY + 2 * K);
+    const size_t smem = R * sizeof(int32_t) * 2 * (SAME ? 2 : 4);    // double-buffered maps
+    dim3 grid((unsigned)((a.nx + STEP2D_TX - 1) / STEP2D_TX), (unsigned)((a.ny + STEP2D_TY - 1) / STEP2D_TY));
+    cudaError_t e;
+    if (a.bmode == BM_TRANSMISSIVE) {
+        e = cudaFuncSetAttribute(k_step2d<RULE, SAME, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k_step2d<RULE, SAME, true><<<grid, 512, smem, st>>>(a, rx, ry);
+    } else {
+        e = cudaFuncSetAttribute(k_step2d<RULE, SAME, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k_step2d<RULE, SAME, false><<<grid, 512, smem, st>>>(a, rx, ry);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_step2d(int rule, bool same, const Step2DArgs& a, const DevRule& rx,
+                          const DevRule& ry, cudaStream_t st)
+{
+    if (a.ksteps < 1 || a.ksteps > STEP2D_KMAX) return cudaErrorInvalidValue;
+    switch (rule) {
+        case R_LIN_HALF: return same ? step2d_rule<R_LIN_HALF, true>(a, rx, ry, st)
+                                     : step2d_rule<R_LIN_HALF, false>(a, rx, ry, st);
+        case R_EO_FAST: return same ? step2d_rule<R_EO_FAST, true>(a, rx, ry, st)
+                                    : step2d_rule<R_EO_FAST, false>(a, rx, ry, st);
+        case R_GENERIC: return same ? step2d_rule<R_GENERIC, true>(a, rx, ry, st)
+                                    : step2d_rule<R_GENERIC, false>(a, rx, ry, st);
+        case R_LIN_FAST: return same ? step2d_rule<R_LIN_FAST, true>(a, rx, ry, st)
+                                     : step2d_rule<R_LIN_FAST, false>(a, rx, ry, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K3: one problem of 32*V cells per warp, all steps in registers
 template <int RULE, int V, bool WALL>
 __global__ void __launch_bounds__(128) k_warp_ensemble(int32_t* __restrict__ q, int64_t batch,
@@ -567,6 +714,7 @@ cudaError_t launch_blocked(int rule, int V, int minb, const BlockedArgs& a, cons
         case R_LIN_HALF: return blocked_rule<R_LIN_HALF>(V, minb, a, r, st, grid_cap);
         case R_EO_FAST: return blocked_rule<R_EO_FAST>(V, minb, a, r, st, grid_cap);
         case R_GENERIC: return blocked_rule<R_GENERIC>(V, minb, a, r, st, grid_cap);
+        case R_LIN_FAST: return blocked_rule<R_LIN_FAST>(V, minb, a, r, st, grid_cap);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -580,6 +728,7 @@ cudaError_t launch_naive(int rule, const int32_t* src, int32_t* dst, int64_t n, 
         case R_LIN_HALF: k_naive<R_LIN_HALF><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
         case R_EO_FAST: k_naive<R_EO_FAST><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
         case R_GENERIC: k_naive<R_GENERIC><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
+        case R_LIN_FAST: k_naive<R_LIN_FAST><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -641,10 +790,12 @@ int resident_capacity_warps(int rule, int V)
     if (V == 8) {
         e = rule == R_LIN_HALF ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_LIN_HALF, 8>, 256, 0)
           : rule == R_EO_FAST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_EO_FAST, 8>, 256, 0)
+          : rule == R_LIN_FAST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_LIN_FAST, 8>, 256, 0)
           : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_GENERIC, 8>, 256, 0);
     } else {
         e = rule == R_LIN_HALF ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_LIN_HALF, 4>, 256, 0)
           : rule == R_EO_FAST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_EO_FAST, 4>, 256, 0)
+          : rule == R_LIN_FAST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_LIN_FAST, 4>, 256, 0)
           : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_GENERIC, 4>, 256, 0);
     }
     if (e != cudaSuccess) return 0;
@@ -661,6 +812,7 @@ cudaError_t launch_resident(int rule, int V, const ResidentArgsHost& h, const De
         case R_LIN_HALF: return V == 8 ? resident_v<R_LIN_HALF, 8>(h, r, st) : resident_v<R_LIN_HALF, 4>(h, r, st);
         case R_EO_FAST: return V == 8 ? resident_v<R_EO_FAST, 8>(h, r, st) : resident_v<R_EO_FAST, 4>(h, r, st);
         case R_GENERIC: return V == 8 ? resident_v<R_GENERIC, 8>(h, r, st) : resident_v<R_GENERIC, 4>(h, r, st);
+        case R_LIN_FAST: return V == 8 ? resident_v<R_LIN_FAST, 8>(h, r, st) : resident_v<R_LIN_FAST, 4>(h, r, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -674,6 +826,7 @@ cudaError_t launch_warp_ensemble(int rule, int V, int32_t* q, int64_t batch, int
         case R_LIN_HALF: return warp_rule<R_LIN_HALF>(V, q, batch, nsteps, bmode, r, st);
         case R_EO_FAST: return warp_rule<R_EO_FAST>(V, q, batch, nsteps, bmode, r, st);
         case R_GENERIC: return warp_rule<R_GENERIC>(V, q, batch, nsteps, bmode, r, st);
+        case R_LIN_FAST: return warp_rule<R_LIN_FAST>(V, q, batch, nsteps, bmode, r, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -698,6 +851,7 @@ cudaError_t launch_cta_ensemble(int rule, int32_t* q, int64_t n, int64_t batch, 
         case R_LIN_HALF: return cta_rule<R_LIN_HALF>(q, n, batch, nsteps, bmode, r, st);
         case R_EO_FAST: return cta_rule<R_EO_FAST>(q, n, batch, nsteps, bmode, r, st);
         case R_GENERIC: return cta_rule<R_GENERIC>(q, n, batch, nsteps, bmode, r, st);
+        case R_LIN_FAST: return cta_rule<R_LIN_FAST>(q, n, batch, nsteps, bmode, r, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -710,6 +864,7 @@ cudaError_t launch_transfer(int rule, const int32_t* q, int32_t* pp, int32_t* pm
         case R_LIN_HALF: k_transfer<R_LIN_HALF><<<g, 256, 0, st>>>(q, pp, pm, n, r); break;
         case R_EO_FAST: k_transfer<R_EO_FAST><<<g, 256, 0, st>>>(q, pp, pm, n, r); break;
         case R_GENERIC: k_transfer<R_GENERIC><<<g, 256, 0, st>>>(q, pp, pm, n, r); break;
+        case R_LIN_FAST: k_transfer<R_LIN_FAST><<<g, 256, 0, st>>>(q, pp, pm, n, r); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -105,6 +105,23 @@ __device__ __forceinline__ void eo_gm(int32_t q, int32_t& g, int32_t& m, const D
 #endif
 }
 
+// LINEAR |kappa| = P/Q <= 1: phi(q) = sign(kappa q) floor((2P|q| + Q)/(2Q)), for
+// |q| < 2^24 and |kappa q| <= 2^20 (planner), with the EO scheme: est = rint(|q_f| cf)
+// (one FFMA, cf <= |kappa|(1 - 2^-21)) is g or g - 1, corrected by the sign of
+// u = 2Q - 1 - (2P|q| + Q - 2Q est) computed modulo 2^32.
+__device__ __forceinline__ int32_t lin_phi(int32_t q, const DevRule& r)
+{
+    const float af = fabsf(__int2float_rn(q));                            // exact
+    const float t = __fmaf_rn(af, r.eo_cf, 12582912.0f);                 // 0x4B400000 + est
+    const int32_t bits = __float_as_int(t);
+    const int32_t a = q < 0 ? -q : q;
+    int32_t u = imad(a, r.eo_ntwoP, r.eo_c1);
+    u = imad(bits, r.eo_twoQ, u);
+    const int32_t g = imad(bits + (int32_t)((uint32_t)u >> 31), r.one, (int32_t)0xB4C00000);
+    const int32_t sgn = q >> 31;                                          // -1 for q < 0
+    return (g ^ sgn) - sgn;                                               // sign(q) g
+}
+
 // (g, m) with g = phi+(q) + phi-(q) and m = phi-(q); phi+(q) = g - m.
 // The step uses F_{j+1/2} = phi+(q_j) + phi-(q_{j+1}) = g_j - m_j + m_{j+1} (one IADD3).
 template <int RULE>
@@ -116,6 +133,11 @@ __device__ __forceinline__ void phi_gm(int32_t q, int32_t& g, int32_t& m, const 
         m = 0;
     } else if (RULE == R_EO_FAST) {
         eo_gm(q, g, m, r);               // phi-(q) = g for q < 0, phi+(q) = g for q > 0, g(0) = 0
+    } else if (RULE == R_LIN_FAST) {
+        // a > 0: phi+ = RHA(kappa q) = v, phi- = 0;  a < 0: phi+ = 0, phi- = RHA(kappa q) = -v
+        const int32_t v = lin_phi(q, r);
+        if (r.lin_minus) { g = -v; m = -v; }
+        else { g = v; m = 0; }
     } else {
         const int32_t p = generic_phi(q, r.c2p, r.c1p, r.denp, r.suppp, r.rounding);
         m = generic_phi(q, r.c2m, r.c1m, r.denm, r.suppm, r.rounding);

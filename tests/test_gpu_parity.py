@@ -444,3 +444,66 @@ def test_split_domain_fused_p2p_virtual_ranks(F):
         ring.step(31)                                   # second call: tags continue
         got = np.concatenate([host(ring.owned(i)) for i in range(P)])
         assert np.array_equal(got, ref2), (P, H)
+
+
+# ---------------------------------------------------------------------------
+# 2D directional composition (Thm P:364-401; NEXT-f3)
+RULES2D = [  # kind, delta, dt/dx, dt/dy, ax, ay, amplitude, offset
+    (W.LINEAR, "1e-3", Fraction(1, 4), Fraction(1, 5), 1, 1, 3000, 0),
+    (W.LINEAR, "1e-3", Fraction(1, 3), Fraction(1, 4), -1, 1, 3000, 100),
+    (W.BURGERS_EO, "1e-5", Fraction(2, 15), Fraction(1, 10), 1, 1, 100000, 20000),
+    (W.BURGERS_EO, "1e-5", Fraction(2, 15), Fraction(2, 15), 1, 1, 100000, 20000),
+]
+
+
+def _field2d(rng, ny, nx, amp, off):
+    x = W.cell_centres(nx)[None, :]
+    y = W.cell_centres(ny)[:, None]
+    u = off + amp * 0.5 * (np.sin(2 * np.pi * x + rng.uniform(0, 6)) *
+                           np.cos(2 * np.pi * 2 * y + rng.uniform(0, 6)))
+    return (np.rint(u) + rng.integers(-amp // 50, amp // 50 + 1, (ny, nx))).astype(np.int64)
+
+
+@pytest.mark.parametrize("case", range(len(RULES2D)))
+@pytest.mark.parametrize("boundary", [W.PERIODIC, W.TRANSMISSIVE])
+@pytest.mark.parametrize("shape", [(33, 129), (70, 300), (257, 1000)])
+def test_2d_matches_oracle(F, case, boundary, shape):
+    kind, d, lx, ly, ax, ay, amp, off = RULES2D[case]
+    ny, nx = shape
+    rng = np.random.default_rng(ny * 7 + nx + case)
+    q0 = _field2d(rng, ny, nx, amp, off)
+    r = oracle.Rule2D(kind, d, lx, ly, ax, ay)
+    for nsteps, k in ((1, 0), (5, 0), (13, 0), (13, 1), (9, 3)):
+        plan = F.fqnm_plan_2d(nx, ny, float(Fraction(d)), float(lx), float(ly), kind, boundary,
+                              float(ax), float(ay))
+        assert plan.info()["kernel"] == 7
+        if k:
+            F.fqnm_debug_override(plan, 0, k, 0)
+        q = to_dev(q0)
+        F.fqnm_step(plan, q, nsteps)
+        assert np.array_equal(host(q), r.run(q0, nsteps, boundary)), (nsteps, k)
+
+
+@pytest.mark.parametrize("lam,a", [(Fraction(7, 9), 1), (Fraction(1, 3), -1), (Fraction(1, 4), 1),
+                                   (Fraction(3, 10), 1)])
+def test_lin_fast_maps_and_families(F, lam, a):
+    """R_LIN_FAST (general |kappa| <= 1, float estimate + exact remainder): the
+    kernels' maps exhaustively over the declared range, and every family's run."""
+    A = min(3_000_000, int(Fraction(1 << 20) / lam))        # the fast path's domain
+    plan = F.fqnm_plan_ex(1 << 20, 1e-3, float(lam), W.LINEAR, flux_param=float(a), q_range=(-A, A))
+    assert plan.info()["rule"] == 4
+    r = oracle.Rule(W.LINEAR, "1e-3", lam, a)
+    q = torch.arange(-A, A + 1, dtype=torch.int32, device=DEV)
+    p, m = F.fqnm_transfer_device(plan, q)
+    qh = np.arange(-A, A + 1, dtype=np.int64)
+    assert np.array_equal(host(p), r.phi_plus(qh)) and np.array_equal(host(m), r.phi_minus(qh))
+    rng = np.random.default_rng(int(lam * 100))
+    for n, fams in ((1024, (3, 4, 1)), (5000, (4, 1)), (70001, (6, 2, 1)), (400003, (2,))):
+        q0 = np.clip(W.smooth_random(rng, n, 2 * A // 3, 0), -A, A)
+        ref = r.run(q0, 37)
+        for fam in fams:
+            pl = F.fqnm_plan_ex(n, 1e-3, float(lam), W.LINEAR, flux_param=float(a), q_range=(-A, A))
+            F.fqnm_debug_override(pl, fam)
+            qd = to_dev(q0)
+            F.fqnm_step(pl, qd, 37)
+            assert np.array_equal(host(qd), ref), (n, fam)

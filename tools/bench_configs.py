@@ -34,7 +34,7 @@ def timed(plan, q0, steps, reps=3):
 def main():
     names = sys.argv[1:] or ["cfg1", "cfg2", "cfg3", "ens1", "cfg5"]
     for name in names:
-        w = W.cfg(name)
+        w = W.cfg(name) if name in W.CONFIG_NAMES else None
         if name == "cfg1":
             q0 = torch.tensor(W.q0_cfg1(), dtype=torch.int32, device="cuda")
             plan = F.fqnm_plan(w.n, 1e-4, W.dt_dx_double(w), F.LINEAR, F.PERIODIC)
@@ -61,6 +61,25 @@ def main():
             if os.environ.get("EULER_V"):
                 F.fqnm_debug_override(plan, 0, 0, int(os.environ["EULER_V"]))
             steps, cells = int(os.environ.get("CFG5_STEPS", 2000)), w.n
+        elif name in ("eo2d", "lin2d"):
+            # 2D directional composition (NEXT-f3): 8192 x 8192 cells, 200 steps
+            nx = ny = int(os.environ.get("N2D", 8192))
+            rng = np.random.default_rng(5)
+            x = W.cell_centres(nx)[None, :]
+            y = W.cell_centres(ny)[:, None]
+            if name == "eo2d":
+                u = 0.2 + 0.5 * np.sin(2 * np.pi * x) * np.cos(2 * np.pi * y)
+                q0 = torch.tensor(W.quantise(u, 1e-6), dtype=torch.int32, device="cuda")
+                qmax = int(q0.abs().max())
+                lam = 0.4 / (1e-6 * qmax) / 2          # nu = 0.4 per direction, split over 2 dims
+                plan = F.fqnm_plan_2d(nx, ny, 1e-6, lam, lam, F.BURGERS_EO, F.PERIODIC)
+            else:
+                u = np.exp(-((x - 0.5) ** 2 + (y - 0.5) ** 2) / 0.01)
+                q0 = torch.tensor(W.quantise(u, 1e-6), dtype=torch.int32, device="cuda")
+                plan = F.fqnm_plan_2d(nx, ny, 1e-6, 0.25, 0.25, F.LINEAR, F.PERIODIC)
+            if os.environ.get("K2D"):
+                F.fqnm_debug_override(plan, 0, int(os.environ["K2D"]), 0)
+            steps, cells = 200, nx * ny
         else:
             raise SystemExit(f"unknown config {name}")
         ms, q = timed(plan, q0, steps, reps=1 if name == "cfg5" else 3)
