@@ -76,6 +76,25 @@ class PlanInfo(ctypes.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
+class LevelStats(ctypes.Structure):
+    _fields_ = [("S", ctypes.c_double), ("N_eff", ctypes.c_double),
+                ("occupied", ctypes.c_int64), ("outside", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class TransitionStats(ctypes.Structure):
+    _fields_ = [("before", LevelStats), ("after", LevelStats), ("rho", ctypes.c_double),
+                ("dS", ctypes.c_double), ("nonzeros", ctypes.c_int64),
+                ("overflow", ctypes.c_int64)]
+
+    def as_dict(self):
+        d = {f: getattr(self, f) for f, _ in self._fields_}
+        d["before"], d["after"] = self.before.as_dict(), self.after.as_dict()
+        return d
+
+
 _lib = None
 
 
@@ -118,6 +137,8 @@ def _load():
     L.fqnm_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
     L.fqnm_ipc_close.argtypes = [vp]
     L.fqnm_launch_count.argtypes = [vp]
+    L.fqnm_levels.argtypes = [vp, vp, i64, i64, vp, ctypes.POINTER(LevelStats)]
+    L.fqnm_transitions.argtypes = [vp, vp, vp, i64, i64, ctypes.POINTER(TransitionStats)]
     L.fqnm_launch_count.restype = i64
     L.fqnm_last_error.restype = ctypes.c_char_p
     L.fqnm_status_str.restype = ctypes.c_char_p
@@ -358,6 +379,36 @@ def fqnm_step_host(plan: Plan, q_host, nsteps: int):
         raise TypeError("q_host must be a contiguous numpy array or CPU tensor")
     _check(L.fqnm_step_host(plan.handle, ctypes.c_void_p(a.ctypes.data), int(nsteps)))
     return a
+
+
+def fqnm_levels(plan: Plan, q, lo: int, hi: int, counts=None) -> dict:
+    """Level histogram statistics of q (SI Eq. pk / discrete_entropy / neff):
+    {S, N_eff, occupied, outside}; `counts` (optional uint32-sized int32 CUDA
+    tensor of hi - lo + 1) receives c_k."""
+    import torch
+    L = _load()
+    ptr = _dev_ptr(q, plan.dtype, "q")
+    cptr = None
+    if counts is not None:
+        if counts.numel() != hi - lo + 1 or counts.element_size() != 4:
+            raise ValueError("counts must hold hi - lo + 1 32-bit entries")
+        cptr = _dev_ptr(counts, None, "counts")
+    st = LevelStats()
+    _check(L.fqnm_set_stream(plan.handle, _stream_ptr(q)))
+    _check(L.fqnm_levels(plan.handle, ptr, int(lo), int(hi), cptr, ctypes.byref(st)))
+    return st.as_dict()
+
+
+def fqnm_transitions(plan: Plan, q0, q1, lo: int, hi: int) -> dict:
+    """Level-transition statistics q0 -> q1 (SI Def. level_transition, row-sum
+    defect rho): {before, after, rho, dS, nonzeros, overflow}."""
+    L = _load()
+    p0 = _dev_ptr(q0, plan.dtype, "q0")
+    p1 = _dev_ptr(q1, plan.dtype, "q1")
+    st = TransitionStats()
+    _check(L.fqnm_set_stream(plan.handle, _stream_ptr(q0)))
+    _check(L.fqnm_transitions(plan.handle, p0, p1, int(lo), int(hi), ctypes.byref(st)))
+    return st.as_dict()
 
 
 def _numel(plan: Plan) -> int:

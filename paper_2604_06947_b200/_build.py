@@ -23,6 +23,7 @@ UNITS = {
     "fqnm_api.cu": [],
     "kernels_scalar.cu": [],
     "kernels_euler.cu": ["-fmad=false"],
+    "kernels_diag.cu": [],
 }
 HEADERS = ["fqnm_internal.h", "maps.cuh"]
 

@@ -1078,6 +1078,123 @@ extern "C" int fqnm_step_host(fqnm_plan_t* p, void* q_host, int64_t nsteps)
     return FQNM_OK;
 }
 
+// ---- level-space diagnostics ----------------------------------------------
+struct DevScratch {                       // small RAII bundle for the synchronous diagnostics
+    std::vector<void*> ptrs;
+    ~DevScratch() { for (void* x : ptrs) cudaFree(x); }
+    template <typename T> cudaError_t alloc(T** out, size_t count)
+    {
+        cudaError_t e = cudaMalloc((void**)out, count * sizeof(T));
+        if (e == cudaSuccess) ptrs.push_back(*out);
+        return e;
+    }
+};
+
+// The level channel: the whole state of a scalar plan (one contiguous segment),
+// the density component (var 0) of each problem of an Euler plan.
+struct LevelSegments {
+    int64_t count, len, stride;   // elements
+};
+static LevelSegments level_segments(const fqnm_plan_desc& d)
+{
+    if (d.nvar == 1) return {1, (int64_t)state_elems(d), 0};
+    return {d.batch, d.n_local, (int64_t)d.nvar * d.n_local};
+}
+static const void* seg_ptr(const fqnm_plan_t* p, const void* q, int64_t s, int64_t stride)
+{
+    return (const char*)q + (size_t)(s * stride) * elem_size(p->d);
+}
+
+static int levels_impl(const fqnm_plan_t* p, const void* q, int64_t lo, int64_t L,
+                       unsigned int* counts, fqnm_level_stats* out)
+{
+    const LevelSegments sg = level_segments(p->d);
+    const int64_t n = sg.count * sg.len;
+    DevScratch sc;
+    unsigned long long* dull = nullptr;     // [0] outside, [1] occupied
+    double* dacc = nullptr;
+    CUDA_TRY(sc.alloc(&dull, 2));
+    CUDA_TRY(sc.alloc(&dacc, 1));
+    CUDA_TRY(cudaMemsetAsync(dull, 0, 2 * sizeof(unsigned long long), p->st));
+    CUDA_TRY(cudaMemsetAsync(dacc, 0, sizeof(double), p->st));
+    CUDA_TRY(cudaMemsetAsync(counts, 0, (size_t)L * sizeof(unsigned int), p->st));
+    for (int64_t b = 0; b < sg.count; ++b)
+        CUDA_TRY(launch_histogram(seg_ptr(p, q, b, sg.stride), p->d.dtype, sg.len, lo, L, counts, dull,
+                                  p->st));
+    CUDA_TRY(launch_clogc(counts, L, dacc, dull + 1, p->st));
+    unsigned long long h[2];
+    double acc;
+    CUDA_TRY(cudaMemcpyAsync(h, dull, sizeof h, cudaMemcpyDeviceToHost, p->st));
+    CUDA_TRY(cudaMemcpyAsync(&acc, dacc, sizeof acc, cudaMemcpyDeviceToHost, p->st));
+    CUDA_TRY(cudaStreamSynchronize(p->st));
+    const double N = (double)(n - (int64_t)h[0]);
+    out->outside = (int64_t)h[0];
+    out->occupied = (int64_t)h[1];
+    out->S = N > 0 ? std::log(N) - acc / N : 0.0;     // -sum (c/N) log(c/N)
+    out->N_eff = std::exp(out->S);
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_levels(const fqnm_plan_t* p, const void* q, int64_t lo, int64_t hi,
+                           uint32_t* counts_dev, fqnm_level_stats* out)
+{
+    if (!p || !q || !out) return fail(FQNM_ERR_ARG, "null argument");
+    if (p->d.boundary == FQNM_HALO)
+        return fail(FQNM_ERR_UNSUPPORTED, "level diagnostics: non-halo plans only");
+    if (hi < lo || hi - lo > ((int64_t)1 << 30)) return fail(FQNM_ERR_ARG, "need lo <= hi, hi - lo <= 2^30");
+    const int64_t L = hi - lo + 1;
+    DevScratch sc;
+    unsigned int* counts = counts_dev;
+    if (!counts) CUDA_TRY(sc.alloc(&counts, (size_t)L));
+    return levels_impl(p, q, lo, L, counts, out);
+}
+
+extern "C" int fqnm_transitions(const fqnm_plan_t* p, const void* q0, const void* q1, int64_t lo,
+                                int64_t hi, fqnm_transition_stats* out)
+{
+    if (!p || !q0 || !q1 || !out) return fail(FQNM_ERR_ARG, "null argument");
+    if (p->d.boundary == FQNM_HALO)
+        return fail(FQNM_ERR_UNSUPPORTED, "level diagnostics: non-halo plans only");
+    if (hi < lo || hi - lo > ((int64_t)1 << 30)) return fail(FQNM_ERR_ARG, "need lo <= hi, hi - lo <= 2^30");
+    const int64_t L = hi - lo + 1;
+    const LevelSegments sg = level_segments(p->d);
+    const int64_t n = sg.count * sg.len;
+    DevScratch sc;
+    unsigned int *c0 = nullptr, *c1 = nullptr, *vals = nullptr;
+    unsigned long long *keys = nullptr, *dull = nullptr;   // dull: [0] overflow [1] npairs [2] maxbits
+    double* rowsum = nullptr;
+    unsigned long long cap = 1024;
+    while (cap < 2ull * (unsigned long long)n) cap <<= 1;
+    CUDA_TRY(sc.alloc(&c0, (size_t)L));
+    CUDA_TRY(sc.alloc(&c1, (size_t)L));
+    CUDA_TRY(sc.alloc(&keys, cap));
+    CUDA_TRY(sc.alloc(&vals, cap));
+    CUDA_TRY(sc.alloc(&rowsum, (size_t)L));
+    CUDA_TRY(sc.alloc(&dull, 3));
+    int rc;
+    if ((rc = levels_impl(p, q0, lo, L, c0, &out->before)) != FQNM_OK) return rc;
+    if ((rc = levels_impl(p, q1, lo, L, c1, &out->after)) != FQNM_OK) return rc;
+    CUDA_TRY(cudaMemsetAsync(keys, 0xff, cap * sizeof(unsigned long long), p->st));
+    CUDA_TRY(cudaMemsetAsync(vals, 0, cap * sizeof(unsigned int), p->st));
+    CUDA_TRY(cudaMemsetAsync(rowsum, 0, (size_t)L * sizeof(double), p->st));
+    CUDA_TRY(cudaMemsetAsync(dull, 0, 3 * sizeof(unsigned long long), p->st));
+    for (int64_t b = 0; b < sg.count; ++b)
+        CUDA_TRY(launch_pairs(seg_ptr(p, q0, b, sg.stride), seg_ptr(p, q1, b, sg.stride), p->d.dtype,
+                              sg.len, lo, L, keys, vals, cap, dull, p->st));
+    CUDA_TRY(launch_rowsums(keys, vals, cap, L, c0, rowsum, dull + 1, p->st));
+    CUDA_TRY(launch_defect(rowsum, c0, c1, L, dull + 2, p->st));
+    unsigned long long h[3];
+    CUDA_TRY(cudaMemcpyAsync(h, dull, sizeof h, cudaMemcpyDeviceToHost, p->st));
+    CUDA_TRY(cudaStreamSynchronize(p->st));
+    out->overflow = (int64_t)h[0];
+    out->nonzeros = (int64_t)h[1];
+    double rho;
+    std::memcpy(&rho, &h[2], sizeof rho);
+    out->rho = rho;
+    out->dS = out->after.S - out->before.S;
+    return FQNM_OK;
+}
+
 extern "C" int fqnm_get_info(const fqnm_plan_t* p, fqnm_plan_info* info)
 {
     if (!p || !info) return fail(FQNM_ERR_ARG, "null argument");

@@ -100,6 +100,20 @@ struct Step2DArgs {
 cudaError_t launch_step2d(int rule, bool same, const Step2DArgs& a, const DevRule& rx,
                           const DevRule& ry, cudaStream_t st);
 
+// level-space diagnostics (kernels_diag.cu)
+cudaError_t launch_histogram(const void* q, int dtype, int64_t n, int64_t lo, int64_t L,
+                             unsigned int* counts, unsigned long long* outside, cudaStream_t st);
+cudaError_t launch_clogc(const unsigned int* counts, int64_t L, double* acc,
+                         unsigned long long* occupied, cudaStream_t st);
+cudaError_t launch_pairs(const void* q0, const void* q1, int dtype, int64_t n, int64_t lo, int64_t L,
+                         unsigned long long* keys, unsigned int* vals, unsigned long long cap,
+                         unsigned long long* overflow, cudaStream_t st);
+cudaError_t launch_rowsums(const unsigned long long* keys, const unsigned int* vals,
+                           unsigned long long cap, int64_t L, const unsigned int* c0, double* rowsum,
+                           unsigned long long* npairs, cudaStream_t st);
+cudaError_t launch_defect(const double* rowsum, const unsigned int* c0, const unsigned int* c1,
+                          int64_t L, unsigned long long* maxbits, cudaStream_t st);
+
 // kernel launchers (kernels_scalar.cu / kernels_euler.cu); return cudaError_t
 cudaError_t launch_blocked(int rule, int V, int minb, const BlockedArgs& a, const DevRule& r,
                            cudaStream_t st, int grid_cap);
