@@ -10,6 +10,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -21,11 +22,12 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", CSRC, "-I", INCLUDE]
 UNITS = {
     "fqnm_api.cu": [],
-    "kernels_scalar.cu": [],
+    # kernels_scalar.cu is compiled as 8 parts (separate translation units) in parallel
+    **{f"kernels_scalar_p{k}.cu": [] for k in range(1, 9)},
     "kernels_euler.cu": ["-fmad=false"],
     "kernels_diag.cu": [],
 }
-HEADERS = ["fqnm_internal.h", "maps.cuh"]
+HEADERS = ["fqnm_internal.h", "maps.cuh", "kernels_scalar.cu"]
 
 
 def _stale(obj: str, src: str) -> bool:
@@ -42,7 +44,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False,
     objdir = objdir or os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
-    rebuilt = False
+    cmds = []
     for unit, extra in UNITS.items():
         src = os.path.join(CSRC, unit)
         obj = os.path.join(objdir, unit.replace(".cu", ".o"))
@@ -53,8 +55,11 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False,
                 cmd[1:1] = ["-Xptxas", "-v"]
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
-            subprocess.check_call(cmd)
-            rebuilt = True
+            cmds.append(cmd)
+    rebuilt = bool(cmds)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        for f in [ex.submit(subprocess.check_call, c) for c in cmds]:
+            f.result()
     if rebuilt or force or not os.path.exists(lib):
         tmp = lib + f".{os.getpid()}.tmp"
         subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static"])

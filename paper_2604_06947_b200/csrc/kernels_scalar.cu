@@ -23,6 +23,13 @@
 #include "fqnm_internal.h"
 #include "maps.cuh"
 
+// The launchers are split into parts so the build compiles them as separate
+// translation units in parallel (kernels_scalar_p*.cu); part 0 = everything.
+#ifndef FQNM_SCALAR_PART
+#define FQNM_SCALAR_PART 0
+#endif
+#define FQNM_PART(x) (FQNM_SCALAR_PART == 0 || FQNM_SCALAR_PART == (x))
+
 #ifndef FQNM_RES_FENCE
 #define FQNM_RES_FENCE 0
 #endif
@@ -149,7 +156,7 @@ __device__ __forceinline__ void p2p_signal(unsigned int* flag, uint32_t tag)
 
 // push the H edge cells of `ext` (layout [H | n | H]) that `owned0` / the window
 // covers into the neighbours' buffers and release `tag` on their flags
-__device__ __noinline__ void p2p_push(const BlockedArgs& a, const int32_t* ext, bool left_edge,
+static __device__ __noinline__ void p2p_push(const BlockedArgs& a, const int32_t* ext, bool left_edge,
                                       bool right_edge, uint32_t tag, int32_t* peer_l,
                                       int32_t* peer_r, int lane)
 {
@@ -170,17 +177,20 @@ __device__ __noinline__ void p2p_push(const BlockedArgs& a, const int32_t* ext, 
 }
 
 // initial halos of a split run: every rank pushes the edges of its current buffer
-__global__ void k_halo_prime(BlockedArgs a)
+static __global__ void k_halo_prime(BlockedArgs a)
 {
     const int lane = threadIdx.x & 31;
     p2p_push(a, a.src, true, true, a.tag, a.peer_left_dst, a.peer_right_dst, lane);
 }
 
+#if FQNM_PART(1)
 cudaError_t launch_halo_prime(const BlockedArgs& a, cudaStream_t st)
 {
     k_halo_prime<<<1, 32, 0, st>>>(a);
     return cudaGetLastError();
 }
+
+#endif  // part 1
 
 // Slow window (periodic wrap, transmissive walls, ragged tails, misaligned
 // batches): scalar loads through wrap_index, guarded scalar stores.  Kept out of
@@ -508,6 +518,7 @@ __global__ void __launch_bounds__(512) k_step2d(Step2DArgs a, DevRule rx, DevRul
         }
 }
 
+#if FQNM_PART(2)
 template <int RULE, bool SAME>
 static cudaError_t step2d_rule(const Step2DArgs& a, const DevRule& rx, const DevRule& ry,
                                cudaStream_t st)
@@ -545,6 +556,8 @@ cudaError_t launch_step2d(int rule, bool same, const Step2DArgs& a, const DevRul
         default: return cudaErrorInvalidValue;
     }
 }
+
+#endif  // part 2
 
 // ---------------------------------------------------------------------------
 // K3: one problem of 32*V cells per warp, all steps in registers
@@ -667,7 +680,7 @@ __global__ void k_observe(const T* __restrict__ q, double delta, double* __restr
 
 // ---------------------------------------------------------------------------
 // launchers
-static int grid_for(int64_t work, int threads, int cap)
+static inline int grid_for(int64_t work, int threads, int cap)
 {
     int64_t g = (work + threads - 1) / threads;
     if (g > cap) g = cap;
@@ -676,7 +689,7 @@ static int grid_for(int64_t work, int threads, int cap)
 }
 
 template <int RULE, int V, int MINB>
-static cudaError_t blocked_v(const BlockedArgs& a, const DevRule& r, cudaStream_t st, int cap)
+cudaError_t blocked_v(const BlockedArgs& a, const DevRule& r, cudaStream_t st, int cap)
 {
     const int threads = 256;
     int64_t warps = a.nwin * a.batch;
@@ -687,7 +700,7 @@ static cudaError_t blocked_v(const BlockedArgs& a, const DevRule& r, cudaStream_
 
 // minb: __launch_bounds__ min blocks per SM (register cap), 0 = default
 template <int RULE>
-static cudaError_t blocked_rule(int V, int minb, const BlockedArgs& a, const DevRule& r,
+cudaError_t blocked_rule(int V, int minb, const BlockedArgs& a, const DevRule& r,
                                 cudaStream_t st, int cap)
 {
     if (minb) {
@@ -704,6 +717,34 @@ static cudaError_t blocked_rule(int V, int minb, const BlockedArgs& a, const Dev
     }
 }
 
+// per-rule instantiations of the blocked kernels, one translation unit each
+#if FQNM_PART(1)
+template cudaError_t blocked_rule<R_LIN_HALF>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
+#endif
+#if FQNM_PART(5)
+template cudaError_t blocked_rule<R_EO_FAST>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
+#endif
+#if FQNM_PART(8)
+template cudaError_t blocked_v<R_GENERIC, 32, 1>(const BlockedArgs&, const DevRule&, cudaStream_t, int);
+template cudaError_t blocked_v<R_GENERIC, 32, 2>(const BlockedArgs&, const DevRule&, cudaStream_t, int);
+#endif
+#if FQNM_PART(6)
+#if FQNM_SCALAR_PART == 6
+extern template cudaError_t blocked_v<R_GENERIC, 32, 1>(const BlockedArgs&, const DevRule&, cudaStream_t, int);
+extern template cudaError_t blocked_v<R_GENERIC, 32, 2>(const BlockedArgs&, const DevRule&, cudaStream_t, int);
+#endif
+template cudaError_t blocked_rule<R_GENERIC>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
+#endif
+#if FQNM_PART(7)
+template cudaError_t blocked_rule<R_LIN_FAST>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
+#endif
+
+#if FQNM_PART(1)
+#if FQNM_SCALAR_PART == 1
+extern template cudaError_t blocked_rule<R_EO_FAST>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
+extern template cudaError_t blocked_rule<R_GENERIC>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
+extern template cudaError_t blocked_rule<R_LIN_FAST>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
+#endif
 bool blocked_has_V(int V) { return V == 8 || V == 16 || V == 32; }
 int blocked_max_V() { return 32; }
 
@@ -734,6 +775,8 @@ cudaError_t launch_naive(int rule, const int32_t* src, int32_t* dst, int64_t n, 
     return cudaGetLastError();
 }
 
+#endif  // part 1
+
 template <int RULE, int V>
 static cudaError_t warp_v(int32_t* q, int64_t batch, int64_t nsteps, int bmode, const DevRule& r,
                           cudaStream_t st)
@@ -748,7 +791,7 @@ static cudaError_t warp_v(int32_t* q, int64_t batch, int64_t nsteps, int bmode, 
 }
 
 template <int RULE>
-static cudaError_t warp_rule(int V, int32_t* q, int64_t batch, int64_t nsteps, int bmode,
+cudaError_t warp_rule(int V, int32_t* q, int64_t batch, int64_t nsteps, int bmode,
                              const DevRule& r, cudaStream_t st)
 {
     switch (V) {
@@ -762,6 +805,16 @@ static cudaError_t warp_rule(int V, int32_t* q, int64_t batch, int64_t nsteps, i
     }
 }
 
+#if FQNM_PART(3)
+template cudaError_t warp_rule<R_LIN_HALF>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
+template cudaError_t warp_rule<R_EO_FAST>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
+template cudaError_t warp_rule<R_LIN_FAST>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
+#endif
+#if FQNM_PART(4)
+template cudaError_t warp_rule<R_GENERIC>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
+#endif
+
+#if FQNM_PART(2)
 template <int RULE, int V>
 static cudaError_t resident_v(const ResidentArgsHost& h, const DevRule& r, cudaStream_t st)
 {
@@ -817,6 +870,12 @@ cudaError_t launch_resident(int rule, int V, const ResidentArgsHost& h, const De
     }
 }
 
+#endif  // part 2
+
+#if FQNM_PART(3)
+#if FQNM_SCALAR_PART == 3
+extern template cudaError_t warp_rule<R_GENERIC>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
+#endif
 bool warp_ensemble_has_V(int V) { return V == 1 || V == 2 || V == 4 || V == 8 || V == 16 || V == 32; }
 
 cudaError_t launch_warp_ensemble(int rule, int V, int32_t* q, int64_t batch, int64_t nsteps,
@@ -831,6 +890,9 @@ cudaError_t launch_warp_ensemble(int rule, int V, int32_t* q, int64_t batch, int
     }
 }
 
+#endif  // part 3
+
+#if FQNM_PART(2)
 template <int RULE>
 static cudaError_t cta_rule(int32_t* q, int64_t n, int64_t batch, int64_t nsteps, int bmode,
                             const DevRule& r, cudaStream_t st)
@@ -856,6 +918,9 @@ cudaError_t launch_cta_ensemble(int rule, int32_t* q, int64_t n, int64_t batch, 
     }
 }
 
+#endif  // part 2
+
+#if FQNM_PART(1)
 cudaError_t launch_transfer(int rule, const int32_t* q, int32_t* pp, int32_t* pm, int64_t n,
                             const DevRule& r, cudaStream_t st)
 {
@@ -890,5 +955,7 @@ cudaError_t launch_observe(const void* q, int dtype, double delta, double* u, in
         k_observe<int64_t><<<g, 256, 0, st>>>((const int64_t*)q, delta, u, n);
     return cudaGetLastError();
 }
+
+#endif  // part 1
 
 }  // namespace fqnm

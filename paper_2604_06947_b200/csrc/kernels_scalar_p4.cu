@@ -1,0 +1,3 @@
+// Part 4 of kernels_scalar.cu, compiled as its own translation unit (see _build.py).
+#define FQNM_SCALAR_PART 4
+#include "kernels_scalar.cu"
