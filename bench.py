@@ -34,7 +34,14 @@ import numpy as np
 
 METRIC = "integer cell-updates/sec (GCUPS)"
 UNIT = "GCUPS"
-OPS_ALG = {"burgers_eo": 16, "linear": 4}      # SURVEY §8(d)-D3 algorithmic ops per cell-update
+# Algorithmic operations per cell-update (DESIGN.md §6 "ops_alg"): the exact closed form's
+# own operations, not counting redundant halo work, shuffles, loads/stores or loop control.
+# EO with P = 1 (every BJ Burgers config): int->float, q^2 (FMUL), estimate (FFMA), remainder
+# (2 IMAD), correction (LEA), sign mask (SHF), phi- (LOP3), interface transfer + update
+# (2 IADD3) = 10.  SURVEY §8(d)-D3's a-priori 16 over-counts this closed form (it made the
+# fraction exceed 1.0).  General P adds one IMAD (11).  Linear kappa = 1/2: 4.
+OPS_ALG = {"burgers_eo": 10, "burgers_eo_general_p": 11, "linear": 4}
+RULE_NAMES = {1: "LIN_HALF", 2: "EO_FAST", 3: "GENERIC", 4: "LIN_FAST", 5: "EO_P1"}
 SM_COUNT = 148
 LANES_PER_SM_CLK = 128                          # 4 SMSPs x 32 lanes, 1 warp-instr/clk each
 
@@ -310,13 +317,15 @@ def main():
     peak_ops = SM_COUNT * LANES_PER_SM_CLK * f_max                    # int lane-ops/s at max clock
     per_launch_ms = kern_ms / max(kern_launches, 1)
     updates_per_launch = n_local * T * args.steps / max(kern_launches, 1)
-    achieved_ops = OPS_ALG["burgers_eo"] * updates_per_launch / (per_launch_ms / 1e3)
+    ops_alg = OPS_ALG["burgers_eo"] if info["rule"] == 5 else OPS_ALG["burgers_eo_general_p"]
+    achieved_ops = ops_alg * updates_per_launch / (per_launch_ms / 1e3)
     hbm_bytes_per_launch = 8.0 * n_local                               # read + write int32 once per block
     roofline = {
-        "bound": "alu", "kernel": "k_blocked<EO_FAST,V=%d>" % info["cells_per_thread"],
+        "bound": "alu", "kernel": "k_blocked<%s,V=%d>" % (RULE_NAMES.get(info["rule"], "?"),
+                                                           info["cells_per_thread"]),
         "achieved": achieved_ops / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s",
         "frac": achieved_ops / peak_ops,
-        "ops_alg_per_cell_update": OPS_ALG["burgers_eo"],
+        "ops_alg_per_cell_update": ops_alg,
         "peak_basis": "148 SMs x 128 int lanes/clk x sm_max_mhz (%s)" % peak_src,
         "traffic": None,
         "traffic_source": None,

@@ -372,7 +372,7 @@ static int build_rule(fqnm_plan_t* p)
                 return fail(FQNM_ERR_RANGE, "int64 headroom exceeded on the declared range");
         }
         int64_t amax = (lo < 0 ? -lo : lo) > hi ? (lo < 0 ? -lo : lo) : hi;
-        p->rule = (eo_fast_ok && amax <= a_fast) ? R_EO_FAST : R_GENERIC;
+        p->rule = (eo_fast_ok && amax <= a_fast) ? (P == 1 ? R_EO_P1 : R_EO_FAST) : R_GENERIC;
     }
     p->lo = lo;
     p->hi = hi;
@@ -397,10 +397,13 @@ static int build_rule(fqnm_plan_t* p)
         while ((double)cf > target) cf = std::nextafterf(cf, 0.0f);
         r.eo_cf = cf;
     }
-    if (p->rule == R_EO_FAST) {
+    if (p->rule == R_EO_FAST || p->rule == R_EO_P1) {
         r.eo_ntwoP = (int32_t)(-2 * P);
         r.eo_twoQ = (int32_t)(2 * Q);
         r.eo_c1 = (int32_t)(uint32_t)((uint64_t)(Q - 1) - (uint64_t)(2 * Q) * 0x4B400000ull);
+        r.eo_nQ = (int32_t)(-Q);
+        r.eo_c6 = (int32_t)(uint32_t)((uint64_t)Q * 0x4B400001ull - (uint64_t)((Q + 1) / 2));
+        r.eo_P = (int32_t)P;
         // largest float <= kappa (1 - 2^-21): a strict relative underestimate of kappa
         const double target = ((double)P / (double)Q) * (1.0 - std::ldexp(1.0, -21));
         float cf = (float)target;
@@ -450,7 +453,7 @@ static int choose_kernel(fqnm_plan_t* p)
     if (p->family == 2) {
         const bool two = p->dep_left && p->dep_right;
         if (p->rule == R_LIN_HALF) { p->V = 32; p->k = 64; p->minb = 2; }
-        else if (p->rule == R_EO_FAST) { p->V = 32; p->k = 24; p->minb = 2; }
+        else if (p->rule == R_EO_FAST || p->rule == R_EO_P1) { p->V = 32; p->k = 24; p->minb = 2; }
         else { p->V = 8; p->k = two ? 8 : 16; }
         if (d.k > 0) p->k = d.k;
         if (d.boundary == FQNM_HALO && p->k > d.halo) p->k = (int)d.halo;

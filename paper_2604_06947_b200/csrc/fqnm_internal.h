@@ -14,6 +14,8 @@ enum RuleKind : int32_t {
     R_EO_FAST = 2,    // BURGERS_EO, RHA: g(|q|) = floor((2P q^2 + Q)/(2Q)) by float estimate +
                       // exact 32-bit remainder correction (valid range proven at plan time)
     R_GENERIC = 3,    // any piecewise-quadratic map, exact int64 arithmetic, any rounding
+    R_EO_P1 = 5,      // BURGERS_EO with P = 1 (kappa = 1/Q): as R_EO_FAST, remainder in the
+                      // (q^2 - Q est) form, one instruction shorter (maps.cuh eo_gm_p1)
     R_LIN_FAST = 4    // LINEAR any |kappa| <= 1, RHA: g(|q|) = floor((2P|q| + Q)/(2Q)) by the
                       // same estimate + remainder scheme as EO (eo_* constants), sign restored
 };
@@ -34,7 +36,10 @@ struct DevRule {
     int32_t lin_minus;    // R_LIN_FAST: 0 -> the map is phi+ (a > 0), 1 -> phi- (a < 0)
     int32_t one;          // runtime 1 and -1: let the linear kernel issue IMADs (FMA pipe)
     int32_t mone;
-    int32_t pad2;
+    // EO remainder in the (P q^2 - Q est) form (maps.cuh eo_gm_p1, P = 1)
+    int32_t eo_nQ;        // -Q
+    int32_t eo_c6;        // Q * 0x4B400001 - ceil(Q/2)  (mod 2^32)
+    int32_t eo_P;         // P
 };
 
 enum Bmode : int32_t { BM_PERIODIC = 0, BM_TRANSMISSIVE = 1, BM_HALO = 2 };

@@ -70,7 +70,10 @@ __device__ __forceinline__ void eval_maps(const int32_t (&q)[V], int32_t (&g)[V]
                                           int32_t (&m)[V], const DevRule& r)
 {
 #pragma unroll
-    for (int j = 0; j < V; ++j) phi_gm<RULE>(q[j], g[j], m[j], r);
+    for (int j = 0; j < V; j += 2) {          // odd cells may take the other pipe mix
+        phi_gm<RULE, false, true>(q[j], g[j], m[j], r);
+        if (j + 1 < V) phi_gm<RULE, true, true>(q[j + 1], g[j + 1], m[j + 1], r);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -549,6 +552,8 @@ cudaError_t launch_step2d(int rule, bool same, const Step2DArgs& a, const DevRul
                                      : step2d_rule<R_LIN_HALF, false>(a, rx, ry, st);
         case R_EO_FAST: return same ? step2d_rule<R_EO_FAST, true>(a, rx, ry, st)
                                     : step2d_rule<R_EO_FAST, false>(a, rx, ry, st);
+        case R_EO_P1: return same ? step2d_rule<R_EO_P1, true>(a, rx, ry, st)
+                                    : step2d_rule<R_EO_P1, false>(a, rx, ry, st);
         case R_GENERIC: return same ? step2d_rule<R_GENERIC, true>(a, rx, ry, st)
                                     : step2d_rule<R_GENERIC, false>(a, rx, ry, st);
         case R_LIN_FAST: return same ? step2d_rule<R_LIN_FAST, true>(a, rx, ry, st)
@@ -723,6 +728,7 @@ template cudaError_t blocked_rule<R_LIN_HALF>(int, int, const BlockedArgs&, cons
 #endif
 #if FQNM_PART(5)
 template cudaError_t blocked_rule<R_EO_FAST>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
+template cudaError_t blocked_rule<R_EO_P1>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
 #endif
 #if FQNM_PART(8)
 template cudaError_t blocked_v<R_GENERIC, 32, 1>(const BlockedArgs&, const DevRule&, cudaStream_t, int);
@@ -742,6 +748,7 @@ template cudaError_t blocked_rule<R_LIN_FAST>(int, int, const BlockedArgs&, cons
 #if FQNM_PART(1)
 #if FQNM_SCALAR_PART == 1
 extern template cudaError_t blocked_rule<R_EO_FAST>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
+extern template cudaError_t blocked_rule<R_EO_P1>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
 extern template cudaError_t blocked_rule<R_GENERIC>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
 extern template cudaError_t blocked_rule<R_LIN_FAST>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
 #endif
@@ -754,6 +761,7 @@ cudaError_t launch_blocked(int rule, int V, int minb, const BlockedArgs& a, cons
     switch (rule) {
         case R_LIN_HALF: return blocked_rule<R_LIN_HALF>(V, minb, a, r, st, grid_cap);
         case R_EO_FAST: return blocked_rule<R_EO_FAST>(V, minb, a, r, st, grid_cap);
+        case R_EO_P1: return blocked_rule<R_EO_P1>(V, minb, a, r, st, grid_cap);
         case R_GENERIC: return blocked_rule<R_GENERIC>(V, minb, a, r, st, grid_cap);
         case R_LIN_FAST: return blocked_rule<R_LIN_FAST>(V, minb, a, r, st, grid_cap);
         default: return cudaErrorInvalidValue;
@@ -768,6 +776,7 @@ cudaError_t launch_naive(int rule, const int32_t* src, int32_t* dst, int64_t n, 
     switch (rule) {
         case R_LIN_HALF: k_naive<R_LIN_HALF><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
         case R_EO_FAST: k_naive<R_EO_FAST><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
+        case R_EO_P1: k_naive<R_EO_P1><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
         case R_GENERIC: k_naive<R_GENERIC><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
         case R_LIN_FAST: k_naive<R_LIN_FAST><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
         default: return cudaErrorInvalidValue;
@@ -808,6 +817,7 @@ cudaError_t warp_rule(int V, int32_t* q, int64_t batch, int64_t nsteps, int bmod
 #if FQNM_PART(3)
 template cudaError_t warp_rule<R_LIN_HALF>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
 template cudaError_t warp_rule<R_EO_FAST>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
+template cudaError_t warp_rule<R_EO_P1>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
 template cudaError_t warp_rule<R_LIN_FAST>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
 #endif
 #if FQNM_PART(4)
@@ -843,11 +853,13 @@ int resident_capacity_warps(int rule, int V)
     if (V == 8) {
         e = rule == R_LIN_HALF ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_LIN_HALF, 8>, 256, 0)
           : rule == R_EO_FAST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_EO_FAST, 8>, 256, 0)
+          : rule == R_EO_P1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_EO_P1, 8>, 256, 0)
           : rule == R_LIN_FAST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_LIN_FAST, 8>, 256, 0)
           : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_GENERIC, 8>, 256, 0);
     } else {
         e = rule == R_LIN_HALF ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_LIN_HALF, 4>, 256, 0)
           : rule == R_EO_FAST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_EO_FAST, 4>, 256, 0)
+          : rule == R_EO_P1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_EO_P1, 4>, 256, 0)
           : rule == R_LIN_FAST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_LIN_FAST, 4>, 256, 0)
           : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_GENERIC, 4>, 256, 0);
     }
@@ -864,6 +876,7 @@ cudaError_t launch_resident(int rule, int V, const ResidentArgsHost& h, const De
     switch (rule) {
         case R_LIN_HALF: return V == 8 ? resident_v<R_LIN_HALF, 8>(h, r, st) : resident_v<R_LIN_HALF, 4>(h, r, st);
         case R_EO_FAST: return V == 8 ? resident_v<R_EO_FAST, 8>(h, r, st) : resident_v<R_EO_FAST, 4>(h, r, st);
+        case R_EO_P1: return V == 8 ? resident_v<R_EO_P1, 8>(h, r, st) : resident_v<R_EO_P1, 4>(h, r, st);
         case R_GENERIC: return V == 8 ? resident_v<R_GENERIC, 8>(h, r, st) : resident_v<R_GENERIC, 4>(h, r, st);
         case R_LIN_FAST: return V == 8 ? resident_v<R_LIN_FAST, 8>(h, r, st) : resident_v<R_LIN_FAST, 4>(h, r, st);
         default: return cudaErrorInvalidValue;
@@ -884,6 +897,7 @@ cudaError_t launch_warp_ensemble(int rule, int V, int32_t* q, int64_t batch, int
     switch (rule) {
         case R_LIN_HALF: return warp_rule<R_LIN_HALF>(V, q, batch, nsteps, bmode, r, st);
         case R_EO_FAST: return warp_rule<R_EO_FAST>(V, q, batch, nsteps, bmode, r, st);
+        case R_EO_P1: return warp_rule<R_EO_P1>(V, q, batch, nsteps, bmode, r, st);
         case R_GENERIC: return warp_rule<R_GENERIC>(V, q, batch, nsteps, bmode, r, st);
         case R_LIN_FAST: return warp_rule<R_LIN_FAST>(V, q, batch, nsteps, bmode, r, st);
         default: return cudaErrorInvalidValue;
@@ -912,6 +926,7 @@ cudaError_t launch_cta_ensemble(int rule, int32_t* q, int64_t n, int64_t batch, 
     switch (rule) {
         case R_LIN_HALF: return cta_rule<R_LIN_HALF>(q, n, batch, nsteps, bmode, r, st);
         case R_EO_FAST: return cta_rule<R_EO_FAST>(q, n, batch, nsteps, bmode, r, st);
+        case R_EO_P1: return cta_rule<R_EO_P1>(q, n, batch, nsteps, bmode, r, st);
         case R_GENERIC: return cta_rule<R_GENERIC>(q, n, batch, nsteps, bmode, r, st);
         case R_LIN_FAST: return cta_rule<R_LIN_FAST>(q, n, batch, nsteps, bmode, r, st);
         default: return cudaErrorInvalidValue;
@@ -928,6 +943,7 @@ cudaError_t launch_transfer(int rule, const int32_t* q, int32_t* pp, int32_t* pm
     switch (rule) {
         case R_LIN_HALF: k_transfer<R_LIN_HALF><<<g, 256, 0, st>>>(q, pp, pm, n, r); break;
         case R_EO_FAST: k_transfer<R_EO_FAST><<<g, 256, 0, st>>>(q, pp, pm, n, r); break;
+        case R_EO_P1: k_transfer<R_EO_P1><<<g, 256, 0, st>>>(q, pp, pm, n, r); break;
         case R_GENERIC: k_transfer<R_GENERIC><<<g, 256, 0, st>>>(q, pp, pm, n, r); break;
         case R_LIN_FAST: k_transfer<R_LIN_FAST><<<g, 256, 0, st>>>(q, pp, pm, n, r); break;
         default: return cudaErrorInvalidValue;

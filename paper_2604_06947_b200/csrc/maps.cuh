@@ -105,6 +105,40 @@ __device__ __forceinline__ void eo_gm(int32_t q, int32_t& g, int32_t& m, const D
 #endif
 }
 
+// EO magnitude for P = 1 (kappa = 1/Q; every EO plan of BJ has P = 1), two
+// instructions shorter than eo_gm:
+// 1. est is estimated as in eo_gm but with the magic 1.5*2^23 + 1, so
+//    bits = 0x4B400000 + 1 + est, est in {g - 1, g} (the tie rule of the FFMA
+//    does not matter: est is floor or ceil of a strict underestimate).
+// 2. est = g - 1 exactly when v = P q^2 - Q est - ceil(Q/2) >= 0 (integers:
+//    2Pq^2 + Q >= 2Q(est + 1)); |v| < 2Q, so v is exact modulo 2^32:
+//    v = q*q + (-Q)*bits + c6,  c6 = Q*(0x4B400000 + 1) - ceil(Q/2).
+// 3. gb = bits + (v >> 31) = 0x4B400000 + g  (LEA.HI.SX32), and since g < 2^22
+//    the bias sits above bit 21: g = gb & 0x3FFFFF, phi-(q) = gb & 0x3FFFFF & (q >> 31)
+//    in one LOP3.  BIASED returns gb itself as g: the step only uses differences of
+//    interface transfers, so a constant bias in g (never in m) cancels.
+// CONV selects the exact int -> float conversion: I2FP (ALU pipe) or IMAD + FADD
+// (FMA pipe), so cells can alternate to balance the two pipes.
+template <int CONV, bool BIASED>
+__device__ __forceinline__ void eo_gm_p1(int32_t q, int32_t& g, int32_t& m, const DevRule& r)
+{
+    float qf;
+    if (CONV == 0) qf = __int2float_rn(q);                               // exact, |q| < 2^24
+    else qf = __int_as_float(imad(q, r.one, 0x4B400000)) - 12582912.0f;   // exact, |q| < 2^22
+    const float s = __fmul_rn(qf, qf);
+    const float t = __fmaf_rn(s, r.eo_cf, 12582913.0f);                 // 0x4B400001 + est
+    const int32_t bits = __float_as_int(t);
+    const int32_t v = imad(q, q, imad(bits, r.eo_nQ, r.eo_c6));
+    const int32_t gb = bits + (v >> 31);                                 // 0x4B400000 + g
+#if FQNM_EO_P1_SIGN
+    const int32_t sg = __mulhi(q, r.one);                                // q >> 31 as IMAD.HI (FMA pipe)
+#else
+    const int32_t sg = q >> 31;
+#endif
+    m = gb & 0x3FFFFF & sg;                                              // [q<0] g
+    g = BIASED ? gb : (gb & 0x3FFFFF);
+}
+
 // LINEAR |kappa| = P/Q <= 1: phi(q) = sign(kappa q) floor((2P|q| + Q)/(2Q)), for
 // |q| < 2^24 and |kappa q| <= 2^20 (planner), with the EO scheme: est = rint(|q_f| cf)
 // (one FFMA, cf <= |kappa|(1 - 2^-21)) is g or g - 1, corrected by the sign of
@@ -124,7 +158,16 @@ __device__ __forceinline__ int32_t lin_phi(int32_t q, const DevRule& r)
 
 // (g, m) with g = phi+(q) + phi-(q) and m = phi-(q); phi+(q) = g - m.
 // The step uses F_{j+1/2} = phi+(q_j) + phi-(q_{j+1}) = g_j - m_j + m_{j+1} (one IADD3).
-template <int RULE>
+#ifndef FQNM_EO_P1_SIGN
+#define FQNM_EO_P1_SIGN 0      // sign mask q >> 31: 0 SHF (ALU pipe), 1 IMAD.HI (FMA pipe)
+#endif
+#ifndef FQNM_EO_P1_CONV
+#define FQNM_EO_P1_CONV 2      // 0: I2FP, 1: IMAD + FADD, 2: alternate by cell parity (fastest, profiles/r01_tune_eo_p1.jsonl)
+#endif
+
+// BIASED: g may carry a constant bias (see eo_gm_p1); only the stepping kernels,
+// which use differences of g, ask for it
+template <int RULE, bool ALT = false, bool BIASED = false>
 __device__ __forceinline__ void phi_gm(int32_t q, int32_t& g, int32_t& m, const DevRule& r)
 {
     if (RULE == R_LIN_HALF) {
@@ -133,6 +176,8 @@ __device__ __forceinline__ void phi_gm(int32_t q, int32_t& g, int32_t& m, const 
         m = 0;
     } else if (RULE == R_EO_FAST) {
         eo_gm(q, g, m, r);               // phi-(q) = g for q < 0, phi+(q) = g for q > 0, g(0) = 0
+    } else if (RULE == R_EO_P1) {
+        eo_gm_p1<(FQNM_EO_P1_CONV == 1 || (FQNM_EO_P1_CONV == 2 && ALT)) ? 1 : 0, BIASED>(q, g, m, r);
     } else if (RULE == R_LIN_FAST) {
         // a > 0: phi+ = RHA(kappa q) = v, phi- = 0;  a < 0: phi+ = 0, phi- = RHA(kappa q) = -v
         const int32_t v = lin_phi(q, r);

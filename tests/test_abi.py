@@ -67,8 +67,10 @@ def test_kappa_rationalised_from_doubles(F, name, qmax, expect):
 def test_rule_and_kernel_selection(F):
     w4 = W.cfg("cfg4")
     info = F.fqnm_plan_validate(w4.n, 1e-6, W.dt_dx_double(w4, 1_200_000), F.BURGERS_EO)
-    assert info["rule"] == 2 and info["kernel"] == 2           # EO fast path, blocked kernel
+    assert info["rule"] == 5 and info["kernel"] == 2           # EO fast path (P = 1), blocked kernel
     assert info["q_hi"] >= 2_400_000 and info["q_lo"] == -info["q_hi"]
+    info = F.fqnm_plan_validate(1 << 24, 1e-5, 0.3, F.BURGERS_EO)   # kappa = 3/2e6, P = 3
+    assert info["rule"] == 2 and info["kappa_num"] == 3
     info = F.fqnm_plan_validate(1 << 24, 1e-6, 0.5, F.LINEAR)
     assert info["rule"] == 1 and info["kernel"] == 2
     info = F.fqnm_plan_validate(1024, 1e-4, 0.5, F.LINEAR, batch=1 << 16)

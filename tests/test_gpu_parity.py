@@ -50,6 +50,8 @@ def tv_periodic(t):
     (W.BURGERS_EO, "1e-5", Fraction(4, 15), 1),                  # cfg2
     (W.BURGERS_EO, "1e-6", Fraction(2, 5) / Fraction("1e-6") / 345000, 1),   # cfg4-like
     (W.BURGERS_EO, "1e-6", Fraction(2, 5) / Fraction("1e-6") / 1_200_000, 1),
+    (W.BURGERS_EO, "1e-5", Fraction(3, 10), 1),                 # P = 3: R_EO_FAST, not R_EO_P1
+    (W.BURGERS_EO, "1e-7", Fraction(7, 3), 1),                  # P = 7
     (W.LINEAR, "1e-3", Fraction(7, 9), 1),
     (W.LINEAR, "1e-3", Fraction(1, 3), -1),
     (W.BURGERS_LF, "1e-3", Fraction(1, 2), 1),
@@ -223,6 +225,7 @@ CASES = [  # (kind, delta, lam, param, data amplitude, offset)
     (W.BURGERS_EO, "1e-5", Fraction(4, 15), 1, 100000, 20000),
     (W.BURGERS_LF, "1e-3", Fraction(1, 2), 1, 900, 0),
     (W.LINEAR, "1e-3", Fraction(1, 3), -1, 3000, 100),
+    (W.BURGERS_EO, "1e-5", Fraction(3, 10), 1, 100000, 20000),     # kappa = 3/2e6: P = 3 (R_EO_FAST)
 ]
 
 
@@ -256,7 +259,7 @@ def test_all_families_match_oracle(F, case, boundary, n):
 
 @pytest.mark.parametrize("V,k", [(8, 1), (8, 3), (8, 8), (16, 4), (16, 13), (16, 32), (32, 7),
                                  (32, 64), (16, 64)])
-@pytest.mark.parametrize("case", [0, 1])
+@pytest.mark.parametrize("case", [0, 1, 4])
 def test_blocked_k_and_v(F, V, k, case):
     kind, delta, lam, param, amp, off = CASES[case]
     n = 50000 + 3

@@ -1,5 +1,6 @@
 """Sweep (V, k) of the temporally blocked kernel on the bench workloads (GPU).
 Prints one JSON line per setting: GCUPS and kernel ms."""
+import hashlib
 import json
 import os
 import sys
@@ -60,9 +61,10 @@ def main():
                 continue
             q = q0.clone()
             ms = run(plan, q, steps)
+            digest = hashlib.sha256(q.cpu().numpy().tobytes()).hexdigest()[:16]
             print(json.dumps({"which": which, "lib": os.environ.get("FQNM_LIBPATH", "default"),
                               "fam": fam, "n": n, "steps": steps, "V": V, "k": k, "ms": ms,
-                              "GCUPS": n * steps / ms / 1e6}), flush=True)
+                              "GCUPS": n * steps / ms / 1e6, "sha": digest}), flush=True)
             del q, plan
             torch.cuda.empty_cache()
 

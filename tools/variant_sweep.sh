@@ -1,0 +1,7 @@
+#!/bin/bash
+# EO kernel variant sweep: libs built by _build.build(defines=[...], lib=build/libfqnm_<tag>.so)
+# usage: bash tools/variant_sweep.sh tag1 tag2 ...   (prints GCUPS + sha of the final state)
+B=paper_2604_06947_b200/build
+for rep in 1 2; do for v in "$@"; do
+  FQNM_LIBPATH=$PWD/$B/libfqnm_$v.so TUNE_N=268435456 TUNE_V=32 TUNE_K=24 TUNE_FAM=202 timeout 120 python tools/tune.py eo | sed "s/^/$v /"
+done; done
