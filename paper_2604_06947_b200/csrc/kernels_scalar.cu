@@ -224,6 +224,17 @@ __device__ __noinline__ void slow_window(const BlockedArgs& a, const DevRule& r,
     }
 }
 
+#ifndef FQNM_PREFETCH
+#define FQNM_PREFETCH 0        // K2: stage the next window in shared memory (cp.async) while stepping
+                               // (measured 2.3% slower at V = 32: the staging registers spill)
+#endif
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa), "l"(gmem) : "memory");
+}
+
 template <int RULE, int V, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_blocked(BlockedArgs a, DevRule r)
 {
@@ -237,16 +248,27 @@ __global__ void __launch_bounds__(256, MINB) k_blocked(BlockedArgs a, DevRule r)
     const bool halo = a.bmode == BM_HALO;
     const int64_t pstride = halo ? n + 2 * a.halo : n;
     const int64_t lowest = halo ? -a.halo : 0;
+#if FQNM_PREFETCH
+    // per warp: the next window's 32*V cells as [V/4][32 lanes] int4 (conflict-free LDS.128)
+    __shared__ int4 stage[256 / 32][V / 4][32];
+    int4 (&my)[V / 4][32] = stage[threadIdx.x >> 5];
+    bool staged = false;
+#endif
+    // window geometry of (b, w): first cell ws, problem offset boff, fast = int4 path
+    auto geom = [&](int64_t bb, int64_t ww, int64_t& ws, int64_t& boff, int64_t& owned0) {
+        owned0 = ww * S;
+        if (a.p2p && owned0 + S > n && n >= S) owned0 = n - S;  // last window ends at n
+        ws = owned0 - a.KL;                                     // first cell of the window
+        boff = bb * pstride + (halo ? a.halo : 0);
+        return ((boff & 3) == 0) && ws >= lowest && ws + W <= n;
+    };
     // window iteration without 64-bit division: (b, w) advanced by nwarps
     int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int64_t b = 0;
     while (w >= a.nwin && b < a.batch) { w -= a.nwin; ++b; }
     while (b < a.batch) {
-        int64_t owned0 = w * S;
-        if (a.p2p && owned0 + S > n && n >= S) owned0 = n - S;  // last window ends at n
-        const int64_t ws = owned0 - a.KL;                       // first cell of the window
-        const int64_t boff = b * pstride + (halo ? a.halo : 0);
-        const bool fast = ((boff & 3) == 0) && ws >= lowest && ws + W <= n;
+        int64_t ws, boff, owned0;
+        const bool fast = geom(b, w, ws, boff, owned0);
         if (a.p2p && (ws < 0 || ws + W > n)) {                  // reads halos: wait for them
             if (lane == 0) {
                 if (ws < 0) p2p_wait(a.self_flags + 0, a.tag);
@@ -254,15 +276,44 @@ __global__ void __launch_bounds__(256, MINB) k_blocked(BlockedArgs a, DevRule r)
             }
             __syncwarp();
         }
+        int64_t w2 = w + nwarps, b2 = b;
+        while (w2 >= a.nwin && b2 < a.batch) { w2 -= a.nwin; ++b2; }
         if (fast) {
-            const int4* s4 = reinterpret_cast<const int4*>(a.src + boff + ws) + lane * (V / 4);
             int4* d4 = reinterpret_cast<int4*>(a.dst + boff + ws) + lane * (V / 4);
             int32_t q[V];
+#if FQNM_PREFETCH
+            if (staged) {
+                asm volatile("cp.async.wait_all;" ::: "memory");
 #pragma unroll
-            for (int j = 0; j < V / 4; ++j) {
-                int4 v = __ldg(s4 + j);
-                q[4 * j] = v.x; q[4 * j + 1] = v.y; q[4 * j + 2] = v.z; q[4 * j + 3] = v.w;
+                for (int j = 0; j < V / 4; ++j) {
+                    const int4 v = my[j][lane];
+                    q[4 * j] = v.x; q[4 * j + 1] = v.y; q[4 * j + 2] = v.z; q[4 * j + 3] = v.w;
+                }
+            } else
+#endif
+            {
+                const int4* s4 = reinterpret_cast<const int4*>(a.src + boff + ws) + lane * (V / 4);
+#pragma unroll
+                for (int j = 0; j < V / 4; ++j) {
+                    int4 v = __ldg(s4 + j);
+                    q[4 * j] = v.x; q[4 * j + 1] = v.y; q[4 * j + 2] = v.z; q[4 * j + 3] = v.w;
+                }
             }
+#if FQNM_PREFETCH
+            // stage the next window (fast, and not a halo window of a p2p run, whose
+            // halos may not have arrived yet) while this one steps
+            staged = false;
+            if (b2 < a.batch) {
+                int64_t ws2, boff2, o2;
+                if (geom(b2, w2, ws2, boff2, o2) && !(a.p2p && (ws2 < 0 || ws2 + W > n))) {
+                    const int4* s4n = reinterpret_cast<const int4*>(a.src + boff2 + ws2) + lane * (V / 4);
+#pragma unroll
+                    for (int j = 0; j < V / 4; ++j) cp_async16(&my[j][lane], s4n + j);
+                    asm volatile("cp.async.commit_group;" ::: "memory");
+                    staged = true;
+                }
+            }
+#endif
             run_window_steps<RULE, V, false>(q, a.ksteps, r, 0, 0);
             // store the cells whose dependence cone stayed inside the window
 #pragma unroll
@@ -273,15 +324,21 @@ __global__ void __launch_bounds__(256, MINB) k_blocked(BlockedArgs a, DevRule r)
             }
         } else {
             slow_window<RULE, V>(a, r, b, ws, lane);
+#if FQNM_PREFETCH
+            staged = false;
+#endif
         }
         if (a.p2p && (owned0 == 0 || owned0 + S >= n)) {
             __syncwarp();
             p2p_push(a, a.dst, owned0 == 0, owned0 + S >= n, a.tag + 1, a.peer_left_dst,
                      a.peer_right_dst, lane);
         }
-        w += nwarps;
-        while (w >= a.nwin && b < a.batch) { w -= a.nwin; ++b; }
+        w = w2;
+        b = b2;
     }
+#if FQNM_PREFETCH
+    asm volatile("cp.async.wait_all;" ::: "memory");
+#endif
 }
 
 // ---------------------------------------------------------------------------
