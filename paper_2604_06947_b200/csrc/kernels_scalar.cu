@@ -111,12 +111,89 @@ __device__ __forceinline__ void one_step(int32_t (&q)[V], const DevRule& r, int 
     }
 }
 
+#ifndef FQNM_FUSED_STEPS
+X
+#endif
+
+// One fused step (no walls, neighbours by shfl): update the lane's cells with the
+// current maps (g, m) and, cell by cell, evaluate the maps of the new value for the
+// next step (NEXT).  Interleaving the ALU-heavy update with the FMA-heavy map
+// evaluation keeps both pipes busy instead of running the step in pipe phases.
+template <int RULE, int V, bool NEXT>
+__device__ __forceinline__ void fused_step(int32_t (&q)[V], int32_t (&g)[V], int32_t (&m)[V],
+                                           const DevRule& r)
+{
+    const int32_t pl = __shfl_up_sync(FULL, g[V - 1] - m[V - 1], 1);
+    const int32_t mr = __shfl_down_sync(FULL, m[0], 1);
+    int32_t Tl = pl + m[0];                                         // F_{-1/2} of the lane
+#pragma unroll
+    for (int j = 0; j < V; j += 2) {          // odd cells may take the other pipe mix
+        int32_t Tr = g[j] - m[j] + ((j + 1 < V) ? m[j + 1] : mr);         // F_{j+1/2}
+        q[j] = q[j] + Tl - Tr;
+        Tl = Tr;
+        if (NEXT) phi_gm<RULE, false, true>(q[j], g[j], m[j], r);
+        if (j + 1 < V) {
+            Tr = g[j + 1] - m[j + 1] + ((j + 2 < V) ? m[j + 2] : mr);
+            q[j + 1] = q[j + 1] + Tl - Tr;
+            Tl = Tr;
+            if (NEXT) phi_gm<RULE, true, true>(q[j + 1], g[j + 1], m[j + 1], r);
+        }
+    }
+}
+
+template <int V, bool NEXT>
+__device__ __forceinline__ void fused_step_lin_half(int32_t (&q)[V], int32_t (&h)[V],
+                                                    int32_t (&p)[V], const DevRule& r)
+{
+    // kappa = 1/2: q'_j = trunc(q_j/2) + phi+(q_{j-1}) with h = trunc(q/2), p = q - h
+    int32_t pprev = __shfl_up_sync(FULL, p[V - 1], 1);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        const int32_t pj = p[j];
+        q[j] = pprev * r.one + h[j];
+        pprev = pj;
+        if (NEXT) {
+            h[j] = q[j] / 2;
+            p[j] = h[j] * r.mone + q[j];
+        }
+    }
+}
+
 // K2: temporally blocked stencil
 template <int RULE, int V, bool WALL>
 __device__ __forceinline__ void run_window_steps(int32_t (&q)[V], int ksteps, const DevRule& r,
                                                  int64_t g0, int64_t n)
 {
     const int lane = threadIdx.x & 31;
+    if (FQNM_FUSED_STEPS && !WALL && ksteps > 0) {
+        int32_t g[V], m[V];
+        if (RULE == R_LIN_HALF) {
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                g[j] = q[j] / 2;
+                m[j] = g[j] * r.mone + q[j];
+            }
+        } else {
+            eval_maps<RULE, V>(q, g, m, r);
+        }
+        int s = 1;
+        for (; s + 2 <= ksteps; s += 2) {
+            if (RULE == R_LIN_HALF) {
+                fused_step_lin_half<V, true>(q, g, m, r);
+                fused_step_lin_half<V, true>(q, g, m, r);
+            } else {
+                fused_step<RULE, V, true>(q, g, m, r);
+                fused_step<RULE, V, true>(q, g, m, r);
+            }
+        }
+        if (s < ksteps) {
+            if (RULE == R_LIN_HALF) fused_step_lin_half<V, true>(q, g, m, r);
+            else fused_step<RULE, V, true>(q, g, m, r);
+        }
+        if (RULE == R_LIN_HALF) fused_step_lin_half<V, false>(q, g, m, r);
+        else fused_step<RULE, V, false>(q, g, m, r);
+        return;
+    }
     int s = 0;
     // unrolled by two: no register renaming moves between steps
     for (; s + 2 <= ksteps; s += 2) {
