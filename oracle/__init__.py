@@ -33,8 +33,8 @@ from typing import Optional
 import numpy as np
 
 from . import rules
-from .rules import (BURGERS_EO, BURGERS_LF, FLOOR, HALF_EVEN, LINEAR, RHA,
-                    map_coefficients)
+from .rules import (BURGERS_EO, BURGERS_EO2, BURGERS_GODUNOV, BURGERS_LF, BURGERS_LF2,
+                    FLOOR, HALF_EVEN, LINEAR, RHA, map_coefficients)
 
 PERIODIC, TRANSMISSIVE = 0, 1
 
@@ -58,6 +58,12 @@ def build(force: bool = False) -> str:
 class _Map(ctypes.Structure):
     _fields_ = [("c2", ctypes.c_int64), ("c1", ctypes.c_int64), ("den", ctypes.c_int64),
                 ("support", ctypes.c_int32), ("rounding", ctypes.c_int32)]
+
+
+class _Transfer(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("rounding", ctypes.c_int32),
+                ("c2", ctypes.c_int64), ("c1", ctypes.c_int64), ("den", ctypes.c_int64),
+                ("pp", _Map), ("pm", _Map)]
 
 
 _lib = None
@@ -95,6 +101,13 @@ def lib():
                                         ctypes.c_int64, P64, P64]
         L.or_run_scalar_2d.argtypes = [PM, PM, PM, PM, ctypes.c_int, ctypes.c_int64,
                                        ctypes.c_int64, P64, ctypes.c_int64, ctypes.c_int]
+        PT = ctypes.POINTER(_Transfer)
+        L.or_transfer_eval.restype = ctypes.c_int64
+        L.or_transfer_eval.argtypes = [PT, ctypes.c_int64, ctypes.c_int64]
+        L.or_transfer_array.argtypes = [PT, P64, P64, P64, ctypes.c_int64]
+        L.or_step_transfer.argtypes = [PT, ctypes.c_int, ctypes.c_int64, P64, P64]
+        L.or_run_transfer.argtypes = [PT, ctypes.c_int, ctypes.c_int64, P64, ctypes.c_int64,
+                                      ctypes.c_int]
         L.or_round_rational.restype = ctypes.c_int64
         L.or_round_rational.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64,
                                         ctypes.c_int]
@@ -167,6 +180,82 @@ class Rule:
             lib().or_run_scalar_batch(ctypes.byref(self._mp), ctypes.byref(self._mm), boundary,
                                       B, N, _p64(q), nsteps, nthreads)
         return q
+
+
+class TransferRule:
+    """An interface transfer rule Phi(qL, qR) (Thm transfer-operator equivalence,
+    P:262-280): either the paper's split rule phi+(qL) + phi-(qR) (kinds 0-2) or a
+    quantised two-point rule round(F(delta qL, delta qR) dt/dx / delta) rounded once
+    (kinds BURGERS_GODUNOV, BURGERS_EO2, BURGERS_LF2)."""
+
+    def __init__(self, kind: int, delta, dt_dx, param=Fraction(1), rounding: int = RHA):
+        self.kind = kind
+        self.delta, self.dt_dx, self.param = Fraction(delta), Fraction(dt_dx), Fraction(param)
+        self.rounding = rounding
+        t = _Transfer()
+        t.rounding = rounding
+        if kind in rules.TWO_POINT_KINDS:
+            t.kind = kind
+            t.c2, t.c1, t.den = rules.two_point_coefficients(kind, delta, dt_dx, param)
+        else:
+            r = Rule(kind, delta, dt_dx, param, rounding)
+            t.kind = 0
+            t.pp, t.pm = r._mp, r._mm
+        self._t = t
+
+    def phi(self, qL, qR) -> np.ndarray:
+        a = np.ascontiguousarray(np.atleast_1d(qL), dtype=np.int64)
+        b = np.ascontiguousarray(np.broadcast_to(np.atleast_1d(qR), a.shape), dtype=np.int64)
+        out = np.empty_like(a)
+        lib().or_transfer_array(ctypes.byref(self._t), _p64(a), _p64(b), _p64(out), a.size)
+        return out
+
+    def _interfaces(self, q, boundary):
+        """(qL, qR) of the interfaces i+1/2, i = -1 .. N-1 (N+1 values; periodic: the
+        first equals the last)."""
+        if boundary == PERIODIC:
+            qL = np.concatenate([q[-1:], q])
+            qR = np.concatenate([q[:1], q[1:], q[:1]])
+        else:
+            qL = np.concatenate([q[:1], q])
+            qR = np.concatenate([q, q[-1:]])
+        return qL, qR
+
+    def step(self, q, boundary: int = PERIODIC) -> np.ndarray:
+        q = np.ascontiguousarray(q, dtype=np.int64)
+        out = np.empty_like(q)
+        lib().or_step_transfer(ctypes.byref(self._t), boundary, q.size, _p64(q), _p64(out))
+        return out
+
+    def run(self, q, nsteps: int, boundary: int = PERIODIC, nthreads: int = 0) -> np.ndarray:
+        q = np.array(q, dtype=np.int64, copy=True, order="C")
+        lib().or_run_transfer(ctypes.byref(self._t), boundary, q.size, _p64(q), nsteps, nthreads)
+        return q
+
+    def equivalence(self, other: "TransferRule", q, nsteps: int, boundary: int = PERIODIC):
+        """Steps q with THIS rule and evaluates `other` on every visited interface
+        state (qL, qR) (the hypothesis of Thm P:274-280).  Returns (q_final, stats)
+        with stats = interface_evals, mismatches, first_mismatch_step, visited_pairs,
+        mismatched_pairs (distinct (qL, qR))."""
+        q = np.array(q, dtype=np.int64, copy=True)
+        evals = mism = 0
+        first = -1
+        visited, bad = set(), set()
+        for s in range(nsteps):
+            qL, qR = self._interfaces(q, boundary)
+            if boundary == PERIODIC:            # N distinct interfaces
+                qL, qR = qL[1:], qR[1:]
+            Ta, Tb = self.phi(qL, qR), other.phi(qL, qR)
+            evals += qL.size
+            neq = Ta != Tb
+            if neq.any() and first < 0:
+                first = s
+            mism += int(neq.sum())
+            visited.update(zip(qL.tolist(), qR.tolist()))
+            bad.update(zip(qL[neq].tolist(), qR[neq].tolist()))
+            q = self.step(q, boundary)
+        return q, {"interface_evals": evals, "mismatches": mism, "first_mismatch_step": first,
+                   "visited_pairs": len(visited), "mismatched_pairs": len(bad)}
 
 
 class Rule2D:

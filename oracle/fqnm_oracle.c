@@ -191,6 +191,93 @@ void or_run_scalar_batch(const or_map* pp, const or_map* pm, int boundary, int64
         run_one(pp, pm, boundary, N, q + b * N, nsteps);
 }
 
+/* ---- 3a. quantised two-point transfer rules ------------------------------- */
+/* Thm transfer-operator equivalence: Phi(qL, qR) =
+ * round(F(delta qL, delta qR) dt/dx / delta) for a classical two-point flux F,
+ * rounded once (Eq. transfer_operator_equivalence_definition).
+ * Kinds (include/fqnm.h codes): 5 Godunov, 6 EO rounded once, 7 LF rounded once,
+ * with integer coefficients from oracle/rules.py (two_point_coefficients):
+ *   Godunov: c2 max(max(qL,0)^2, min(qR,0)^2) / den
+ *   EO2:     c2 (max(qL,0)^2 + min(qR,0)^2) / den
+ *   LF2:     (c2 (qL^2 + qR^2) + c1 (qL - qR)) / den
+ * A split rule (kind 0) is the paper's F = phi+(qL) + phi-(qR). */
+typedef struct {
+    int32_t kind;          /* 0 split, 5/6/7 two-point */
+    int32_t rounding;
+    int64_t c2, c1, den;   /* two-point coefficients */
+    or_map pp, pm;         /* split maps */
+} or_transfer;
+
+static int64_t or_round_i128(i128 num, i128 d, int rounding)
+{
+    if (rounding == OR_FLOOR) return (int64_t)floor_div(num, d);
+    i128 a = num < 0 ? -num : num;
+    if (rounding == OR_RHA) {
+        i128 r = (2 * a + d) / (2 * d);
+        return (int64_t)(num < 0 ? -r : r);
+    }
+    i128 fl = a / d, rem = a - fl * d, r;
+    if (2 * rem > d) r = fl + 1;
+    else if (2 * rem < d) r = fl;
+    else r = (fl % 2 == 0) ? fl : fl + 1;
+    return (int64_t)(num < 0 ? -r : r);
+}
+
+int64_t or_transfer_eval(const or_transfer* t, int64_t qL, int64_t qR)
+{
+    if (t->kind == 0) return or_phi(&t->pp, qL) + or_phi(&t->pm, qR);
+    i128 L = qL, R = qR, num;
+    i128 a = L > 0 ? L : 0, b = R < 0 ? R : 0;
+    if (t->kind == 5) num = (i128)t->c2 * (a * a > b * b ? a * a : b * b);
+    else if (t->kind == 6) num = (i128)t->c2 * (a * a + b * b);
+    else num = (i128)t->c2 * (L * L + R * R) + (i128)t->c1 * (L - R);
+    return or_round_i128(num, t->den, t->rounding);
+}
+
+void or_transfer_array(const or_transfer* t, const int64_t* qL, const int64_t* qR, int64_t* out,
+                       int64_t n)
+{
+    for (int64_t i = 0; i < n; ++i) out[i] = or_transfer_eval(t, qL[i], qR[i]);
+}
+
+/* interface transfer T_{i+1/2} = Phi(q_i, q_{i+1}), i = -1 .. N-1, ghosts as flux_at */
+static int64_t transfer_at(const or_transfer* t, int boundary, int64_t N, const int64_t* q,
+                           int64_t i)
+{
+    int64_t iL = i, iR = i + 1;
+    if (boundary == OR_PERIODIC) {
+        if (iL < 0) iL += N;
+        if (iR >= N) iR -= N;
+    } else {
+        if (iL < 0) iL = 0;
+        if (iR >= N) iR = N - 1;
+    }
+    return or_transfer_eval(t, q[iL], q[iR]);
+}
+
+/* q^{n+1}_i = q^n_i - (T_{i+1/2} - T_{i-1/2})  (P:86-89 with F replaced by Phi) */
+void or_step_transfer(const or_transfer* t, int boundary, int64_t N, const int64_t* q,
+                      int64_t* out)
+{
+    #pragma omp parallel for schedule(static) if (N >= 32768)
+    for (int64_t i = 0; i < N; ++i)
+        out[i] = q[i] - (transfer_at(t, boundary, N, q, i) - transfer_at(t, boundary, N, q, i - 1));
+}
+
+void or_run_transfer(const or_transfer* t, int boundary, int64_t N, int64_t* q, int64_t nsteps,
+                     int nthreads)
+{
+    set_threads(nthreads);
+    int64_t* a = q;
+    int64_t* b = (int64_t*)malloc(sizeof(int64_t) * (size_t)N);
+    for (int64_t s = 0; s < nsteps; ++s) {
+        or_step_transfer(t, boundary, N, a, b);
+        int64_t* x = a; a = b; b = x;
+    }
+    if (a != q) { memcpy(q, a, sizeof(int64_t) * (size_t)N); b = a; }
+    free(b);
+}
+
 /* ---- 3b. Cartesian extension by directional composition ------------------ */
 /* Thm formal Cartesian dimensional extension, d = 2, unsplit:
  *   q'_{i,j} = q_{i,j} - (F^x_{i+1/2,j} - F^x_{i-1/2,j}) - (F^y_{i,j+1/2} - F^y_{i,j-1/2}),

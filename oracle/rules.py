@@ -14,6 +14,16 @@ are available for the brute-force studies), and the flux splittings
     LINEAR      f(u) = a u,   upwind split f+ = max(a,0) u, f- = min(a,0) u
     BURGERS_EO  f(u) = u^2/2, f+ = max(u,0)^2/2, f- = min(u,0)^2/2          (BJ.cfg2/cfg4, A4)
     BURGERS_LF  f+- = (u^2/2 +- alpha u)/2                                 ("Lax-Friedrichs")
+
+and, for Thm transfer-operator equivalence, the quantised two-point
+transfer rules  Phi(qL, qR) = round( F(delta qL, delta qR) (dt/dx) delta^{-1} )
+(Eq. transfer_operator_equivalence_definition) of three classical
+Burgers fluxes, each rounded ONCE:
+
+    GODUNOV  F = f(u*(0; uL, uR)), u* the exact Riemann solution at x/t = 0
+    EO2      F = f+(uL) + f-(uR) with the Engquist-Osher split  (rounded once,
+             unlike the split rule's round(f+) + round(f-))
+    LF2      F = (f(uL) + f(uR))/2 - alpha (uR - uL)/2
 """
 from __future__ import annotations
 
@@ -22,6 +32,9 @@ from math import gcd
 from typing import Callable, Tuple
 
 LINEAR, BURGERS_EO, BURGERS_LF = 0, 1, 2
+# two-point kinds (same codes as include/fqnm.h)
+BURGERS_GODUNOV, BURGERS_EO2, BURGERS_LF2 = 5, 6, 7
+TWO_POINT_KINDS = (BURGERS_GODUNOV, BURGERS_EO2, BURGERS_LF2)
 RHA, FLOOR, HALF_EVEN = 0, 1, 2
 SUPP_ALL, SUPP_POS, SUPP_NEG = 0, 1, 2
 
@@ -109,3 +122,75 @@ def kappa(kind: int, delta, dt_dx, param=Fraction(1)) -> Fraction:
     if kind == BURGERS_EO:
         return delta * dt_dx / 2
     raise ValueError("kappa is defined for LINEAR and BURGERS_EO only")
+
+
+# ---------------------------------------------------------------------------
+# Quantised two-point transfer rules (Thm transfer-operator equivalence)
+
+def burgers_f(u: Fraction) -> Fraction:
+    return u * u / 2
+
+
+def burgers_riemann_at_zero(uL: Fraction, uR: Fraction) -> Fraction:
+    """u*(x/t = 0) of the exact entropy solution of the Burgers Riemann problem
+    (textbook: a shock of speed (uL + uR)/2 if uL > uR, else a rarefaction fan
+    u = x/t between uL and uR)."""
+    if uL > uR:                       # shock
+        s = (uL + uR) / 2
+        return uL if s > 0 else (uR if s < 0 else uL)   # s = 0: f(uL) = f(uR), either
+    if uL >= 0:                       # rarefaction moving right
+        return uL
+    if uR <= 0:                       # rarefaction moving left
+        return uR
+    return Fraction(0)                # transonic rarefaction: the sonic point
+
+
+def two_point_flux(kind: int, uL: Fraction, uR: Fraction, param=Fraction(1)) -> Fraction:
+    """The classical numerical flux F(uL, uR) of a two-point kind."""
+    uL, uR = Fraction(uL), Fraction(uR)
+    if kind == BURGERS_GODUNOV:
+        return burgers_f(burgers_riemann_at_zero(uL, uR))
+    if kind == BURGERS_EO2:
+        zero = Fraction(0)
+        return max(uL, zero) ** 2 / 2 + min(uR, zero) ** 2 / 2
+    if kind == BURGERS_LF2:
+        return (burgers_f(uL) + burgers_f(uR)) / 2 - Fraction(param) * (uR - uL) / 2
+    raise ValueError(f"not a two-point kind: {kind}")
+
+
+def two_point_phi(kind: int, delta, dt_dx, qL: int, qR: int, param=Fraction(1),
+                  rounding: int = RHA) -> int:
+    """Phi(qL, qR) = round(F(delta qL, delta qR) (dt/dx) / delta)."""
+    delta, dt_dx = Fraction(delta), Fraction(dt_dx)
+    return round_rational(two_point_flux(kind, delta * qL, delta * qR, param) * dt_dx / delta,
+                          rounding)
+
+
+def two_point_coefficients(kind: int, delta, dt_dx, param=Fraction(1)):
+    """Integer coefficients (c2, c1, den) of the C oracle's evaluation:
+    GODUNOV: Phi = round(c2 max(max(qL,0)^2, min(qR,0)^2) / den)
+    EO2:     Phi = round(c2 (max(qL,0)^2 + min(qR,0)^2) / den)
+    LF2:     Phi = round((c2 (qL^2 + qR^2) + c1 (qL - qR)) / den)
+    derived from F(delta qL, delta qR) dt/dx / delta by exact interpolation and
+    checked against the literal definition at sample points."""
+    delta, dt_dx = Fraction(delta), Fraction(dt_dx)
+    g = lambda a, b: two_point_flux(kind, delta * a, delta * b, param) * dt_dx / delta
+    if kind in (BURGERS_GODUNOV, BURGERS_EO2):
+        c2f, c1f = g(1, 0), Fraction(0)                     # = kappa = delta dt/dx / 2
+    elif kind == BURGERS_LF2:
+        # g(a, 0) = c2 a^2 + c1 a
+        c2f = (g(2, 0) - 2 * g(1, 0)) / 2
+        c1f = g(1, 0) - c2f
+    else:
+        raise ValueError(kind)
+    den = c2f.denominator * c1f.denominator // gcd(c2f.denominator, c1f.denominator)
+    c2, c1 = int(c2f * den), int(c1f * den)
+    for a, b in ((3, -2), (-5, 4), (7, 7), (-3, -9), (0, 6), (6, 0), (2, -2)):
+        if kind == BURGERS_GODUNOV:
+            num = c2 * max(max(a, 0) ** 2, min(b, 0) ** 2)
+        elif kind == BURGERS_EO2:
+            num = c2 * (max(a, 0) ** 2 + min(b, 0) ** 2)
+        else:
+            num = c2 * (a * a + b * b) + c1 * (a - b)
+        assert Fraction(num, den) == g(a, b), (kind, a, b)
+    return c2, c1, den
