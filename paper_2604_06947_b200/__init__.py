@@ -23,12 +23,15 @@ __all__ = [
     "fqnm_roe_transfer_device", "fqnm_debug_override", "fqnm_launch_count", "fqnm_destroy",
     "fqnm_plan_validate", "fqnm_profile_enable", "fqnm_profile_read", "fqnm_halo_buffers",
     "fqnm_halo_connect", "fqnm_halo_owned", "fqnm_step_group", "fqnm_ipc_export",
-    "fqnm_ipc_open", "fqnm_ipc_close", "owned_tensor", "fqnm_plan_2d",
+    "fqnm_ipc_open", "fqnm_ipc_close", "owned_tensor", "fqnm_plan_2d", "fqnm_transfer2",
+    "fqnm_transfer2_device", "fqnm_equivalence",
     "LINEAR", "BURGERS_EO", "BURGERS_LF", "EULER_ROE", "EULER_ROE_DENSITY", "PERIODIC", "TRANSMISSIVE", "HALO",
+    "BURGERS_GODUNOV", "BURGERS_EO2", "BURGERS_LF2",
     "I32", "I64", "ROUND_HALF_AWAY", "ROUND_FLOOR", "ROUND_HALF_EVEN", "lib_path",
 ]
 
 LINEAR, BURGERS_EO, BURGERS_LF, EULER_ROE, EULER_ROE_DENSITY = 0, 1, 2, 3, 4
+BURGERS_GODUNOV, BURGERS_EO2, BURGERS_LF2 = 5, 6, 7      # two-point rules (Thm P:262-280)
 PERIODIC, TRANSMISSIVE, HALO = 0, 1, 2
 I32, I64 = 0, 1
 ROUND_HALF_AWAY, ROUND_FLOOR, ROUND_HALF_EVEN = 0, 1, 2
@@ -95,6 +98,15 @@ class TransitionStats(ctypes.Structure):
         return d
 
 
+class EquivalenceStats(ctypes.Structure):
+    _fields_ = [("interface_evals", ctypes.c_int64), ("mismatches", ctypes.c_int64),
+                ("first_mismatch_step", ctypes.c_int64), ("visited_pairs", ctypes.c_int64),
+                ("mismatched_pairs", ctypes.c_int64), ("overflow", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
 _lib = None
 
 
@@ -125,6 +137,9 @@ def _load():
     L.fqnm_transfer.argtypes = [vp, i64, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.fqnm_transfer_device.argtypes = [vp, vp, vp, vp, i64]
     L.fqnm_roe_transfer_device.argtypes = [vp, vp, vp, vp, i64]
+    L.fqnm_transfer2.argtypes = [vp, i64, i64, ctypes.POINTER(i64)]
+    L.fqnm_transfer2_device.argtypes = [vp, vp, vp, vp, i64]
+    L.fqnm_equivalence.argtypes = [vp, vp, vp, i64, i64, ctypes.POINTER(EquivalenceStats)]
     L.fqnm_debug_override.argtypes = [vp, i32, i32, i32]
     L.fqnm_plan_validate.argtypes = [ctypes.POINTER(PlanDesc), ctypes.POINTER(PlanInfo)]
     L.fqnm_profile_enable.argtypes = [vp, ctypes.c_int]
@@ -438,6 +453,41 @@ def fqnm_transfer_device(plan: Plan, q):
     _check(L.fqnm_set_stream(plan.handle, _stream_ptr(q)))
     _check(L.fqnm_transfer_device(plan.handle, qp, _dev_ptr(p), _dev_ptr(m), q.numel()))
     return p, m
+
+
+def fqnm_transfer2(plan: Plan, qL: int, qR: int) -> int:
+    """Host evaluation of the interface transfer Phi(qL, qR) of a scalar plan."""
+    t = ctypes.c_int64()
+    _check(_load().fqnm_transfer2(plan.handle, int(qL), int(qR), ctypes.byref(t)))
+    return t.value
+
+
+def fqnm_transfer2_device(plan: Plan, qL, qR):
+    """The kernels' interface-transfer code on int32 device tensors qL, qR."""
+    import torch
+    T = torch.empty_like(qL)
+    L = _load()
+    a = _dev_ptr(qL, torch.int32, "qL")
+    b = _dev_ptr(qR, torch.int32, "qR")
+    if qR.numel() != qL.numel():
+        raise ValueError("qL and qR must have the same size")
+    _check(L.fqnm_set_stream(plan.handle, _stream_ptr(qL)))
+    _check(L.fqnm_transfer2_device(plan.handle, a, b, _dev_ptr(T), qL.numel()))
+    return T
+
+
+def fqnm_equivalence(plan_a: Plan, plan_b: Plan, q, nsteps: int, pair_capacity: int = 0) -> dict:
+    """Thm transfer-operator equivalence check: advance q (int32 device tensor, in
+    place) by nsteps of plan_a's rule, evaluating plan_b's transfer on every visited
+    interface state.  Synchronous; returns the statistics as a dict."""
+    import torch
+    L = _load()
+    qp = _dev_ptr(q, torch.int32, "q")
+    st = EquivalenceStats()
+    _check(L.fqnm_set_stream(plan_a.handle, _stream_ptr(q)))
+    _check(L.fqnm_equivalence(plan_a.handle, plan_b.handle, qp, int(nsteps), int(pair_capacity),
+                              ctypes.byref(st)))
+    return st.as_dict()
 
 
 def fqnm_roe_transfer_device(plan: Plan, qL, qR):

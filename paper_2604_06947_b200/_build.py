@@ -22,8 +22,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", CSRC, "-I", INCLUDE]
 UNITS = {
     "fqnm_api.cu": [],
-    # kernels_scalar.cu is compiled as 8 parts (separate translation units) in parallel
-    **{f"kernels_scalar_p{k}.cu": [] for k in range(1, 9)},
+    # kernels_scalar.cu is compiled as 10 parts (separate translation units) in parallel
+    **{f"kernels_scalar_p{k}.cu": [] for k in range(1, 11)},
     "kernels_euler.cu": ["-fmad=false"],
     "kernels_diag.cu": [],
 }

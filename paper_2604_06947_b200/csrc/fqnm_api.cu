@@ -245,7 +245,12 @@ static bool generic_headroom(const HostMap& m, int64_t a)
 static int build_rule(fqnm_plan_t* p)
 {
     fqnm_plan_desc& d = p->d;
-    const int kind = d.flux_kind;
+    // two-point kinds (Thm P:262-280) reuse the rule builder of their split
+    // counterpart for kappa, coefficients and the admissible range
+    const int tp_kind = (d.flux_kind == FQNM_BURGERS_GODUNOV || d.flux_kind == FQNM_BURGERS_EO2 ||
+                         d.flux_kind == FQNM_BURGERS_LF2) ? d.flux_kind : 0;
+    const int kind = tp_kind == FQNM_BURGERS_LF2 ? FQNM_BURGERS_LF
+                   : tp_kind ? FQNM_BURGERS_EO : d.flux_kind;
     int64_t P = d.kappa_num, Q = d.kappa_den;
     if (kind == FQNM_LINEAR || kind == FQNM_BURGERS_EO) {
         if (P == 0 && Q == 0) {
@@ -374,6 +379,18 @@ static int build_rule(fqnm_plan_t* p)
         int64_t amax = (lo < 0 ? -lo : lo) > hi ? (lo < 0 ? -lo : lo) : hi;
         p->rule = (eo_fast_ok && amax <= a_fast) ? (P == 1 ? R_EO_P1 : R_EO_FAST) : R_GENERIC;
     }
+    if (tp_kind) {
+        // Phi = round(num/den), num = the two maps' numerators combined (max for Godunov):
+        // |num| <= 2 (|c2| a^2 + |c1| a) on the range; int64 headroom for round_div_i64
+        const int64_t amax = (lo < 0 ? -lo : lo) > hi ? (lo < 0 ? -lo : lo) : hi;
+        const HostMap& m = p->hp;
+        i128 A = amax;
+        i128 num = 2 * ((i128)(m.c2 < 0 ? -m.c2 : m.c2) * A * A + (i128)(m.c1 < 0 ? -m.c1 : m.c1) * A);
+        if (2 * num + m.den >= ((i128)1 << 62))
+            return fail(FQNM_ERR_RANGE, "int64 headroom exceeded for the two-point rule");
+        p->rule = R_TWOPOINT;
+        p->dep_left = p->dep_right = true;
+    }
     p->lo = lo;
     p->hi = hi;
 
@@ -396,6 +413,12 @@ static int build_rule(fqnm_plan_t* p)
         float cf = (float)target;
         while ((double)cf > target) cf = std::nextafterf(cf, 0.0f);
         r.eo_cf = cf;
+    }
+    if (p->rule == R_TWOPOINT) {
+        r.tp_kind = tp_kind;
+        r.tp_c2 = p->hp.c2;
+        r.tp_c1 = tp_kind == FQNM_BURGERS_LF2 ? p->hp.c1 : 0;
+        r.tp_den = p->hp.den;
     }
     if (p->rule == R_EO_FAST || p->rule == R_EO_P1) {
         r.eo_ntwoP = (int32_t)(-2 * P);
@@ -1209,6 +1232,8 @@ extern "C" int fqnm_transfer(const fqnm_plan_t* p, int64_t q, int64_t* phi_plus,
 {
     if (!p || !phi_plus || !phi_minus) return fail(FQNM_ERR_ARG, "null argument");
     if (p->d.nvar != 1) return fail(FQNM_ERR_ARG, "scalar plans only");
+    if (p->rule == R_TWOPOINT)
+        return fail(FQNM_ERR_UNSUPPORTED, "two-point rule has no split maps: use fqnm_transfer2");
     *phi_plus = host_phi(p->hp, q, p->d.rounding);
     *phi_minus = host_phi(p->hm, q, p->d.rounding);
     return FQNM_OK;
@@ -1223,6 +1248,115 @@ extern "C" int fqnm_transfer_device(const fqnm_plan_t* p, const int32_t* q, int3
     CUDA_TRY(launch_transfer(p->rule, q, pp, pm, n, p->dr, p->st));
     const_cast<fqnm_plan_t*>(p)->launches++;
     return FQNM_OK;
+}
+
+static int64_t host_transfer2(const fqnm_plan_t* p, int64_t qL, int64_t qR)
+{
+    const int rd = p->d.rounding;
+    if (p->rule != R_TWOPOINT) return host_phi(p->hp, qL, rd) + host_phi(p->hm, qR, rd);
+    const DevRule& r = p->dr;
+    const i128 L = qL, R = qR;
+    i128 num;
+    if (r.tp_kind == FQNM_BURGERS_LF2) {
+        num = (i128)r.tp_c2 * (L * L + R * R) + (i128)r.tp_c1 * (L - R);
+    } else {
+        const i128 a = L > 0 ? L : 0, b = R < 0 ? R : 0;
+        num = (i128)r.tp_c2 * (r.tp_kind == FQNM_BURGERS_GODUNOV ? (a * a > b * b ? a * a : b * b)
+                                                                : a * a + b * b);
+    }
+    return (int64_t)round128(num, r.tp_den, rd);
+}
+
+extern "C" int fqnm_transfer2(const fqnm_plan_t* p, int64_t qL, int64_t qR, int64_t* T)
+{
+    if (!p || !T) return fail(FQNM_ERR_ARG, "null argument");
+    if (p->d.nvar != 1 || p->family == 7) return fail(FQNM_ERR_ARG, "1D scalar plans only");
+    *T = host_transfer2(p, qL, qR);
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_transfer2_device(const fqnm_plan_t* p, const int32_t* qL, const int32_t* qR,
+                                     int32_t* T, int64_t n)
+{
+    if (!p || !qL || !qR || !T) return fail(FQNM_ERR_ARG, "null argument");
+    if (p->d.nvar != 1 || p->family == 7) return fail(FQNM_ERR_ARG, "1D scalar plans only");
+    if (n <= 0) return FQNM_OK;
+    CUDA_TRY(launch_transfer2(p->rule, qL, qR, T, n, p->dr, p->st));
+    const_cast<fqnm_plan_t*>(p)->launches++;
+    return FQNM_OK;
+}
+
+extern "C" int fqnm_equivalence(fqnm_plan_t* a, const fqnm_plan_t* b, void* q, int64_t nsteps,
+                                int64_t pair_capacity, fqnm_equivalence_stats* out)
+{
+    if (!a || !b || !q || !out) return fail(FQNM_ERR_ARG, "null argument");
+    if (nsteps < 0 || pair_capacity < 0) return fail(FQNM_ERR_ARG, "nsteps and pair_capacity must be >= 0");
+    const fqnm_plan_desc &da = a->d, &db = b->d;
+    if (da.nvar != 1 || db.nvar != 1 || a->family == 7 || b->family == 7)
+        return fail(FQNM_ERR_ARG, "equivalence needs 1D scalar plans");
+    if (da.batch != 1 || db.batch != 1 || da.boundary == FQNM_HALO || db.boundary == FQNM_HALO)
+        return fail(FQNM_ERR_ARG, "equivalence needs single, unsplit problems");
+    if (da.n_local != db.n_local || da.boundary != db.boundary)
+        return fail(FQNM_ERR_ARG, "plans differ in N or boundary");
+    if (((uintptr_t)q & 3) != 0) return fail(FQNM_ERR_ARG, "q must be 4-byte aligned");
+    const int64_t n = da.n_local;
+    const int bm = da.boundary == FQNM_PERIODIC ? BM_PERIODIC : BM_TRANSMISSIVE;
+    std::memset(out, 0, sizeof *out);
+    // pair table over the union of the two plans' ranges
+    const int64_t lo = a->lo < b->lo ? a->lo : b->lo, hi = a->hi > b->hi ? a->hi : b->hi;
+    const int64_t L = hi - lo + 1;
+    unsigned long long cap = 0;
+    if (pair_capacity > 0) {
+        if (L >= ((int64_t)1 << 31)) return fail(FQNM_ERR_ARG, "range too wide for pair tracking");
+        cap = 1;
+        while ((int64_t)cap < pair_capacity) cap <<= 1;
+    }
+    int32_t *buf = nullptr, *T = nullptr;
+    unsigned long long *counters = nullptr, *keys = nullptr, *cnt2 = nullptr;
+    unsigned int* vals = nullptr;
+    int rc = FQNM_OK;
+    cudaError_t e = cudaSuccess;
+    const unsigned long long init[3] = {0ull, ~0ull, 0ull};
+    unsigned long long hc[3] = {0, 0, 0}, h2[2] = {0, 0};
+    cudaStream_t st = a->st;
+    auto ok = [&](cudaError_t x) { if (x != cudaSuccess && e == cudaSuccess) e = x; return e == cudaSuccess; };
+    if (ok(cudaMalloc(&buf, (size_t)n * 4)) && ok(cudaMalloc(&T, (size_t)(n + 1) * 4)) &&
+        ok(cudaMalloc(&counters, 3 * sizeof(unsigned long long))) &&
+        ok(cudaMalloc(&cnt2, 2 * sizeof(unsigned long long))) &&
+        ok(cudaMemcpyAsync(counters, init, sizeof init, cudaMemcpyHostToDevice, st)) &&
+        ok(cudaMemsetAsync(cnt2, 0, 2 * sizeof(unsigned long long), st))) {
+        if (cap) {
+            if (ok(cudaMalloc(&keys, cap * sizeof(unsigned long long))) &&
+                ok(cudaMalloc(&vals, cap * sizeof(unsigned int)))) {
+                ok(cudaMemsetAsync(keys, 0xff, cap * sizeof(unsigned long long), st));
+                ok(cudaMemsetAsync(vals, 0, cap * sizeof(unsigned int), st));
+            }
+        }
+        int32_t* cur = (int32_t*)q;
+        int32_t* nxt = buf;
+        for (int64_t s = 0; s < nsteps && e == cudaSuccess; ++s) {
+            ok(launch_equiv_step(cur, nxt, T, n, bm, a->dr, a->rule, b->dr, b->rule, s, counters,
+                                 keys, vals, cap ? cap - 1 : 0, lo, L, st));
+            a->launches += 2;
+            int32_t* t = cur; cur = nxt; nxt = t;
+        }
+        if (e == cudaSuccess && cur != (int32_t*)q)
+            ok(cudaMemcpyAsync(q, cur, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+        if (e == cudaSuccess && cap) ok(launch_equiv_count(keys, vals, cap, cnt2, st));
+        if (e == cudaSuccess) ok(cudaMemcpyAsync(hc, counters, sizeof hc, cudaMemcpyDeviceToHost, st));
+        if (e == cudaSuccess) ok(cudaMemcpyAsync(h2, cnt2, sizeof h2, cudaMemcpyDeviceToHost, st));
+        if (e == cudaSuccess) ok(cudaStreamSynchronize(st));
+    }
+    cudaFree(buf); cudaFree(T); cudaFree(counters); cudaFree(cnt2); cudaFree(keys); cudaFree(vals);
+    if (e != cudaSuccess) return fail(FQNM_ERR_CUDA, "equivalence: %s", cudaGetErrorString(e));
+    const int64_t nI = bm == BM_PERIODIC ? n : n + 1;
+    out->interface_evals = nsteps * nI;
+    out->mismatches = (int64_t)hc[0];
+    out->first_mismatch_step = hc[1] == ~0ull ? -1 : (int64_t)hc[1];
+    out->overflow = (int64_t)hc[2];
+    out->visited_pairs = cap ? (int64_t)h2[0] : -1;
+    out->mismatched_pairs = cap ? (int64_t)h2[1] : -1;
+    return rc;
 }
 
 extern "C" int fqnm_roe_transfer_device(const fqnm_plan_t* p, const int64_t* qL, const int64_t* qR,
@@ -1338,7 +1472,8 @@ extern "C" int fqnm_debug_override(fqnm_plan_t* p, int32_t kernel, int32_t k, in
         V = 0;                           // consumed above
     }
     if (V) {
-        if (p->family != 2 || !blocked_has_V(V)) return fail(FQNM_ERR_UNSUPPORTED, "V override needs K2 and V in {8,16,32}");
+        if (p->family != 2 || !blocked_rule_has_V(p->rule, V))
+            return fail(FQNM_ERR_UNSUPPORTED, "V override needs K2 and V in {8,16,32} ({8,16} for two-point rules)");
         p->V = V;
     }
     if (k && p->family == 7) {

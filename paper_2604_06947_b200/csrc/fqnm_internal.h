@@ -16,6 +16,8 @@ enum RuleKind : int32_t {
     R_GENERIC = 3,    // any piecewise-quadratic map, exact int64 arithmetic, any rounding
     R_EO_P1 = 5,      // BURGERS_EO with P = 1 (kappa = 1/Q): as R_EO_FAST, remainder in the
                       // (q^2 - Q est) form, one instruction shorter (maps.cuh eo_gm_p1)
+    R_TWOPOINT = 6,   // quantised two-point rule Phi(qL, qR) rounded once (Godunov / EO2 / LF2),
+                      // exact int64 evaluation (maps.cuh tp_phi)
     R_LIN_FAST = 4    // LINEAR any |kappa| <= 1, RHA: g(|q|) = floor((2P|q| + Q)/(2Q)) by the
                       // same estimate + remainder scheme as EO (eo_* constants), sign restored
 };
@@ -40,6 +42,12 @@ struct DevRule {
     int32_t eo_nQ;        // -Q
     int32_t eo_c6;        // Q * 0x4B400001 - ceil(Q/2)  (mod 2^32)
     int32_t eo_P;         // P
+    // two-point rule (R_TWOPOINT): Phi = round(num / tp_den),
+    //   Godunov: num = c2 max(max(qL,0)^2, min(qR,0)^2); EO2: c2 (max(qL,0)^2 + min(qR,0)^2);
+    //   LF2: c2 (qL^2 + qR^2) + c1 (qL - qR)
+    int32_t tp_kind;      // 0 = split rule, 5 Godunov, 6 EO2, 7 LF2 (fqnm_flux_kind codes)
+    int32_t pad3;
+    int64_t tp_c2, tp_c1, tp_den;
 };
 
 enum Bmode : int32_t { BM_PERIODIC = 0, BM_TRANSMISSIVE = 1, BM_HALO = 2 };
@@ -131,6 +139,18 @@ cudaError_t launch_warp_ensemble(int rule, int V, int32_t* q, int64_t batch, int
                                  int bmode, const DevRule& r, cudaStream_t st);
 cudaError_t launch_cta_ensemble(int rule, int32_t* q, int64_t n, int64_t batch, int64_t nsteps,
                                 int bmode, const DevRule& r, cudaStream_t st);
+cudaError_t launch_transfer2(int rule, const int32_t* qL, const int32_t* qR, int32_t* T, int64_t n,
+                             const DevRule& r, cudaStream_t st);
+// transfer-operator equivalence checker (kernels_diag.cu): one step of rule a with
+// rule b evaluated on every interface; counters: [0] mismatches, [1] first step (min),
+// [2] table overflow
+cudaError_t launch_equiv_step(const int32_t* q, int32_t* qn, int32_t* T, int64_t n, int bmode,
+                              const DevRule& ra, int rule_a, const DevRule& rb, int rule_b,
+                              int64_t step, unsigned long long* counters, unsigned long long* keys,
+                              unsigned int* vals, unsigned long long mask, int64_t lo, int64_t L,
+                              cudaStream_t st);
+cudaError_t launch_equiv_count(const unsigned long long* keys, const unsigned int* vals,
+                               unsigned long long cap, unsigned long long* out2, cudaStream_t st);
 cudaError_t launch_transfer(int rule, const int32_t* q, int32_t* pp, int32_t* pm, int64_t n,
                             const DevRule& r, cudaStream_t st);
 cudaError_t launch_minmax(const void* q, int dtype, int64_t n, long long* out2, cudaStream_t st);
@@ -142,6 +162,7 @@ cudaError_t launch_roe_transfer(const int64_t* qL, const int64_t* qR, int64_t* T
 
 int blocked_max_V();
 bool blocked_has_V(int V);
+bool blocked_rule_has_V(int rule, int V);
 bool warp_ensemble_has_V(int V);
 bool euler_has_V(int V);
 

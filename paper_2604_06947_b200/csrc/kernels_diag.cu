@@ -5,10 +5,13 @@
 //   rho = max_{k'} |sum_k M_{k'k} - 1|  over the union of the two supports.
 // Kernels: a dense level histogram (global atomics), an entropy reduction over
 // the histogram, and an open-addressing hash aggregation of (k, k') pairs.
+// Also the transfer-operator equivalence checker (Thm P:262-280): one explicit
+// step of rule a while rule b is evaluated on every visited interface state.
 #include <cstdint>
 #include <cuda_runtime.h>
 
 #include "fqnm_internal.h"
+#include "maps.cuh"
 
 namespace fqnm {
 
@@ -157,6 +160,125 @@ cudaError_t launch_defect(const double* rowsum, const unsigned int* c0, const un
                           int64_t L, unsigned long long* maxbits, cudaStream_t st)
 {
     k_defect<<<grid_for_diag(L), 256, 0, st>>>(rowsum, c0, c1, L, maxbits);
+    return cudaGetLastError();
+}
+
+// ---- transfer-operator equivalence (Thm P:262-280) -------------------------
+__device__ __forceinline__ int32_t transfer_any(int rule, int32_t qL, int32_t qR, const DevRule& r)
+{
+    switch (rule) {
+        case R_LIN_HALF: return transfer_lr<R_LIN_HALF>(qL, qR, r);
+        case R_EO_FAST: return transfer_lr<R_EO_FAST>(qL, qR, r);
+        case R_EO_P1: return transfer_lr<R_EO_P1>(qL, qR, r);
+        case R_LIN_FAST: return transfer_lr<R_LIN_FAST>(qL, qR, r);
+        case R_TWOPOINT: return transfer_lr<R_TWOPOINT>(qL, qR, r);
+        default: return transfer_lr<R_GENERIC>(qL, qR, r);
+    }
+}
+
+// interfaces t = 0 .. nI-1: periodic nI = n, interface t + 1/2 between cells t and
+// (t+1) mod n; transmissive nI = n + 1, interface t - 1/2 between t-1 and t (ghost copies)
+__global__ void k_equiv_transfer(const int32_t* __restrict__ q, int32_t* __restrict__ T, int64_t n,
+                                 int bmode, DevRule ra, int rule_a, DevRule rb, int rule_b,
+                                 int64_t step, unsigned long long* __restrict__ counters,
+                                 unsigned long long* __restrict__ keys,
+                                 unsigned int* __restrict__ vals, unsigned long long mask,
+                                 int64_t lo, int64_t L)
+{
+    const int64_t nI = bmode == BM_PERIODIC ? n : n + 1;
+    unsigned long long mism = 0;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nI;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t iL, iR;
+        if (bmode == BM_PERIODIC) { iL = t; iR = (t + 1 == n) ? 0 : t + 1; }
+        else { iL = t == 0 ? 0 : t - 1; iR = t == n ? n - 1 : t; }
+        const int32_t qL = q[iL], qR = q[iR];
+        const int32_t Ta = transfer_any(rule_a, qL, qR, ra);
+        const int32_t Tb = transfer_any(rule_b, qL, qR, rb);
+        T[t] = Ta;
+        const bool bad = Ta != Tb;
+        mism += bad;
+        if (mask) {
+            const int64_t a = (int64_t)qL - lo, b = (int64_t)qR - lo;
+            if (a < 0 || a >= L || b < 0 || b >= L) {
+                atomicAdd(counters + 2, 1ull);
+            } else {
+                const unsigned long long key = (unsigned long long)a * (unsigned long long)L +
+                                               (unsigned long long)b;
+                unsigned long long h = (key * 0x9E3779B97F4A7C15ull) & mask;
+                bool done = false;
+                for (unsigned long long probe = 0; probe <= mask; ++probe) {
+                    const unsigned long long prev = atomicCAS(keys + h, EMPTY, key);
+                    if (prev == EMPTY || prev == key) {
+                        atomicOr(vals + h, bad ? 3u : 1u);
+                        done = true;
+                        break;
+                    }
+                    h = (h + 1) & mask;
+                }
+                if (!done) atomicAdd(counters + 2, 1ull);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mism += __shfl_xor_sync(0xffffffffu, mism, o);
+    if ((threadIdx.x & 31) == 0 && mism) {
+        atomicAdd(counters, mism);
+        atomicMin(counters + 1, (unsigned long long)step);
+    }
+}
+
+// q'_i = q_i - (T_{i+1/2} - T_{i-1/2})  (P:86-89 with the transfer of rule a)
+__global__ void k_equiv_update(const int32_t* __restrict__ q, const int32_t* __restrict__ T,
+                               int32_t* __restrict__ qn, int64_t n, int bmode)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t Tr = bmode == BM_PERIODIC ? T[i] : T[i + 1];
+        const int32_t Tl = bmode == BM_PERIODIC ? T[i == 0 ? n - 1 : i - 1] : T[i];
+        qn[i] = q[i] - (Tr - Tl);
+    }
+}
+
+__global__ void k_equiv_count(const unsigned long long* __restrict__ keys,
+                              const unsigned int* __restrict__ vals, unsigned long long cap,
+                              unsigned long long* __restrict__ out2)
+{
+    unsigned long long v = 0, m = 0;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < cap;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        if (keys[i] != EMPTY) {
+            ++v;
+            m += (vals[i] >> 1) & 1u;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+        m += __shfl_xor_sync(0xffffffffu, m, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out2, v);
+        atomicAdd(out2 + 1, m);
+    }
+}
+
+cudaError_t launch_equiv_step(const int32_t* q, int32_t* qn, int32_t* T, int64_t n, int bmode,
+                              const DevRule& ra, int rule_a, const DevRule& rb, int rule_b,
+                              int64_t step, unsigned long long* counters, unsigned long long* keys,
+                              unsigned int* vals, unsigned long long mask, int64_t lo, int64_t L,
+                              cudaStream_t st)
+{
+    k_equiv_transfer<<<grid_for_diag(n + 1), 256, 0, st>>>(q, T, n, bmode, ra, rule_a, rb, rule_b,
+                                                           step, counters, keys, vals, mask, lo, L);
+    k_equiv_update<<<grid_for_diag(n), 256, 0, st>>>(q, T, qn, n, bmode);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_equiv_count(const unsigned long long* keys, const unsigned int* vals,
+                               unsigned long long cap, unsigned long long* out2, cudaStream_t st)
+{
+    k_equiv_count<<<grid_for_diag((int64_t)cap), 256, 0, st>>>(keys, vals, cap, out2);
     return cudaGetLastError();
 }
 

@@ -99,6 +99,26 @@ __device__ __forceinline__ void one_step(int32_t (&q)[V], const DevRule& r, int 
         q[0] = pl * r.one + h[0];
 #pragma unroll
         for (int j = 1; j < V; ++j) q[j] = p[j - 1] * r.one + h[j];
+    } else if (RULE == R_TWOPOINT) {
+        // two-point rule: T_{j+1/2} = Phi(q_j, q_{j+1}); needs the right neighbour's state
+        const int32_t qr = NB == 0 ? __shfl_down_sync(FULL, q[0], 1)
+                                   : __shfl_sync(FULL, q[0], (lane + 1) & 31);
+        int32_t T[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            int32_t qn = (j + 1 < V) ? q[j + 1] : qr;
+            if (WALL && g0 + j == n - 1) qn = q[j];             // ghost q_N = q_{N-1}
+            T[j] = tp_phi(q[j], qn, r);
+        }
+        int32_t Tl = NB == 0 ? __shfl_up_sync(FULL, T[V - 1], 1)
+                             : __shfl_sync(FULL, T[V - 1], (lane + 31) & 31);
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            if (WALL && g0 + j == 0) Tl = tp_phi(q[j], q[j], r);  // ghost q_{-1} = q_0
+            const int32_t t = T[j];
+            q[j] = q[j] + Tl - t;
+            Tl = t;
+        }
     } else {
         int32_t g[V], m[V];
         eval_maps<RULE, V>(q, g, m, r);
@@ -166,7 +186,7 @@ __device__ __forceinline__ void run_window_steps(int32_t (&q)[V], int ksteps, co
                                                  int64_t g0, int64_t n)
 {
     const int lane = threadIdx.x & 31;
-    if (FQNM_FUSED_STEPS && !WALL && ksteps > 0) {
+    if (FQNM_FUSED_STEPS && RULE != R_TWOPOINT && !WALL && ksteps > 0) {
         int32_t g[V], m[V];
         if (RULE == R_LIN_HALF) {
 #pragma unroll
@@ -437,6 +457,10 @@ __global__ void k_naive(const int32_t* __restrict__ src, int32_t* __restrict__ d
         } else {
             if (il < 0) il = 0;
             if (ir >= n) ir = n - 1;
+        }
+        if (RULE == R_TWOPOINT) {
+            dst[b * n + i] = s[i] - (tp_phi(s[i], s[ir], r) - tp_phi(s[il], s[i], r));
+            continue;
         }
         int32_t pl, ml, pc, mc, pr, mr;
         phi_pm<RULE>(s[il], pl, ml, r);
@@ -753,6 +777,22 @@ __global__ void __launch_bounds__(1024) k_cta_ensemble(int32_t* __restrict__ q, 
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) Q[i] = qb[i];
     __syncthreads();
     for (int64_t s = 0; s < nsteps; ++s) {
+        if (RULE == R_TWOPOINT) {
+            // P[i] = T_{i+1/2} = Phi(q_i, q_{i+1}) (ghost/wrap as the boundary says)
+            for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+                int64_t ir = i + 1;
+                if (ir >= n) ir = (bmode == BM_PERIODIC) ? 0 : n - 1;
+                P[i] = tp_phi(Q[i], Q[ir], r);
+            }
+            __syncthreads();
+            for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+                const int32_t Fl = (i > 0) ? P[i - 1]
+                                 : (bmode == BM_PERIODIC ? P[n - 1] : tp_phi(Q[0], Q[0], r));
+                Q[i] = Q[i] - (P[i] - Fl);
+            }
+            __syncthreads();
+            continue;
+        }
         for (int64_t i = threadIdx.x; i < n; i += blockDim.x) phi_pm<RULE>(Q[i], P[i], M[i], r);
         __syncthreads();
         for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
@@ -876,6 +916,21 @@ extern template cudaError_t blocked_v<R_GENERIC, 32, 2>(const BlockedArgs&, cons
 #endif
 template cudaError_t blocked_rule<R_GENERIC>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
 #endif
+// two-point rules: V = 8 or 16, no register-cap variants (int64 evaluation)
+template <>
+cudaError_t blocked_rule<R_TWOPOINT>(int V, int minb, const BlockedArgs& a, const DevRule& r,
+                                     cudaStream_t st, int cap);
+#if FQNM_PART(9)
+template <>
+cudaError_t blocked_rule<R_TWOPOINT>(int V, int minb, const BlockedArgs& a, const DevRule& r,
+                                     cudaStream_t st, int cap)
+{
+    if (minb) return cudaErrorInvalidValue;
+    if (V == 8) return blocked_v<R_TWOPOINT, 8, 1>(a, r, st, cap);
+    if (V == 16) return blocked_v<R_TWOPOINT, 16, 1>(a, r, st, cap);
+    return cudaErrorInvalidValue;
+}
+#endif
 #if FQNM_PART(7)
 template cudaError_t blocked_rule<R_LIN_FAST>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
 #endif
@@ -888,6 +943,7 @@ extern template cudaError_t blocked_rule<R_GENERIC>(int, int, const BlockedArgs&
 extern template cudaError_t blocked_rule<R_LIN_FAST>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
 #endif
 bool blocked_has_V(int V) { return V == 8 || V == 16 || V == 32; }
+bool blocked_rule_has_V(int rule, int V) { return rule == R_TWOPOINT ? (V == 8 || V == 16) : blocked_has_V(V); }
 int blocked_max_V() { return 32; }
 
 cudaError_t launch_blocked(int rule, int V, int minb, const BlockedArgs& a, const DevRule& r,
@@ -899,6 +955,7 @@ cudaError_t launch_blocked(int rule, int V, int minb, const BlockedArgs& a, cons
         case R_EO_P1: return blocked_rule<R_EO_P1>(V, minb, a, r, st, grid_cap);
         case R_GENERIC: return blocked_rule<R_GENERIC>(V, minb, a, r, st, grid_cap);
         case R_LIN_FAST: return blocked_rule<R_LIN_FAST>(V, minb, a, r, st, grid_cap);
+        case R_TWOPOINT: return blocked_rule<R_TWOPOINT>(V, minb, a, r, st, grid_cap);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -914,6 +971,7 @@ cudaError_t launch_naive(int rule, const int32_t* src, int32_t* dst, int64_t n, 
         case R_EO_P1: k_naive<R_EO_P1><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
         case R_GENERIC: k_naive<R_GENERIC><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
         case R_LIN_FAST: k_naive<R_LIN_FAST><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
+        case R_TWOPOINT: k_naive<R_TWOPOINT><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -955,6 +1013,9 @@ template cudaError_t warp_rule<R_EO_FAST>(int, int32_t*, int64_t, int64_t, int, 
 template cudaError_t warp_rule<R_EO_P1>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
 template cudaError_t warp_rule<R_LIN_FAST>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
 #endif
+#if FQNM_PART(10)
+template cudaError_t warp_rule<R_TWOPOINT>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
+#endif
 #if FQNM_PART(4)
 template cudaError_t warp_rule<R_GENERIC>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
 #endif
@@ -990,12 +1051,14 @@ int resident_capacity_warps(int rule, int V)
           : rule == R_EO_FAST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_EO_FAST, 8>, 256, 0)
           : rule == R_EO_P1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_EO_P1, 8>, 256, 0)
           : rule == R_LIN_FAST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_LIN_FAST, 8>, 256, 0)
+          : rule == R_TWOPOINT ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_TWOPOINT, 8>, 256, 0)
           : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_GENERIC, 8>, 256, 0);
     } else {
         e = rule == R_LIN_HALF ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_LIN_HALF, 4>, 256, 0)
           : rule == R_EO_FAST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_EO_FAST, 4>, 256, 0)
           : rule == R_EO_P1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_EO_P1, 4>, 256, 0)
           : rule == R_LIN_FAST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_LIN_FAST, 4>, 256, 0)
+          : rule == R_TWOPOINT ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_TWOPOINT, 4>, 256, 0)
           : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_GENERIC, 4>, 256, 0);
     }
     if (e != cudaSuccess) return 0;
@@ -1014,6 +1077,7 @@ cudaError_t launch_resident(int rule, int V, const ResidentArgsHost& h, const De
         case R_EO_P1: return V == 8 ? resident_v<R_EO_P1, 8>(h, r, st) : resident_v<R_EO_P1, 4>(h, r, st);
         case R_GENERIC: return V == 8 ? resident_v<R_GENERIC, 8>(h, r, st) : resident_v<R_GENERIC, 4>(h, r, st);
         case R_LIN_FAST: return V == 8 ? resident_v<R_LIN_FAST, 8>(h, r, st) : resident_v<R_LIN_FAST, 4>(h, r, st);
+        case R_TWOPOINT: return V == 8 ? resident_v<R_TWOPOINT, 8>(h, r, st) : resident_v<R_TWOPOINT, 4>(h, r, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -1023,6 +1087,7 @@ cudaError_t launch_resident(int rule, int V, const ResidentArgsHost& h, const De
 #if FQNM_PART(3)
 #if FQNM_SCALAR_PART == 3
 extern template cudaError_t warp_rule<R_GENERIC>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
+extern template cudaError_t warp_rule<R_TWOPOINT>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
 #endif
 bool warp_ensemble_has_V(int V) { return V == 1 || V == 2 || V == 4 || V == 8 || V == 16 || V == 32; }
 
@@ -1035,6 +1100,7 @@ cudaError_t launch_warp_ensemble(int rule, int V, int32_t* q, int64_t batch, int
         case R_EO_P1: return warp_rule<R_EO_P1>(V, q, batch, nsteps, bmode, r, st);
         case R_GENERIC: return warp_rule<R_GENERIC>(V, q, batch, nsteps, bmode, r, st);
         case R_LIN_FAST: return warp_rule<R_LIN_FAST>(V, q, batch, nsteps, bmode, r, st);
+        case R_TWOPOINT: return warp_rule<R_TWOPOINT>(V, q, batch, nsteps, bmode, r, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -1064,6 +1130,7 @@ cudaError_t launch_cta_ensemble(int rule, int32_t* q, int64_t n, int64_t batch, 
         case R_EO_P1: return cta_rule<R_EO_P1>(q, n, batch, nsteps, bmode, r, st);
         case R_GENERIC: return cta_rule<R_GENERIC>(q, n, batch, nsteps, bmode, r, st);
         case R_LIN_FAST: return cta_rule<R_LIN_FAST>(q, n, batch, nsteps, bmode, r, st);
+        case R_TWOPOINT: return cta_rule<R_TWOPOINT>(q, n, batch, nsteps, bmode, r, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -1071,6 +1138,31 @@ cudaError_t launch_cta_ensemble(int rule, int32_t* q, int64_t n, int64_t batch, 
 #endif  // part 2
 
 #if FQNM_PART(1)
+template <int RULE>
+__global__ void k_transfer2(const int32_t* __restrict__ qL, const int32_t* __restrict__ qR,
+                            int32_t* __restrict__ T, int64_t n, DevRule r)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        T[i] = transfer_lr<RULE>(qL[i], qR[i], r);
+}
+
+cudaError_t launch_transfer2(int rule, const int32_t* qL, const int32_t* qR, int32_t* T, int64_t n,
+                             const DevRule& r, cudaStream_t st)
+{
+    int g = grid_for(n, 256, 148 * 16);
+    switch (rule) {
+        case R_LIN_HALF: k_transfer2<R_LIN_HALF><<<g, 256, 0, st>>>(qL, qR, T, n, r); break;
+        case R_EO_FAST: k_transfer2<R_EO_FAST><<<g, 256, 0, st>>>(qL, qR, T, n, r); break;
+        case R_EO_P1: k_transfer2<R_EO_P1><<<g, 256, 0, st>>>(qL, qR, T, n, r); break;
+        case R_GENERIC: k_transfer2<R_GENERIC><<<g, 256, 0, st>>>(qL, qR, T, n, r); break;
+        case R_LIN_FAST: k_transfer2<R_LIN_FAST><<<g, 256, 0, st>>>(qL, qR, T, n, r); break;
+        case R_TWOPOINT: k_transfer2<R_TWOPOINT><<<g, 256, 0, st>>>(qL, qR, T, n, r); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_transfer(int rule, const int32_t* q, int32_t* pp, int32_t* pm, int64_t n,
                             const DevRule& r, cudaStream_t st)
 {

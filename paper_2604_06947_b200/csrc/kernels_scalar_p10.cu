@@ -1,0 +1,3 @@
+// Part 10 of kernels_scalar.cu, compiled as its own translation unit (see _build.py).
+#define FQNM_SCALAR_PART 10
+#include "kernels_scalar.cu"

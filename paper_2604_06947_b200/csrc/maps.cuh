@@ -198,4 +198,34 @@ __device__ __forceinline__ void phi_pm(int32_t q, int32_t& p, int32_t& m, const 
     p = g - m;
 }
 
+// Quantised two-point transfer rule, rounded once (Thm transfer-operator
+// equivalence; include/fqnm.h FQNM_BURGERS_GODUNOV/EO2/LF2):
+// Phi(qL, qR) = round(num / den) with num from the plan's integer coefficients,
+// evaluated exactly in int64 (headroom validated by the planner).
+__device__ __forceinline__ int32_t tp_phi(int32_t qL, int32_t qR, const DevRule& r)
+{
+    const int64_t L = qL, R = qR;
+    int64_t num;
+    if (r.tp_kind == 7) {
+        num = r.tp_c2 * (L * L + R * R) + r.tp_c1 * (L - R);
+    } else {
+        const int64_t a = L > 0 ? L : 0, b = R < 0 ? R : 0;
+        const int64_t A = a * a, B = b * b;
+        num = r.tp_c2 * (r.tp_kind == 5 ? (A > B ? A : B) : A + B);
+    }
+    return (int32_t)round_div_i64(num, r.tp_den, r.rounding);
+}
+
+// Interface transfer T = Phi(qL, qR) of any scalar rule: split rules
+// phi+(qL) + phi-(qR), two-point rules tp_phi.
+template <int RULE>
+__device__ __forceinline__ int32_t transfer_lr(int32_t qL, int32_t qR, const DevRule& r)
+{
+    if (RULE == R_TWOPOINT) return tp_phi(qL, qR, r);
+    int32_t pL, mL, pR, mR;
+    phi_pm<RULE>(qL, pL, mL, r);
+    phi_pm<RULE>(qR, pR, mR, r);
+    return pL + mR;
+}
+
 }  // namespace fqnm

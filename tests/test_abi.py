@@ -107,7 +107,8 @@ def test_d8_admissible_range_matches_oracle(F):
     (dict(n_local=64, delta=1e-4, dt_dx=1.25, flux_kind=0), 2),              # nu > 1
     (dict(n_local=64, delta=1e-3, dt_dx=1 / 3, flux_kind=2, flux_param=1.2,
           q_range=(-1200, 1200)), 2),                                        # LF breaks D8
-    (dict(n_local=64, delta=1e-4, dt_dx=0.5, flux_kind=7), 1),
+    (dict(n_local=64, delta=1e-4, dt_dx=0.5, flux_kind=9), 1),                # unknown kind
+    (dict(n_local=64, delta=1e-4, dt_dx=0.5, flux_kind=7), 1),                # LF2 needs alpha
     (dict(n_local=64, delta=1e-4, dt_dx=0.5, flux_kind=0, boundary=9), 1),
     (dict(n_local=64, delta=1e-4, dt_dx=0.5, flux_kind=3), 1),               # Euler needs nvar 3
 ])
@@ -131,3 +132,19 @@ def test_gpu_entry_points_fail_loudly_without_gpu(F):
         q = torch.zeros(8, dtype=torch.int32)
         plan = F.Plan(ctypes.c_void_p(), F.make_desc(8, 1e-4, 0.5))
         F.fqnm_step(plan, q, 1)
+
+
+def test_two_point_rules_validate(F):
+    """Two-point kinds (Thm P:262-280) build R_TWOPOINT (6) with the admissible range
+    of their split counterpart and the same kappa."""
+    for kind, split in ((F.BURGERS_GODUNOV, F.BURGERS_EO), (F.BURGERS_EO2, F.BURGERS_EO)):
+        info = F.fqnm_plan_validate(65536, 1e-5, 4 / 15, kind)
+        ref = F.fqnm_plan_validate(65536, 1e-5, 4 / 15, split)
+        assert info["rule"] == 6
+        assert (info["kappa_num"], info["kappa_den"]) == (ref["kappa_num"], ref["kappa_den"])
+        assert (info["q_lo"], info["q_hi"]) == (ref["q_lo"], ref["q_hi"])
+        assert info["kernel"] == ref["kernel"]
+    info = F.fqnm_plan_validate(1 << 20, 1e-3, 0.5, F.BURGERS_LF2, flux_param=1.0)
+    ref = F.fqnm_plan_validate(1 << 20, 1e-3, 0.5, F.BURGERS_LF, flux_param=1.0)
+    assert info["rule"] == 6 and info["kernel"] == 2 and info["cells_per_thread"] == 8
+    assert (info["q_lo"], info["q_hi"]) == (ref["q_lo"], ref["q_hi"])
