@@ -108,6 +108,11 @@ def lib():
         L.or_step_transfer.argtypes = [PT, ctypes.c_int, ctypes.c_int64, P64, P64]
         L.or_run_transfer.argtypes = [PT, ctypes.c_int, ctypes.c_int64, P64, ctypes.c_int64,
                                       ctypes.c_int]
+        PPM = ctypes.POINTER(PM)
+        L.or_step_scalar_3d.argtypes = [PPM, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                        ctypes.c_int64, P64, P64]
+        L.or_run_scalar_3d.argtypes = [PPM, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                       ctypes.c_int64, P64, ctypes.c_int64, ctypes.c_int]
         L.or_round_rational.restype = ctypes.c_int64
         L.or_round_rational.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64,
                                         ctypes.c_int]
@@ -282,6 +287,34 @@ class Rule2D:
         q = np.array(q, dtype=np.int64, copy=True, order="C")
         ny, nx = q.shape
         lib().or_run_scalar_2d(*self._maps(), boundary, nx, ny, _p64(q), nsteps, nthreads)
+        return q
+
+
+class Rule3D:
+    """Directional composition in 3D (Thm P:364-401, d = 3): one scalar Rule per
+    direction (same flux kind and delta; dt/dx, dt/dy, dt/dz; per-direction param).
+    State layout [nz][ny][nx] (x fastest)."""
+
+    def __init__(self, kind: int, delta, dt_dx, dt_dy, dt_dz, params=(1, 1, 1),
+                 rounding: int = RHA):
+        self.rs = [Rule(kind, delta, l, Fraction(a), rounding)
+                   for l, a in zip((dt_dx, dt_dy, dt_dz), params)]
+        maps = []
+        for r in self.rs:
+            maps += [ctypes.pointer(r._mp), ctypes.pointer(r._mm)]
+        self._maps = (ctypes.POINTER(_Map) * 6)(*maps)
+
+    def step(self, q, boundary: int = PERIODIC) -> np.ndarray:
+        q = np.ascontiguousarray(q, dtype=np.int64)
+        nz, ny, nx = q.shape
+        out = np.empty_like(q)
+        lib().or_step_scalar_3d(self._maps, boundary, nx, ny, nz, _p64(q), _p64(out))
+        return out
+
+    def run(self, q, nsteps: int, boundary: int = PERIODIC, nthreads: int = 0) -> np.ndarray:
+        q = np.array(q, dtype=np.int64, copy=True, order="C")
+        nz, ny, nx = q.shape
+        lib().or_run_scalar_3d(self._maps, boundary, nx, ny, nz, _p64(q), nsteps, nthreads)
         return q
 
 

@@ -328,6 +328,56 @@ void or_run_scalar_2d(const or_map* ppx, const or_map* pmx, const or_map* ppy, c
     free(b);
 }
 
+/* d = 3 (Thm P:364-401, Eq. nd_transfer_rule with d = 3), unsplit:
+ *   q'_{i,j,k} = q - sum_{m = x,y,z} (F_{+e_m} - F_{-e_m}),
+ *   F_{i+1/2 e_m} = phi+_m(q_i) + phi-_m(q_{i+e_m}),  all on q^n.
+ * Layout q[(k * ny + j) * nx + i] (x fastest).  Boundaries per direction as in 1D. */
+static int64_t wrap3(int boundary, int64_t i, int64_t n)
+{
+    if (boundary == OR_PERIODIC) return (i % n + n) % n;
+    return i < 0 ? 0 : (i >= n ? n - 1 : i);
+}
+
+void or_step_scalar_3d(const or_map* const* maps, int boundary, int64_t nx, int64_t ny,
+                       int64_t nz, const int64_t* q, int64_t* out)
+{
+    /* maps = {phi+_x, phi-_x, phi+_y, phi-_y, phi+_z, phi-_z} */
+    #pragma omp parallel for schedule(static) if (nx * ny * nz >= 32768)
+    for (int64_t k = 0; k < nz; ++k)
+        for (int64_t j = 0; j < ny; ++j)
+            for (int64_t i = 0; i < nx; ++i) {
+                const int64_t c = q[(k * ny + j) * nx + i];
+                const int64_t xp = q[(k * ny + j) * nx + wrap3(boundary, i + 1, nx)];
+                const int64_t xm = q[(k * ny + j) * nx + wrap3(boundary, i - 1, nx)];
+                const int64_t yp = q[(k * ny + wrap3(boundary, j + 1, ny)) * nx + i];
+                const int64_t ym = q[(k * ny + wrap3(boundary, j - 1, ny)) * nx + i];
+                const int64_t zp = q[(wrap3(boundary, k + 1, nz) * ny + j) * nx + i];
+                const int64_t zm = q[(wrap3(boundary, k - 1, nz) * ny + j) * nx + i];
+                const int64_t Fxr = or_phi(maps[0], c) + or_phi(maps[1], xp);
+                const int64_t Fxl = or_phi(maps[0], xm) + or_phi(maps[1], c);
+                const int64_t Fyr = or_phi(maps[2], c) + or_phi(maps[3], yp);
+                const int64_t Fyl = or_phi(maps[2], ym) + or_phi(maps[3], c);
+                const int64_t Fzr = or_phi(maps[4], c) + or_phi(maps[5], zp);
+                const int64_t Fzl = or_phi(maps[4], zm) + or_phi(maps[5], c);
+                out[(k * ny + j) * nx + i] = c - (Fxr - Fxl) - (Fyr - Fyl) - (Fzr - Fzl);
+            }
+}
+
+void or_run_scalar_3d(const or_map* const* maps, int boundary, int64_t nx, int64_t ny, int64_t nz,
+                      int64_t* q, int64_t nsteps, int nthreads)
+{
+    set_threads(nthreads);
+    const size_t N = (size_t)(nx * ny * nz);
+    int64_t* a = q;
+    int64_t* b = (int64_t*)malloc(sizeof(int64_t) * N);
+    for (int64_t s = 0; s < nsteps; ++s) {
+        or_step_scalar_3d(maps, boundary, nx, ny, nz, a, b);
+        int64_t* t = a; a = b; b = t;
+    }
+    if (a != q) { memcpy(q, a, sizeof(int64_t) * N); b = a; }
+    free(b);
+}
+
 /* ---- 4. reconstruction ---------------------------------------------------- */
 void or_observe(double delta, const int64_t* q, double* u, int64_t n)
 {
