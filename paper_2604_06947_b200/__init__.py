@@ -24,7 +24,7 @@ __all__ = [
     "fqnm_plan_validate", "fqnm_profile_enable", "fqnm_profile_read", "fqnm_halo_buffers",
     "fqnm_halo_connect", "fqnm_halo_owned", "fqnm_step_group", "fqnm_ipc_export",
     "fqnm_ipc_open", "fqnm_ipc_close", "owned_tensor", "fqnm_plan_2d", "fqnm_transfer2",
-    "fqnm_transfer2_device", "fqnm_equivalence",
+    "fqnm_transfer2_device", "fqnm_equivalence", "fqnm_plan_3d",
     "LINEAR", "BURGERS_EO", "BURGERS_LF", "EULER_ROE", "EULER_ROE_DENSITY", "PERIODIC", "TRANSMISSIVE", "HALO",
     "BURGERS_GODUNOV", "BURGERS_EO2", "BURGERS_LF2",
     "I32", "I64", "ROUND_HALF_AWAY", "ROUND_FLOOR", "ROUND_HALF_EVEN", "lib_path",
@@ -124,6 +124,8 @@ def _load():
     L.fqnm_plan_ex.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(PlanDesc)]
     L.fqnm_plan_2d.argtypes = [ctypes.POINTER(vp), i64, i64, dbl, dbl, dbl, ctypes.c_int,
                                ctypes.c_int, dbl, dbl]
+    L.fqnm_plan_3d.argtypes = [ctypes.POINTER(vp), i64, i64, i64, dbl, dbl, dbl, dbl, ctypes.c_int,
+                               ctypes.c_int, dbl, dbl, dbl]
     L.fqnm_desc_init.argtypes = [ctypes.POINTER(PlanDesc)]
     L.fqnm_desc_init.restype = None
     L.fqnm_destroy.argtypes = [vp]
@@ -270,6 +272,23 @@ def fqnm_plan_2d(nx: int, ny: int, delta: float, dt_dx: float, dt_dy: float,
     d = PlanDesc()
     L.fqnm_desc_init(ctypes.byref(d))
     d.n_local = d.n_global = nx * ny
+    d.delta, d.dt_dx, d.flux_kind, d.boundary = delta, dt_dx, flux_kind, boundary
+    d.check_range = 1
+    return Plan(h, d)
+
+
+def fqnm_plan_3d(nx: int, ny: int, nz: int, delta: float, dt_dx: float, dt_dy: float,
+                 dt_dz: float, flux_kind: int = LINEAR, boundary: int = PERIODIC,
+                 params=(0.0, 0.0, 0.0)) -> "Plan":
+    """3D directional composition (Thm P:364-401, d = 3); state int32 [nz][ny][nx]."""
+    L = _load()
+    h = ctypes.c_void_p()
+    _check(L.fqnm_plan_3d(ctypes.byref(h), int(nx), int(ny), int(nz), float(delta), float(dt_dx),
+                          float(dt_dy), float(dt_dz), int(flux_kind), int(boundary),
+                          float(params[0]), float(params[1]), float(params[2])))
+    d = PlanDesc()
+    L.fqnm_desc_init(ctypes.byref(d))
+    d.n_local = d.n_global = int(nx) * int(ny) * int(nz)
     d.delta, d.dt_dx, d.flux_kind, d.boundary = delta, dt_dx, flux_kind, boundary
     d.check_range = 1
     return Plan(h, d)

@@ -26,6 +26,7 @@ UNITS = {
     **{f"kernels_scalar_p{k}.cu": [] for k in range(1, 11)},
     "kernels_euler.cu": ["-fmad=false"],
     "kernels_diag.cu": [],
+    "kernels_3d.cu": [],
 }
 HEADERS = ["fqnm_internal.h", "maps.cuh", "kernels_scalar.cu"]
 

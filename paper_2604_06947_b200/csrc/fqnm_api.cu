@@ -182,6 +182,9 @@ struct fqnm_plan {
     HostMap hpy, hmy;
     DevRule dry{};
     bool same_xy = false;
+    // 3D plans (family 8): z-direction rule
+    int64_t nz = 0;
+    DevRule drz{};
     cudaStream_t st = nullptr;
     int64_t launches = 0;
     // profiling (fqnm_profile_enable)
@@ -712,6 +715,69 @@ extern "C" int fqnm_plan_2d(fqnm_plan_t** out, int64_t nx, int64_t ny, double de
     return FQNM_OK;
 }
 
+extern "C" int fqnm_plan_3d(fqnm_plan_t** out, int64_t nx, int64_t ny, int64_t nz, double delta,
+                            double dt_dx, double dt_dy, double dt_dz, int flux_kind, int boundary,
+                            double param_x, double param_y, double param_z)
+{
+    if (!out) return fail(FQNM_ERR_ARG, "null argument");
+    *out = nullptr;
+    if (nx < 2 || ny < 2 || nz < 2) return fail(FQNM_ERR_ARG, "nx, ny and nz must be >= 2");
+    if (nx > ((int64_t)1 << 31) / ny / nz) return fail(FQNM_ERR_ARG, "nx * ny * nz must be < 2^31");
+    if (flux_kind != FQNM_LINEAR && flux_kind != FQNM_BURGERS_EO && flux_kind != FQNM_BURGERS_LF)
+        return fail(FQNM_ERR_UNSUPPORTED, "3D plans support the split scalar flux kinds");
+    if (boundary != FQNM_PERIODIC && boundary != FQNM_TRANSMISSIVE)
+        return fail(FQNM_ERR_ARG, "3D plans: boundary must be PERIODIC or TRANSMISSIVE");
+    if (!(std::isfinite(dt_dy) && dt_dy > 0 && std::isfinite(dt_dz) && dt_dz > 0))
+        return fail(FQNM_ERR_ARG, "dt_dy and dt_dz must be finite and > 0");
+    fqnm_plan_desc d;
+    fqnm_desc_init(&d);
+    d.n_local = nx * ny * nz;
+    d.n_global = d.n_local;
+    d.delta = delta;
+    d.flux_kind = flux_kind;
+    d.boundary = boundary;
+    d.check_range = 1;
+    // per-direction rules (host-only builds), then the plan with the x rule
+    fqnm_plan_t* pd[3] = {nullptr, nullptr, nullptr};
+    const double lam[3] = {dt_dx, dt_dy, dt_dz}, par[3] = {param_x, param_y, param_z};
+    for (int m = 2; m >= 0; --m) {
+        d.dt_dx = lam[m];
+        d.flux_param = par[m];
+        int rc = plan_build(&pd[m], &d, false);
+        if (rc != FQNM_OK) {
+            for (int j = 0; j < 3; ++j) delete pd[j];
+            return rc;
+        }
+    }
+    fqnm_plan_t* p = pd[0];
+    p->nx = nx;
+    p->ny = ny;
+    p->nz = nz;
+    p->dry = pd[1]->dr;
+    p->drz = pd[2]->dr;
+    p->same_xy = std::memcmp(&p->dr, &pd[1]->dr, sizeof(DevRule)) == 0 &&
+                 std::memcmp(&p->dr, &pd[2]->dr, sizeof(DevRule)) == 0;
+    for (int m = 1; m < 3; ++m) {
+        if (p->rule != pd[m]->rule) p->rule = R_GENERIC;     // all directions on the int64 path
+        p->lo = p->lo > pd[m]->lo ? p->lo : pd[m]->lo;
+        p->hi = p->hi < pd[m]->hi ? p->hi : pd[m]->hi;
+        delete pd[m];
+    }
+    p->family = 8;
+    p->V = 0;
+    p->k = 1;
+    p->scratch_bytes = state_elems(p->d) * elem_size(p->d);
+    cudaError_t e;
+    if ((e = cudaMalloc(&p->scratch, p->scratch_bytes)) != cudaSuccess ||
+        (e = cudaMalloc(&p->d_minmax, 2 * sizeof(long long))) != cudaSuccess ||
+        (e = cudaMallocHost(&p->h_minmax, 4 * sizeof(long long))) != cudaSuccess) {
+        fqnm_destroy(p);
+        return fail(FQNM_ERR_NOMEM, "allocating 3D plan buffers: %s", cudaGetErrorString(e));
+    }
+    *out = p;
+    return FQNM_OK;
+}
+
 extern "C" void fqnm_destroy(fqnm_plan_t* p)
 {
     if (!p) return;
@@ -880,6 +946,23 @@ extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
             a.ksteps = (int)(base + (b < rem ? 1 : 0));
             a.bmode = bm;
             PROF_LAUNCH(launch_step2d(p->rule, p->same_xy, a, p->dr, p->dry, p->st));
+            cur ^= 1;
+        }
+        if (cur != 0) CUDA_TRY(cudaMemcpyAsync(q, bufs[cur], bytes, cudaMemcpyDeviceToDevice, p->st));
+        return FQNM_OK;
+    }
+    if (p->family == 8) {
+        Step3DArgs a;
+        std::memset(&a, 0, sizeof a);
+        a.nx = p->nx;
+        a.ny = p->ny;
+        a.nz = p->nz;
+        a.zchunk = step3d_zchunk(p->nx, p->ny, p->nz);
+        a.bmode = bm;
+        for (int64_t s = 0; s < nsteps; ++s) {
+            a.src = (const int32_t*)bufs[cur];
+            a.dst = (int32_t*)bufs[cur ^ 1];
+            PROF_LAUNCH(launch_step3d(p->rule, p->same_xy, a, p->dr, p->dry, p->drz, p->st));
             cur ^= 1;
         }
         if (cur != 0) CUDA_TRY(cudaMemcpyAsync(q, bufs[cur], bytes, cudaMemcpyDeviceToDevice, p->st));
@@ -1270,7 +1353,7 @@ static int64_t host_transfer2(const fqnm_plan_t* p, int64_t qL, int64_t qR)
 extern "C" int fqnm_transfer2(const fqnm_plan_t* p, int64_t qL, int64_t qR, int64_t* T)
 {
     if (!p || !T) return fail(FQNM_ERR_ARG, "null argument");
-    if (p->d.nvar != 1 || p->family == 7) return fail(FQNM_ERR_ARG, "1D scalar plans only");
+    if (p->d.nvar != 1 || p->family >= 7) return fail(FQNM_ERR_ARG, "1D scalar plans only");
     *T = host_transfer2(p, qL, qR);
     return FQNM_OK;
 }
@@ -1279,7 +1362,7 @@ extern "C" int fqnm_transfer2_device(const fqnm_plan_t* p, const int32_t* qL, co
                                      int32_t* T, int64_t n)
 {
     if (!p || !qL || !qR || !T) return fail(FQNM_ERR_ARG, "null argument");
-    if (p->d.nvar != 1 || p->family == 7) return fail(FQNM_ERR_ARG, "1D scalar plans only");
+    if (p->d.nvar != 1 || p->family >= 7) return fail(FQNM_ERR_ARG, "1D scalar plans only");
     if (n <= 0) return FQNM_OK;
     CUDA_TRY(launch_transfer2(p->rule, qL, qR, T, n, p->dr, p->st));
     const_cast<fqnm_plan_t*>(p)->launches++;
@@ -1292,7 +1375,7 @@ extern "C" int fqnm_equivalence(fqnm_plan_t* a, const fqnm_plan_t* b, void* q, i
     if (!a || !b || !q || !out) return fail(FQNM_ERR_ARG, "null argument");
     if (nsteps < 0 || pair_capacity < 0) return fail(FQNM_ERR_ARG, "nsteps and pair_capacity must be >= 0");
     const fqnm_plan_desc &da = a->d, &db = b->d;
-    if (da.nvar != 1 || db.nvar != 1 || a->family == 7 || b->family == 7)
+    if (da.nvar != 1 || db.nvar != 1 || a->family >= 7 || b->family >= 7)
         return fail(FQNM_ERR_ARG, "equivalence needs 1D scalar plans");
     if (da.batch != 1 || db.batch != 1 || da.boundary == FQNM_HALO || db.boundary == FQNM_HALO)
         return fail(FQNM_ERR_ARG, "equivalence needs single, unsplit problems");
@@ -1429,6 +1512,8 @@ extern "C" int fqnm_debug_override(fqnm_plan_t* p, int32_t kernel, int32_t k, in
         if (V) p->V = V;
         return FQNM_OK;
     }
+    if (p->family == 8 && (kernel || k || V))
+        return fail(FQNM_ERR_UNSUPPORTED, "3D plans have one kernel (K8, one step per launch)");
     if (kernel >= 100) {               // K2 with a register-cap variant: 2 + 100 * minb
         p->minb = kernel / 100;
         kernel = kernel % 100;

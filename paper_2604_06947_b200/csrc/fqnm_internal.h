@@ -113,6 +113,19 @@ struct Step2DArgs {
 cudaError_t launch_step2d(int rule, bool same, const Step2DArgs& a, const DevRule& rx,
                           const DevRule& ry, cudaStream_t st);
 
+// K8: 3D directional composition, one step per launch, 2.5D z-streaming (kernels_3d.cu)
+struct Step3DArgs {
+    const int32_t* src;
+    int32_t* dst;
+    int64_t nx, ny, nz;
+    int64_t zchunk;     // z planes per CTA
+    int32_t bmode;
+    int32_t pad;
+};
+cudaError_t launch_step3d(int rule, bool same, const Step3DArgs& a, const DevRule& rx,
+                          const DevRule& ry, const DevRule& rz, cudaStream_t st);
+int64_t step3d_zchunk(int64_t nx, int64_t ny, int64_t nz);     // z planes per CTA
+
 // level-space diagnostics (kernels_diag.cu)
 cudaError_t launch_histogram(const void* q, int dtype, int64_t n, int64_t lo, int64_t L,
                              unsigned int* counts, unsigned long long* outside, cudaStream_t st);
