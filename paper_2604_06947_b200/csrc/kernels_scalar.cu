@@ -777,7 +777,7 @@ __global__ void __launch_bounds__(1024) k_cta_ensemble(int32_t* __restrict__ q, 
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) Q[i] = qb[i];
     __syncthreads();
     for (int64_t s = 0; s < nsteps; ++s) {
-        if (RULE == R_TWOPOINT) {
+        if constexpr (RULE == R_TWOPOINT) {
             // P[i] = T_{i+1/2} = Phi(q_i, q_{i+1}) (ghost/wrap as the boundary says)
             for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
                 int64_t ir = i + 1;
@@ -791,25 +791,25 @@ __global__ void __launch_bounds__(1024) k_cta_ensemble(int32_t* __restrict__ q, 
                 Q[i] = Q[i] - (P[i] - Fl);
             }
             __syncthreads();
-            continue;
-        }
-        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) phi_pm<RULE>(Q[i], P[i], M[i], r);
-        __syncthreads();
-        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-            int64_t il = i - 1, ir = i + 1;
-            int32_t Fl, Fr;
-            if (bmode == BM_PERIODIC) {
-                if (il < 0) il += n;
-                if (ir >= n) ir -= n;
-                Fl = P[il] + M[i];
-                Fr = P[i] + M[ir];
-            } else {
-                Fl = (i == 0) ? P[0] + M[0] : P[il] + M[i];
-                Fr = (i == n - 1) ? P[i] + M[i] : P[i] + M[ir];
+        } else {
+            for (int64_t i = threadIdx.x; i < n; i += blockDim.x) phi_pm<RULE>(Q[i], P[i], M[i], r);
+            __syncthreads();
+            for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+                int64_t il = i - 1, ir = i + 1;
+                int32_t Fl, Fr;
+                if (bmode == BM_PERIODIC) {
+                    if (il < 0) il += n;
+                    if (ir >= n) ir -= n;
+                    Fl = P[il] + M[i];
+                    Fr = P[i] + M[ir];
+                } else {
+                    Fl = (i == 0) ? P[0] + M[0] : P[il] + M[i];
+                    Fr = (i == n - 1) ? P[i] + M[i] : P[i] + M[ir];
+                }
+                Q[i] = Q[i] - (Fr - Fl);
             }
-            Q[i] = Q[i] - (Fr - Fl);
+            __syncthreads();
         }
-        __syncthreads();
     }
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) qb[i] = Q[i];
 }

@@ -8,6 +8,6 @@ for rep in 1 2; do for v in "$@"; do
   if [ "$WHICH" = eo ]; then
     FQNM_LIBPATH=$PWD/$B/libfqnm_$v.so TUNE_N=268435456 TUNE_V=32 TUNE_K=24 TUNE_FAM=202 timeout 120 python tools/tune.py eo | sed "s/^/$v /"
   else
-    FQNM_LIBPATH=$PWD/$B/libfqnm_$v.so TUNE_V=32 TUNE_K=64 TUNE_FAM=202 timeout 120 python tools/tune.py lin | sed "s/^/$v /"
+    FQNM_LIBPATH=$PWD/$B/libfqnm_$v.so TUNE_V=32 TUNE_K=${LIN_K:-64} TUNE_FAM=202 timeout 120 python tools/tune.py lin | sed "s/^/$v /"
   fi
 done; done
