@@ -382,6 +382,7 @@ static int build_rule(fqnm_plan_t* p)
         int64_t amax = (lo < 0 ? -lo : lo) > hi ? (lo < 0 ? -lo : lo) : hi;
         p->rule = (eo_fast_ok && amax <= a_fast) ? (P == 1 ? R_EO_P1 : R_EO_FAST) : R_GENERIC;
     }
+    int tp_fast = 0;
     if (tp_kind) {
         // Phi = round(num/den), num = the two maps' numerators combined (max for Godunov):
         // |num| <= 2 (|c2| a^2 + |c1| a) on the range; int64 headroom for round_div_i64
@@ -391,6 +392,10 @@ static int build_rule(fqnm_plan_t* p)
         i128 num = 2 * ((i128)(m.c2 < 0 ? -m.c2 : m.c2) * A * A + (i128)(m.c1 < 0 ? -m.c1 : m.c1) * A);
         if (2 * num + m.den >= ((i128)1 << 62))
             return fail(FQNM_ERR_RANGE, "int64 headroom exceeded for the two-point rule");
+        // Godunov on the EO fast path's domain: Phi = g(max(max(qL,0), -min(qR,0))) with the
+        // EO magnitude g(x) = RHA(kappa x^2) evaluated by the closed form (maps.cuh)
+        tp_fast = (tp_kind == FQNM_BURGERS_GODUNOV && (p->rule == R_EO_P1 || p->rule == R_EO_FAST))
+                      ? (p->rule == R_EO_P1 ? 1 : 2) : 0;
         p->rule = R_TWOPOINT;
         p->dep_left = p->dep_right = true;
     }
@@ -422,8 +427,9 @@ static int build_rule(fqnm_plan_t* p)
         r.tp_c2 = p->hp.c2;
         r.tp_c1 = tp_kind == FQNM_BURGERS_LF2 ? p->hp.c1 : 0;
         r.tp_den = p->hp.den;
+        r.tp_fast = tp_fast;
     }
-    if (p->rule == R_EO_FAST || p->rule == R_EO_P1) {
+    if (p->rule == R_EO_FAST || p->rule == R_EO_P1 || tp_fast) {
         r.eo_ntwoP = (int32_t)(-2 * P);
         r.eo_twoQ = (int32_t)(2 * Q);
         r.eo_c1 = (int32_t)(uint32_t)((uint64_t)(Q - 1) - (uint64_t)(2 * Q) * 0x4B400000ull);

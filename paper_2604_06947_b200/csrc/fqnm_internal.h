@@ -46,7 +46,7 @@ struct DevRule {
     //   Godunov: num = c2 max(max(qL,0)^2, min(qR,0)^2); EO2: c2 (max(qL,0)^2 + min(qR,0)^2);
     //   LF2: c2 (qL^2 + qR^2) + c1 (qL - qR)
     int32_t tp_kind;      // 0 = split rule, 5 Godunov, 6 EO2, 7 LF2 (fqnm_flux_kind codes)
-    int32_t pad3;
+    int32_t tp_fast;      // Godunov on the EO fast domain: 1 = EO P = 1 closed form, 2 = general P
     int64_t tp_c2, tp_c1, tp_den;
 };
 

@@ -204,6 +204,17 @@ __device__ __forceinline__ void phi_pm(int32_t q, int32_t& p, int32_t& m, const 
 // evaluated exactly in int64 (headroom validated by the planner).
 __device__ __forceinline__ int32_t tp_phi(int32_t qL, int32_t qR, const DevRule& r)
 {
+    if (r.tp_fast) {
+        // Godunov for Burgers: Phi = RHA(kappa max(max(qL,0)^2, min(qR,0)^2)) = g(x) with
+        // x = max(max(qL,0), -min(qR,0)) and the EO magnitude g (closed form, exact on the
+        // planner-proved domain |q| < 2^22, kappa q^2 <= 2^20)
+        const int32_t a = qL > 0 ? qL : 0, b = qR < 0 ? -qR : 0;
+        const int32_t x = a > b ? a : b;
+        int32_t g, m;
+        if (r.tp_fast == 1) eo_gm_p1<0, false>(x, g, m, r);
+        else eo_gm(x, g, m, r);
+        return g;
+    }
     const int64_t L = qL, R = qR;
     int64_t num;
     if (r.tp_kind == 7) {

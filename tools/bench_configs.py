@@ -80,6 +80,33 @@ def main():
             if os.environ.get("K2D"):
                 F.fqnm_debug_override(plan, 0, int(os.environ["K2D"]), 0)
             steps, cells = 200, nx * ny
+        elif name in ("godunov2", "godunov26"):
+            # quantised two-point Godunov rule (Thm P:262-280) on cfg2 data (K6) and on
+            # a 2^26-cell slice of cfg4 data (K2, int64 exact evaluation)
+            if name == "godunov2":
+                w = W.cfg("cfg2")
+                q0 = torch.tensor(W.q0_cfg2(), dtype=torch.int32, device="cuda")
+                plan = F.fqnm_plan(w.n, 1e-5, W.dt_dx_double(w, 150000), F.BURGERS_GODUNOV,
+                                   F.PERIODIC)
+                steps, cells = w.steps, w.n
+            else:
+                n = 1 << 26
+                q0 = W.q0_cfg4(n=1 << 31, count=n, device="cuda")
+                qmax = int(q0.abs().max())
+                plan = F.fqnm_plan(n, 1e-6, W.dt_dx_double(W.cfg("cfg4"), qmax),
+                                   F.BURGERS_GODUNOV, F.PERIODIC)
+                steps, cells = 96, n
+        elif name in ("eo3d", "lin3d"):
+            # 3D directional composition (NEXT-f3, d = 3), 512^3 cells, 20 steps
+            n3 = int(os.environ.get("N3D", 512))
+            g = torch.Generator(device="cuda").manual_seed(0)
+            amp = 100000 if name == "eo3d" else 3000
+            q0 = torch.randint(-amp, amp, (n3, n3, n3), dtype=torch.int32, device="cuda", generator=g)
+            if name == "eo3d":
+                plan = F.fqnm_plan_3d(n3, n3, n3, 1e-5, 1 / 15, 1 / 15, 1 / 15, F.BURGERS_EO)
+            else:
+                plan = F.fqnm_plan_3d(n3, n3, n3, 1e-3, 0.25, 0.25, 0.25, F.LINEAR)
+            steps, cells = 20, n3 ** 3
         else:
             raise SystemExit(f"unknown config {name}")
         ms, q = timed(plan, q0, steps, reps=1 if name == "cfg5" else 3)
