@@ -30,6 +30,10 @@
 #endif
 #define FQNM_PART(x) (FQNM_SCALAR_PART == 0 || FQNM_SCALAR_PART == (x))
 
+#ifndef FQNM_STREAM_STEP
+#define FQNM_STREAM_STEP 0     // K2/K3/K6 interior cells updated in map order (variant)
+#endif
+
 #ifndef FQNM_RES_FENCE
 #define FQNM_RES_FENCE 0
 #endif
@@ -119,6 +123,28 @@ __device__ __forceinline__ void one_step(int32_t (&q)[V], const DevRule& r, int 
             q[j] = q[j] + Tl - t;
             Tl = t;
         }
+    } else if (FQNM_STREAM_STEP && NB == 0 && !WALL && V >= 4) {
+        // interior cells first, in cell order: the maps of cell j+1 are evaluated right
+        // before cell j is updated (FMA-pipe map work interleaved with the ALU-pipe
+        // updates); the two cells that need the neighbour lanes' maps come last, after
+        // the shuffles
+        int32_t g[V], m[V];
+        phi_gm<RULE, false, true>(q[0], g[0], m[0], r);
+        phi_gm<RULE, true, true>(q[1], g[1], m[1], r);
+        const int32_t q0 = q[0];
+        int32_t Tl = g[0] - m[0] + m[1];                                // F_{1/2}
+#pragma unroll
+        for (int j = 1; j + 1 < V; ++j) {
+            if (j & 1) phi_gm<RULE, false, true>(q[j + 1], g[j + 1], m[j + 1], r);
+            else phi_gm<RULE, true, true>(q[j + 1], g[j + 1], m[j + 1], r);
+            const int32_t Tr = g[j] - m[j] + m[j + 1];                  // F_{j+1/2}
+            q[j] = q[j] + Tl - Tr;
+            Tl = Tr;
+        }
+        const int32_t pl = __shfl_up_sync(FULL, g[V - 1] - m[V - 1], 1);
+        const int32_t mr = __shfl_down_sync(FULL, m[0], 1);
+        q[0] = q0 + (pl + m[0]) - (g[0] - m[0] + m[1]);
+        q[V - 1] = q[V - 1] + Tl - (g[V - 1] - m[V - 1] + mr);
     } else {
         int32_t g[V], m[V];
         eval_maps<RULE, V>(q, g, m, r);
