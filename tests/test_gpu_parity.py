@@ -202,6 +202,28 @@ def test_cfg5_full_size_windows(F):
         assert np.array_equal(qh[:, a:b], ref[:, a - lo:b - lo]), (a, b)
 
 
+@pytest.mark.parametrize("V", [1, 2, 4])
+@pytest.mark.parametrize("kind", [3, 4])                 # FQNM_EULER_ROE, FQNM_EULER_ROE_DENSITY
+def test_euler_window_widths(F, V, kind):
+    """K5 with 1, 2 and 4 cells per lane (window 32 V with one-cell overlaps), ragged N,
+    the Sod data shifted so the diaphragm falls inside a window."""
+    n = 3 * 1024 + 37
+    nsteps, lam = W.sod_steps_and_dt_dx(n)
+    nsteps = 120
+    if kind == 3:
+        q0 = np.roll(W.sod_q0(n), 101, axis=1)
+        run = lambda q, s: oracle.euler_run(q, s, 1e-7, lam)
+    else:
+        q0 = np.ascontiguousarray(np.roll(_sod_mixed(n), 101, axis=1))
+        run = lambda q, s: oracle.euler_density_run(q, s, 1e-7, lam)
+    plan = F.fqnm_plan(n, 1e-7, lam, kind, F.TRANSMISSIVE)
+    F.fqnm_debug_override(plan, 0, 0, V)
+    assert plan.info()["cells_per_thread"] == V
+    q = to_dev(q0, torch.int64)
+    F.fqnm_step(plan, q, nsteps)
+    assert np.array_equal(q.cpu().numpy(), run(q0, nsteps))
+
+
 def test_roe_transfer_device_random_states(F):
     rng = np.random.default_rng(61)
     n = 4096
