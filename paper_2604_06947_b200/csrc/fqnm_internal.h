@@ -120,7 +120,7 @@ struct Step3DArgs {
     int64_t nx, ny, nz;
     int64_t zchunk;     // z planes per CTA
     int32_t bmode;
-    int32_t pad;
+    int32_t xt0;        // first x tile of the launch (set by launch_step3d)
 };
 cudaError_t launch_step3d(int rule, bool same, const Step3DArgs& a, const DevRule& rx,
                           const DevRule& ry, const DevRule& rz, cudaStream_t st);

@@ -69,7 +69,10 @@ struct Maps3 {
     }
 };
 
-template <int RULE, bool SAME>
+// VEC: every tile of the launch is a full 128-cell row segment with nx % 4 == 0 (int4
+// loads/stores); otherwise scalar accesses with wrapped x offsets (the last partial
+// tile column, launched separately)
+template <int RULE, bool SAME, bool VEC>
 __global__ void __launch_bounds__(32 * K8_WARPS) k_step3d(Step3DArgs a, DevRule rx, DevRule ry,
                                                         DevRule rz)
 {
@@ -78,7 +81,7 @@ __global__ void __launch_bounds__(32 * K8_WARPS) k_step3d(Step3DArgs a, DevRule 
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int nx = (int)a.nx, ny = (int)a.ny, nz = (int)a.nz, bm = a.bmode;
     const int plane = nx * ny;
-    const int x0 = blockIdx.x * K8_TX, y0 = blockIdx.y * K8_TY;
+    const int x0 = (blockIdx.x + a.xt0) * K8_TX, y0 = blockIdx.y * K8_TY;
     const int z0 = blockIdx.z * (int)a.zchunk;
     const int z1 = z0 + (int)a.zchunk < nz ? z0 + (int)a.zchunk : nz;
     const bool halo_row = (w == 0 || w == K8_WARPS - 1);     // warp-uniform
@@ -91,7 +94,7 @@ __global__ void __launch_bounds__(32 * K8_WARPS) k_step3d(Step3DArgs a, DevRule 
     int xo[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) xo[j] = (xl + j < nx) ? xl + j : wrap_i(xl + j, nx, bm);
-    const bool vec = (x0 + K8_TX <= nx) && (nx % 4 == 0);   // int4 path (uniform per CTA)
+    constexpr bool vec = VEC;
     // the cell beyond the tile's x edge: lane 0 -> x0 - 1, lane 31 -> x0 + 128
     const bool edge_lane = (lane == 0 || lane == 31);
     const int xe = lane == 0 ? wrap_i(x0 - 1, nx, bm) : wrap_i(x0 + K8_TX, nx, bm);
@@ -223,14 +226,28 @@ __global__ void __launch_bounds__(32 * K8_WARPS) k_step3d(Step3DArgs a, DevRule 
 }
 
 template <int RULE>
-static cudaError_t step3d_rule(bool same, const Step3DArgs& a, const DevRule& rx, const DevRule& ry,
-                               const DevRule& rz, cudaStream_t st)
+static cudaError_t step3d_rule(bool same, const Step3DArgs& a0, const DevRule& rx,
+                               const DevRule& ry, const DevRule& rz, cudaStream_t st)
 {
+    Step3DArgs a = a0;
     dim3 block(32 * K8_WARPS);
-    dim3 grid((unsigned)((a.nx + K8_TX - 1) / K8_TX), (unsigned)((a.ny + K8_TY - 1) / K8_TY),
-              (unsigned)((a.nz + a.zchunk - 1) / a.zchunk));
-    if (same) k_step3d<RULE, true><<<grid, block, 0, st>>>(a, rx, ry, rz);
-    else k_step3d<RULE, false><<<grid, block, 0, st>>>(a, rx, ry, rz);
+    const unsigned gy = (unsigned)((a.ny + K8_TY - 1) / K8_TY);
+    const unsigned gz = (unsigned)((a.nz + a.zchunk - 1) / a.zchunk);
+    // full 128-wide tiles on the int4 path, the partial last tile column separately
+    const int64_t full = (a.nx % 4 == 0) ? a.nx / K8_TX : 0;
+    const int64_t total = (a.nx + K8_TX - 1) / K8_TX;
+    if (full > 0) {
+        a.xt0 = 0;
+        dim3 grid((unsigned)full, gy, gz);
+        if (same) k_step3d<RULE, true, true><<<grid, block, 0, st>>>(a, rx, ry, rz);
+        else k_step3d<RULE, false, true><<<grid, block, 0, st>>>(a, rx, ry, rz);
+    }
+    if (total > full) {
+        a.xt0 = full;
+        dim3 grid((unsigned)(total - full), gy, gz);
+        if (same) k_step3d<RULE, true, false><<<grid, block, 0, st>>>(a, rx, ry, rz);
+        else k_step3d<RULE, false, false><<<grid, block, 0, st>>>(a, rx, ry, rz);
+    }
     return cudaGetLastError();
 }
 

@@ -49,7 +49,8 @@ def _plan(F, case, shape, boundary):
 
 @pytest.mark.parametrize("case", range(len(RULES3D)))
 @pytest.mark.parametrize("boundary", [W.PERIODIC, W.TRANSMISSIVE])
-@pytest.mark.parametrize("shape", [(2, 3, 5), (7, 9, 33), (19, 17, 70), (40, 24, 64)])
+@pytest.mark.parametrize("shape", [(2, 3, 5), (7, 9, 33), (19, 17, 70), (40, 24, 64), (5, 11, 260),
+                                   (3, 9, 256), (4, 8, 130)])
 def test_3d_matches_oracle(F, case, boundary, shape):
     kind, d, lams, params, amp, off = RULES3D[case]
     rng = np.random.default_rng(sum(shape) * 11 + case)
