@@ -187,6 +187,16 @@ struct fqnm_plan {
     DevRule drz{};
     cudaStream_t st = nullptr;
     int64_t launches = 0;
+    // pipelined end-to-end stepping (fqnm_step_host): chunk plan + 3 ext buffers + streams
+    const int* guard = nullptr;          // K2 launches return at once when *guard != 0
+    fqnm_plan_t* pipe_child = nullptr;
+    int64_t pipe_H = 0, pipe_C = 0, pipe_m = 0;
+    void* pipe_buf[3] = {nullptr, nullptr, nullptr};
+    int* pipe_guard = nullptr;           // one flag per chunk
+    int* pipe_guard_host = nullptr;
+    int64_t pipe_guard_n = 0;
+    cudaStream_t pipe_h2d = nullptr, pipe_d2h = nullptr;
+    cudaEvent_t pipe_ev[9] = {};         // [0..2] h2d done, [3..5] compute done, [6..8] d2h done
     // profiling (fqnm_profile_enable)
     bool prof = false;
     std::vector<cudaEvent_t> ev;      // pairs (start, stop)
@@ -784,6 +794,26 @@ extern "C" int fqnm_plan_3d(fqnm_plan_t** out, int64_t nx, int64_t ny, int64_t n
     return FQNM_OK;
 }
 
+static void pipe_release(fqnm_plan_t* p)
+{
+    if (p->pipe_child) fqnm_destroy(p->pipe_child);
+    p->pipe_child = nullptr;
+    for (int i = 0; i < 3; ++i) {
+        if (p->pipe_buf[i]) cudaFree(p->pipe_buf[i]);
+        p->pipe_buf[i] = nullptr;
+    }
+    if (p->pipe_guard) cudaFree(p->pipe_guard);
+    if (p->pipe_guard_host) cudaFreeHost(p->pipe_guard_host);
+    p->pipe_guard = nullptr;
+    p->pipe_guard_host = nullptr;
+    for (cudaEvent_t& e : p->pipe_ev)
+        if (e) { cudaEventDestroy(e); e = nullptr; }
+    if (p->pipe_h2d) cudaStreamDestroy(p->pipe_h2d);
+    if (p->pipe_d2h) cudaStreamDestroy(p->pipe_d2h);
+    p->pipe_h2d = p->pipe_d2h = nullptr;
+    p->pipe_H = p->pipe_C = p->pipe_m = 0;
+}
+
 extern "C" void fqnm_destroy(fqnm_plan_t* p)
 {
     if (!p) return;
@@ -798,6 +828,7 @@ extern "C" void fqnm_destroy(fqnm_plan_t* p)
         if (p->hbuf[i]) cudaFree(p->hbuf[i]);
     if (p->hflags) cudaFree(p->hflags);
     for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
+    pipe_release(p);
     delete p;
 }
 
@@ -880,6 +911,7 @@ static int launch_block(fqnm_plan_t* p, const int32_t* src, int32_t* dst, int ks
     a.KL = p->dep_left ? round4(ksteps) : 0;
     a.KR = p->dep_right ? round4(ksteps) : 0;
     a.bmode = bmode_of(d);
+    a.guard = p->guard;
     const int64_t S = 32 * p->V - a.KL - a.KR;
     if (S < 4) return fail(FQNM_ERR_ARG, "k = %d too large for V = %d", ksteps, p->V);
     a.nwin = (d.n_local + S - 1) / S;
@@ -1176,9 +1208,131 @@ extern "C" int fqnm_observe(const fqnm_plan_t* p, const void* q, double* u)
     return FQNM_OK;
 }
 
+// Pipelined end-to-end path for one large periodic scalar problem: the domain is cut
+// into m chunks of C cells; chunk c is stepped independently on its extended region
+// [cC - H, cC + C + H) (periodic wrap) as a transmissive problem, H >= nsteps, so its
+// C inner cells are exact (their dependence cone, one cell per step and side, stays
+// inside the region); the extra work is 2H/C.  Three device buffers rotate so that
+// the H2D copy of chunk c+1 and the D2H copy of chunk c-1 overlap the stepping of
+// chunk c (three streams, events).  The input range check of each extended region
+// runs on the device and, if it fails, turns that chunk's launches into no-ops.
+static int pipe_setup(fqnm_plan_t* p, int64_t nsteps)
+{
+    const int64_t n = p->d.n_local;
+    const int64_t H = (nsteps + 31) / 32 * 32;
+    int64_t m = 0, C = 0;
+    for (int64_t mm = 4; mm <= 256; mm *= 2) {
+        if (n % mm) break;
+        const int64_t c = n / mm;
+        if (c % 32) break;
+        if (c <= ((int64_t)1 << 27) && H * 16 <= c) { m = mm; C = c; break; }
+    }
+    if (!m) return FQNM_ERR_UNSUPPORTED;
+    if (p->pipe_child && p->pipe_H == H && p->pipe_C == C) return FQNM_OK;
+    pipe_release(p);
+    fqnm_plan_desc d = p->d;
+    d.n_local = d.n_global = C + 2 * H;
+    d.offset = 0;
+    d.boundary = FQNM_TRANSMISSIVE;
+    d.kappa_num = p->kap_num;
+    d.kappa_den = p->kap_den;
+    d.q_lo = p->lo;
+    d.q_hi = p->hi;
+    d.check_range = 0;
+    d.k = p->k;
+    d.stream = (void*)p->st;
+    fqnm_plan_t* c = nullptr;
+    int rc = plan_build(&c, &d, true);
+    if (rc != FQNM_OK) return rc;
+    if (c->family != 2 || c->rule != p->rule) { fqnm_destroy(c); return FQNM_ERR_UNSUPPORTED; }
+    c->st = p->st;
+    p->pipe_child = c;
+    p->pipe_H = H;
+    p->pipe_C = C;
+    p->pipe_m = m;
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < 3 && e == cudaSuccess; ++i) e = cudaMalloc(&p->pipe_buf[i], (size_t)(C + 2 * H) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&p->pipe_guard, (size_t)m * sizeof(int));
+    if (e == cudaSuccess) e = cudaMallocHost(&p->pipe_guard_host, (size_t)m * sizeof(int));
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->pipe_h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->pipe_d2h, cudaStreamNonBlocking);
+    for (int i = 0; i < 9 && e == cudaSuccess; ++i)
+        e = cudaEventCreateWithFlags(&p->pipe_ev[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        pipe_release(p);
+        return fail(FQNM_ERR_NOMEM, "e2e pipeline buffers: %s", cudaGetErrorString(e));
+    }
+    p->pipe_guard_n = m;
+    return FQNM_OK;
+}
+
+static int step_host_pipelined(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
+{
+    const int64_t n = p->d.n_local, C = p->pipe_C, H = p->pipe_H, m = p->pipe_m, E = C + 2 * H;
+    fqnm_plan_t* ch = p->pipe_child;
+    ch->st = p->st;                                                // the caller's current stream
+    cudaEvent_t* ev_in = p->pipe_ev;
+    cudaEvent_t* ev_comp = p->pipe_ev + 3;
+    cudaEvent_t* ev_out = p->pipe_ev + 6;
+    const bool check = p->d.check_range != 0;
+    CUDA_TRY(cudaMemsetAsync(p->pipe_guard, 0, (size_t)m * sizeof(int), p->st));
+    CUDA_TRY(cudaEventRecord(ev_comp[0], p->st));                 // guard reset before any use
+    CUDA_TRY(cudaStreamWaitEvent(p->pipe_h2d, ev_comp[0], 0));
+    for (int64_t c = 0; c < m; ++c) {
+        const int b = (int)(c % 3);
+        int32_t* buf = (int32_t*)p->pipe_buf[b];
+        // H2D of the extended region (wraps around the periodic domain)
+        if (c >= 3) CUDA_TRY(cudaStreamWaitEvent(p->pipe_h2d, ev_out[b], 0));
+        int64_t s0 = c * C - H;
+        if (s0 < 0) s0 += n;
+        const int64_t first = (s0 + E <= n) ? E : n - s0;
+        CUDA_TRY(cudaMemcpyAsync(buf, qh + s0, (size_t)first * 4, cudaMemcpyHostToDevice, p->pipe_h2d));
+        if (first < E)
+            CUDA_TRY(cudaMemcpyAsync(buf + first, qh, (size_t)(E - first) * 4, cudaMemcpyHostToDevice,
+                                     p->pipe_h2d));
+        CUDA_TRY(cudaEventRecord(ev_in[b], p->pipe_h2d));
+        // range check + stepping on the compute stream
+        CUDA_TRY(cudaStreamWaitEvent(p->st, ev_in[b], 0));
+        if (check) {
+            CUDA_TRY(launch_range_guard(buf, E, p->lo, p->hi, p->pipe_guard + c, p->st));
+            p->launches++;
+            ch->guard = p->pipe_guard + c;
+        } else {
+            ch->guard = nullptr;
+        }
+        const int64_t l0 = ch->launches;
+        int rc = fqnm_step(ch, buf, nsteps);
+        p->launches += ch->launches - l0;
+        ch->guard = nullptr;
+        if (rc != FQNM_OK) return rc;
+        CUDA_TRY(cudaEventRecord(ev_comp[b], p->st));
+        // D2H of the inner C cells
+        CUDA_TRY(cudaStreamWaitEvent(p->pipe_d2h, ev_comp[b], 0));
+        CUDA_TRY(cudaMemcpyAsync(qh + c * C, buf + H, (size_t)C * 4, cudaMemcpyDeviceToHost, p->pipe_d2h));
+        CUDA_TRY(cudaEventRecord(ev_out[b], p->pipe_d2h));
+    }
+    if (check)
+        CUDA_TRY(cudaMemcpyAsync(p->pipe_guard_host, p->pipe_guard, (size_t)m * sizeof(int),
+                                 cudaMemcpyDeviceToHost, p->st));
+    CUDA_TRY(cudaStreamSynchronize(p->st));
+    CUDA_TRY(cudaStreamSynchronize(p->pipe_d2h));
+    if (check)
+        for (int64_t c = 0; c < m; ++c)
+            if (p->pipe_guard_host[c])
+                return fail(FQNM_ERR_RANGE, "state outside the plan's admissible range [%lld, %lld] "
+                            "in chunk %lld (q_host is partially stepped)", (long long)p->lo,
+                            (long long)p->hi, (long long)c);
+    return FQNM_OK;
+}
+
 extern "C" int fqnm_step_host(fqnm_plan_t* p, void* q_host, int64_t nsteps)
 {
     if (!p || !q_host) return fail(FQNM_ERR_ARG, "null argument");
+    if (nsteps < 0) return fail(FQNM_ERR_ARG, "nsteps must be >= 0");
+    const fqnm_plan_desc& d = p->d;
+    if (nsteps > 0 && d.nvar == 1 && d.batch == 1 && d.boundary == FQNM_PERIODIC && p->family == 2 &&
+        d.n_local >= ((int64_t)1 << 24) && pipe_setup(p, nsteps) == FQNM_OK)
+        return step_host_pipelined(p, (int32_t*)q_host, nsteps);
     const size_t bytes = state_elems(p->d) * elem_size(p->d);
     if (!p->e2e_dev) {
         cudaError_t e = cudaMalloc(&p->e2e_dev, bytes);

@@ -73,6 +73,7 @@ struct BlockedArgs {
     unsigned int* self_flags;      // [0]: left-halo tag, [1]: right-halo tag (written by peers)
     unsigned int* peer_left_flags;
     unsigned int* peer_right_flags;
+    const int* guard;              // optional: nonzero -> the launch does nothing (failed range check)
 };
 
 struct EulerArgs {
@@ -167,6 +168,9 @@ cudaError_t launch_equiv_count(const unsigned long long* keys, const unsigned in
 cudaError_t launch_transfer(int rule, const int32_t* q, int32_t* pp, int32_t* pm, int64_t n,
                             const DevRule& r, cudaStream_t st);
 cudaError_t launch_minmax(const void* q, int dtype, int64_t n, long long* out2, cudaStream_t st);
+// flag |= any q[i] outside [lo, hi]  (int32 state; asynchronous range check of the e2e pipeline)
+cudaError_t launch_range_guard(const int32_t* q, int64_t n, long long lo, long long hi, int* flag,
+                               cudaStream_t st);
 cudaError_t launch_observe(const void* q, int dtype, double delta, double* u, int64_t n,
                            cudaStream_t st);
 cudaError_t launch_euler(int V, const EulerArgs& a, cudaStream_t st);

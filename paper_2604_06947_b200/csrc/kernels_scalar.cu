@@ -363,6 +363,7 @@ template <int RULE, int V, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_blocked(BlockedArgs a, DevRule r)
 {
     static_assert(V % 4 == 0, "V must be a multiple of 4 (int4 vectors)");
+    if (a.guard && *a.guard) return;                            // input failed its range check
     constexpr int W = 32 * V;
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1201,6 +1202,25 @@ cudaError_t launch_transfer(int rule, const int32_t* q, int32_t* pp, int32_t* pm
         case R_LIN_FAST: k_transfer<R_LIN_FAST><<<g, 256, 0, st>>>(q, pp, pm, n, r); break;
         default: return cudaErrorInvalidValue;
     }
+    return cudaGetLastError();
+}
+
+__global__ void k_range_guard(const int32_t* __restrict__ q, int64_t n, long long lo, long long hi,
+                              int* flag)
+{
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const long long v = q[i];
+        bad |= (v < lo) | (v > hi);
+    }
+    if (__any_sync(FULL, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+cudaError_t launch_range_guard(const int32_t* q, int64_t n, long long lo, long long hi, int* flag,
+                               cudaStream_t st)
+{
+    k_range_guard<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(q, n, lo, hi, flag);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,74 @@
+"""The end-to-end entry point fqnm_step_host (host buffer in, steps, host buffer out).
+For one large periodic problem it runs the chunked pipeline (each chunk stepped on its
+extended region [cC - H, cC + C + H) with H >= nsteps, copies overlapped with the
+stepping on three streams): the result must equal the device-resident fqnm_step bit for
+bit, the range check must still refuse out-of-range input, and small or non-periodic
+plans take the plain path."""
+import numpy as np
+import pytest
+
+import workloads as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def F():
+    import paper_2604_06947_b200 as F
+    return F
+
+
+def _eo_plan(F, n, check=True):
+    w = W.cfg("cfg4")
+    q = W.q0_cfg4(n=1 << 31, count=n, device="cuda")
+    qmax = int(q.abs().max())
+    if check:
+        plan = F.fqnm_plan(n, 1e-6, W.dt_dx_double(w, qmax), F.BURGERS_EO, F.PERIODIC)
+    else:
+        plan = F.fqnm_plan_ex(n, 1e-6, W.dt_dx_double(w, qmax), F.BURGERS_EO)
+    return plan, q
+
+
+@pytest.mark.parametrize("n,nsteps", [(1 << 24, 100), (1 << 24, 1), ((1 << 25) + (1 << 24), 257)])
+@pytest.mark.parametrize("check", [True, False])
+def test_pipelined_step_host_equals_device_path(F, n, nsteps, check):
+    plan, q = _eo_plan(F, n, check)
+    ref = q.clone()
+    F.fqnm_step(plan, ref, nsteps)
+    qh = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    qh.copy_(q.cpu())
+    launches0 = plan.launches()
+    F.fqnm_step_host(plan, qh, nsteps)
+    assert plan.launches() > launches0
+    assert torch.equal(qh, ref.cpu())
+    # a second call reuses the pipeline (same nsteps) and continues the trajectory
+    F.fqnm_step(plan, ref, nsteps)
+    F.fqnm_step_host(plan, qh, nsteps)
+    assert torch.equal(qh, ref.cpu())
+
+
+def test_pipelined_step_host_range_check(F):
+    n = 1 << 24
+    plan, q = _eo_plan(F, n, True)
+    hi = plan.info()["q_hi"]
+    qh = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    qh.copy_(q.cpu())
+    qh[n // 2 + 12345] = hi + 1
+    with pytest.raises(F.FqnmError) as e:
+        F.fqnm_step_host(plan, qh, 50)
+    assert e.value.status == 3                              # FQNM_ERR_RANGE
+
+
+def test_plain_step_host_paths(F):
+    # small periodic, transmissive and batched plans take the plain (single copy) path
+    rng = np.random.default_rng(4)
+    for kw in (dict(n=70001, boundary=W.PERIODIC), dict(n=(1 << 24) + 4, boundary=W.TRANSMISSIVE)):
+        n = kw["n"]
+        q0 = W.smooth_random(rng, n, 100000, 20000).astype(np.int32)
+        plan = F.fqnm_plan(n, 1e-5, 4 / 15, F.BURGERS_EO, kw["boundary"])
+        ref = torch.tensor(q0, device="cuda")
+        F.fqnm_step(plan, ref, 33)
+        qh = torch.tensor(q0).pin_memory()
+        F.fqnm_step_host(plan, qh, 33)
+        assert torch.equal(qh, ref.cpu())
