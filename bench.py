@@ -163,7 +163,7 @@ def run_reference(args):
     w = W.cfg("cfg4")
     n_sample = 1 << 20
     q = W.q0_cfg4(n=w.n, count=n_sample).numpy().astype(np.int64)
-    qmax = 345000                      # sample only; kappa as for a typical cfg4 Q_max
+    qmax = 344848                      # max |q0| of cfg4 (the GPU arm's kappa = 1/(5 Q_max) = 1/1724240)
     rule = oracle.Rule(oracle.BURGERS_EO, w.delta, W.dt_dx(w, qmax))
     steps_per = 1000                   # the time steps of one cfg4 bench step
     for _ in range(args.warmup):
