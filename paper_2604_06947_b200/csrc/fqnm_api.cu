@@ -182,6 +182,7 @@ struct fqnm_plan {
     HostMap hpy, hmy;
     DevRule dry{};
     bool same_xy = false;
+    bool stream2d = true;               // 2D: K9 streaming (1 step/launch) instead of K7
     // 3D plans (family 8): z-direction rule
     int64_t nz = 0;
     DevRule drz{};
@@ -971,6 +972,21 @@ extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
     // ping-pong families
     void* bufs[2] = {q, p->scratch};
     int cur = 0;
+    if (p->family == 7 && p->stream2d) {
+        Step2DArgs a;
+        a.nx = p->nx;
+        a.ny = p->ny;
+        a.ksteps = (int32_t)step2d_stream_rows(p->nx, p->ny);
+        a.bmode = bm;
+        for (int64_t s = 0; s < nsteps; ++s) {
+            a.src = (const int32_t*)bufs[cur];
+            a.dst = (int32_t*)bufs[cur ^ 1];
+            PROF_LAUNCH(launch_step2d_stream(p->rule, p->same_xy, a, p->dr, p->dry, p->st));
+            cur ^= 1;
+        }
+        if (cur != 0) CUDA_TRY(cudaMemcpyAsync(q, bufs[cur], bytes, cudaMemcpyDeviceToDevice, p->st));
+        return FQNM_OK;
+    }
     if (p->family == 7) {
         int64_t nb = (nsteps + p->k - 1) / p->k;
         if (nb % 2 == 1 && nsteps >= nb + 1) nb += 1;
@@ -1674,6 +1690,17 @@ extern "C" int fqnm_debug_override(fqnm_plan_t* p, int32_t kernel, int32_t k, in
     }
     if (p->family == 8 && (kernel || k || V))
         return fail(FQNM_ERR_UNSUPPORTED, "3D plans have one kernel (K8, one step per launch)");
+    if (p->family == 7) {                 // 2D: kernel 7 = K7 smem-tiled (k <= 4), 9 = K9 streaming
+        if (kernel == 9) p->stream2d = true;
+        else if (kernel == 7) p->stream2d = false;
+        else if (kernel) return fail(FQNM_ERR_UNSUPPORTED, "2D plans: kernel 7 or 9");
+        if (k) {
+            if (k > STEP2D_KMAX) return fail(FQNM_ERR_ARG, "2D plans: k <= %d", STEP2D_KMAX);
+            p->k = k;
+            p->stream2d = false;
+        }
+        return FQNM_OK;
+    }
     if (kernel >= 100) {               // K2 with a register-cap variant: 2 + 100 * minb
         p->minb = kernel / 100;
         kernel = kernel % 100;
@@ -1720,11 +1747,6 @@ extern "C" int fqnm_debug_override(fqnm_plan_t* p, int32_t kernel, int32_t k, in
         if (p->family != 2 || !blocked_rule_has_V(p->rule, V))
             return fail(FQNM_ERR_UNSUPPORTED, "V override needs K2 and V in {8,16,32} ({8,16} for two-point rules)");
         p->V = V;
-    }
-    if (k && p->family == 7) {
-        if (k > STEP2D_KMAX) return fail(FQNM_ERR_ARG, "2D plans: k <= %d", STEP2D_KMAX);
-        p->k = k;
-        return FQNM_OK;
     }
     if (k && p->family == 6) {
         int P, base, rem, H;

@@ -113,6 +113,11 @@ struct Step2DArgs {
 };
 cudaError_t launch_step2d(int rule, bool same, const Step2DArgs& a, const DevRule& rx,
                           const DevRule& ry, cudaStream_t st);
+// K9: 2D streaming, one step per launch, warp per (x strip, y chunk) (kernels_2d.cu);
+// a.ksteps carries the rows per chunk
+cudaError_t launch_step2d_stream(int rule, bool same, const Step2DArgs& a, const DevRule& rx,
+                                 const DevRule& ry, cudaStream_t st);
+int64_t step2d_stream_rows(int64_t nx, int64_t ny);
 
 // K8: 3D directional composition, one step per launch, 2.5D z-streaming (kernels_3d.cu)
 struct Step3DArgs {

@@ -491,22 +491,23 @@ def _field2d(rng, ny, nx, amp, off):
 
 @pytest.mark.parametrize("case", range(len(RULES2D)))
 @pytest.mark.parametrize("boundary", [W.PERIODIC, W.TRANSMISSIVE])
-@pytest.mark.parametrize("shape", [(33, 129), (70, 300), (257, 1000)])
+@pytest.mark.parametrize("shape", [(33, 129), (70, 300), (257, 1000), (5, 7), (19, 248)])
 def test_2d_matches_oracle(F, case, boundary, shape):
     kind, d, lx, ly, ax, ay, amp, off = RULES2D[case]
     ny, nx = shape
     rng = np.random.default_rng(ny * 7 + nx + case)
     q0 = _field2d(rng, ny, nx, amp, off)
     r = oracle.Rule2D(kind, d, lx, ly, ax, ay)
-    for nsteps, k in ((1, 0), (5, 0), (13, 0), (13, 1), (9, 3)):
+    # K9 streaming (default, one step per launch) and K7 smem-tiled with k = 1, 3, 4
+    for nsteps, kern, k in ((1, 0, 0), (5, 9, 0), (13, 0, 0), (13, 7, 1), (9, 7, 3), (11, 7, 4)):
         plan = F.fqnm_plan_2d(nx, ny, float(Fraction(d)), float(lx), float(ly), kind, boundary,
                               float(ax), float(ay))
         assert plan.info()["kernel"] == 7
-        if k:
-            F.fqnm_debug_override(plan, 0, k, 0)
+        if kern or k:
+            F.fqnm_debug_override(plan, kern, k, 0)
         q = to_dev(q0)
         F.fqnm_step(plan, q, nsteps)
-        assert np.array_equal(host(q), r.run(q0, nsteps, boundary)), (nsteps, k)
+        assert np.array_equal(host(q), r.run(q0, nsteps, boundary)), (nsteps, kern, k)
 
 
 @pytest.mark.parametrize("lam,a", [(Fraction(7, 9), 1), (Fraction(1, 3), -1), (Fraction(1, 4), 1),

@@ -1,5 +1,5 @@
 """Small driver for ncu captures: one fqnm_step of a bench workload slice.
-usage: python tools/prof_step.py eo|lin|euler|3d [n] [steps]"""
+usage: python tools/prof_step.py eo|lin|euler|2d|3d [n] [steps]"""
 import os
 import sys
 
@@ -22,6 +22,11 @@ elif which == "lin":
     steps = int(sys.argv[3]) if len(sys.argv) > 3 else 128
     q = torch.tensor(W.q0_cfg3(n), dtype=torch.int32, device="cuda")
     plan = F.fqnm_plan(n, 1e-6, 0.5, F.LINEAR, F.PERIODIC)
+elif which == "2d":
+    n = int(sys.argv[2]) if len(sys.argv) > 2 else 8192
+    steps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    q = torch.randint(-100000, 100000, (n, n), dtype=torch.int32, device="cuda")
+    plan = F.fqnm_plan_2d(n, n, 1e-5, 1 / 15, 1 / 15, F.BURGERS_EO, F.PERIODIC)
 elif which == "3d":
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 512
     steps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
