@@ -7,8 +7,9 @@
 // which the outer 2 on each side are halo (strip stride 124 cells), and marches down
 // its chunk of rows.  x neighbours' maps come from the lane's own registers and warp
 // shuffles, y neighbours' maps from the rows above and below kept in registers; every
-// loaded cell's maps are evaluated once.  Rows are loaded two ahead with the loop
-// unrolled by three so the row rotation needs no register moves.
+// loaded cell's maps are evaluated once.  Rows stream through a per-warp shared-memory
+// ring, 6 rows in flight per lane (cp.async), and the loop is unrolled so the row
+// rotation needs no register moves.
 // HBM traffic: one read and one write of the state per step (8 B per cell-update),
 // 3.1 % redundant halo columns.  Indices are 32-bit (nx * ny < 2^31).
 #include <cstdint>
@@ -24,6 +25,7 @@ static constexpr int K9_V = 4;                  // x cells per lane
 static constexpr int K9_W = 32 * K9_V;          // loaded strip width
 static constexpr int K9_H = 2;                  // halo columns per side
 static constexpr int K9_S = K9_W - 2 * K9_H;    // strip stride (stored columns)
+static constexpr int K9_LOOK = 6;               // rows in flight per lane (cp.async ring)
 
 __device__ __forceinline__ int wrap2(int i, int n, int bmode)
 {
@@ -84,30 +86,54 @@ __global__ void __launch_bounds__(256) k_step2d_s(Step2DArgs a, DevRule rx, DevR
         st[j] = p >= K9_H && p < K9_W - K9_H && x >= 0 && x < nx;
     }
 
-    auto load_row = [&](int r, int32_t (&v)[V]) {
-        const int32_t* row = a.src + wrap_row(r, ny, bm) * nx;
-        if (vec) {
-            const int2 t0 = __ldg(reinterpret_cast<const int2*>(row + xl));
-            const int2 t1 = __ldg(reinterpret_cast<const int2*>(row + xl + 2));
-            v[0] = t0.x; v[1] = t0.y; v[2] = t1.x; v[3] = t1.y;
-        } else {
+    // Row ring in shared memory: each lane streams its 4 cells K9_LOOK rows ahead with
+    // cp.async (two 8-byte copies: strips start at x = 2 mod 4), one commit group per
+    // row; a lane reads only the slots it filled, so no barrier is needed.
+    // Stage of row r: (r - y0 + 1) % S.
+    constexpr int L = K9_LOOK, S = K9_LOOK + 1;
+    __shared__ int4 ring[S][256 / 32][32];
+    const int wib = threadIdx.x >> 5;
+    const unsigned ring0 = (unsigned)__cvta_generic_to_shared(&ring[0][wib][lane]);
+    constexpr unsigned RSTRIDE = sizeof(ring[0]);
+    auto issue = [&](int r, int stg) {
+        if (r <= y1) {                                     // rows beyond y1 are never read
+            const int32_t* row = a.src + wrap_row(r, ny, bm) * nx;
+            const unsigned d = ring0 + stg * RSTRIDE;
+            if (vec) {
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(d), "l"(row + xl) : "memory");
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(d + 8), "l"(row + xl + 2) : "memory");
+            } else {
 #pragma unroll
-            for (int j = 0; j < V; ++j) v[j] = __ldg(row + xo[j]);
+                for (int j = 0; j < V; ++j)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(d + 4 * j), "l"(row + xo[j]) : "memory");
+            }
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto read = [&](int stg, int32_t (&v)[V]) {
+        int4 t;
+        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(t.x), "=r"(t.y), "=r"(t.z), "=r"(t.w) : "r"(ring0 + stg * RSTRIDE) : "memory");
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
     };
 
     Maps2<RULE, SAME> M0, M1, M2;
     int32_t Q0[V], Q1[V], Q2[V];
-    load_row(y0 - 1, Q2);
+    for (int r = y0 - 1; r < y0 + L; ++r) issue(r, r - y0 + 1);   // rows y0 - 1 .. y0 + L - 1
+    asm volatile("cp.async.wait_group %0;" :: "n"(L - 1) : "memory");   // rows y0 - 1, y0 landed
+    read(0, Q2);
     M2.eval(Q2, rx, ry);                                   // row y0 - 1 (its phi+_y)
-    load_row(y0, Q0);
+    read(1, Q0);
     M0.eval(Q0, rx, ry);
-    load_row(y0 + 1, Q1);
-    // one row: Qc/Mc = row r, Qn/Mn = row r + 1 (maps evaluated here), Ql = load target
-    // (row r + 2), Mp = row r - 1
-    auto body = [&](int r, int32_t (&Qc)[V], int32_t (&Qn)[V], int32_t (&Ql)[V],
-                    Maps2<RULE, SAME>& Mp, Maps2<RULE, SAME>& Mc, Maps2<RULE, SAME>& Mn) {
-        load_row(r + 2, Ql);
+    int sz = 1;                                            // stage of row r
+    // one row: Qc/Mc = row r, Qn/Mn = row r + 1 (read from the ring, maps evaluated
+    // here), Mp = row r - 1
+    auto body = [&](int r, int32_t (&Qc)[V], int32_t (&Qn)[V], Maps2<RULE, SAME>& Mp,
+                    Maps2<RULE, SAME>& Mc, Maps2<RULE, SAME>& Mn) {
+        const int sn = sz + 1 == S ? 0 : sz + 1, sl = sz == 0 ? S - 1 : sz - 1;
+        asm volatile("cp.async.wait_group %0;" :: "n"(L - 2) : "memory");  // rows <= r + 1
+        read(sn, Qn);
+        issue(r + L, sl);                                  // into row r - 1's stage
         Mn.eval(Qn, rx, ry);
         const int32_t pl = __shfl_up_sync(FULL2, Mc.px[V - 1], 1);   // lane 0: halo cell, unused
         const int32_t mr = __shfl_down_sync(FULL2, Mc.mx[0], 1);     // lane 31: halo, unused
@@ -123,32 +149,32 @@ __global__ void __launch_bounds__(256) k_step2d_s(Step2DArgs a, DevRule rx, DevR
             out[j] = Qc[j] + txl - txr + tyl - tyr;
         }
         // (transmissive rows: wrap_row clamps, so the ghost rows repeat the edge row)
-        {
-            int32_t* row = a.dst + r * nx;
-            if (vec) {
-                if (lane > 0 && lane < 31) {
-                    *reinterpret_cast<int2*>(row + xl) = make_int2(out[0], out[1]);
-                    *reinterpret_cast<int2*>(row + xl + 2) = make_int2(out[2], out[3]);
-                } else if (lane == 0) {
-                    *reinterpret_cast<int2*>(row + xl + 2) = make_int2(out[2], out[3]);
-                } else {
-                    *reinterpret_cast<int2*>(row + xl) = make_int2(out[0], out[1]);
-                }
+        int32_t* row = a.dst + r * nx;
+        if (vec) {
+            if (lane > 0 && lane < 31) {
+                *reinterpret_cast<int2*>(row + xl) = make_int2(out[0], out[1]);
+                *reinterpret_cast<int2*>(row + xl + 2) = make_int2(out[2], out[3]);
+            } else if (lane == 0) {
+                *reinterpret_cast<int2*>(row + xl + 2) = make_int2(out[2], out[3]);
             } else {
-#pragma unroll
-                for (int j = 0; j < V; ++j)
-                    if (st[j]) row[xl + j] = out[j];
+                *reinterpret_cast<int2*>(row + xl) = make_int2(out[0], out[1]);
             }
+        } else {
+#pragma unroll
+            for (int j = 0; j < V; ++j)
+                if (st[j]) row[xl + j] = out[j];
         }
+        sz = sn;
     };
     int r = y0;
     for (; r + 3 <= y1; r += 3) {
-        body(r, Q0, Q1, Q2, M2, M0, M1);
-        body(r + 1, Q1, Q2, Q0, M0, M1, M2);
-        body(r + 2, Q2, Q0, Q1, M1, M2, M0);
+        body(r, Q0, Q1, M2, M0, M1);
+        body(r + 1, Q1, Q2, M0, M1, M2);
+        body(r + 2, Q2, Q0, M1, M2, M0);
     }
-    if (r < y1) body(r, Q0, Q1, Q2, M2, M0, M1);
-    if (r + 1 < y1) body(r + 1, Q1, Q2, Q0, M0, M1, M2);
+    if (r < y1) body(r, Q0, Q1, M2, M0, M1);
+    if (r + 1 < y1) body(r + 1, Q1, Q2, M0, M1, M2);
+    asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 int64_t step2d_stream_rows(int64_t nx, int64_t ny)
