@@ -151,6 +151,25 @@ def cpu_oracle_rate(q_sample: np.ndarray, qmax: int, target_s: float = 12.0):
     return n * steps / dt / 1e9, steps, dt, oracle.max_threads()
 
 
+def state_invariants(q, chunk=1 << 28):
+    """Sum (int64), min, max and periodic total variation of a 1-D int32 CUDA state,
+    by plain torch reductions in chunks (independent of the FQNM kernels)."""
+    import torch
+    n = q.numel()
+    tot, mn, mx, tv = 0, None, None, 0
+    for i in range(0, n, chunk):
+        c = q[i:i + chunk]
+        tot += int(c.sum(dtype=torch.int64))
+        cmin, cmax = int(c.min()), int(c.max())
+        mn = cmin if mn is None else min(mn, cmin)
+        mx = cmax if mx is None else max(mx, cmax)
+        j = min(i + chunk + 1, n)
+        seg = q[i:j].to(torch.int64)
+        tv += int((seg[1:] - seg[:-1]).abs().sum())
+    tv += abs(int(q[0]) - int(q[n - 1]))
+    return {"sum": tot, "min": mn, "max": mx, "tv": tv}
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle timed on host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -273,6 +292,9 @@ def main():
                 sd.step(T)
         stepper_plans = [plan]
 
+    # invariants of the initial state (independent torch reductions)
+    inv0 = state_invariants(q) if world == 1 else None
+
     # ---- warm-up ----
     for _ in range(max(args.warmup, 0)):
         do_step()
@@ -343,6 +365,8 @@ def main():
         roofline["traffic_source"] = tr_src
         roofline["traffic_over_algorithmic"] = tr / hbm_bytes_per_launch
 
+    inv1 = state_invariants(q) if world == 1 else None
+
     # ---- end-to-end through the public API with host buffers (H2D + steps + D2H) ----
     e2e = None
     if not args.no_e2e:
@@ -393,6 +417,16 @@ def main():
                     parity["ok"] &= bool(np.array_equal(ref, got))
         except Exception as ex:       # never let the spot check kill the bench line
             parity = {"ok": None, "error": str(ex)[:200]}
+        if inv0 is not None and inv1 is not None:
+            # exact conservation, maximum principle and TVD of the whole 2^31-cell state
+            # after warm-up + timed steps (Lemma P:197-238, Thm conservation)
+            parity["invariants"] = {
+                "sum_conserved": inv1["sum"] == inv0["sum"],
+                "max_principle": inv1["min"] >= inv0["min"] and inv1["max"] <= inv0["max"],
+                "tv_nonincreasing": inv1["tv"] <= inv0["tv"],
+                "initial": inv0, "final": inv1}
+            parity["ok"] = bool(parity["ok"]) and all(
+                parity["invariants"][k] for k in ("sum_conserved", "max_principle", "tv_nonincreasing"))
 
     # ---- CPU baseline (oracle on host cores; rank 0, N = 1 only) ----
     cpu = None
