@@ -27,6 +27,7 @@ UNITS = {
     "kernels_euler.cu": ["-fmad=false"],
     "kernels_diag.cu": [],
     "kernels_3d.cu": [],
+    "kernels_3d_s.cu": [],
     "kernels_2d.cu": [],
 }
 HEADERS = ["fqnm_internal.h", "maps.cuh", "kernels_scalar.cu"]

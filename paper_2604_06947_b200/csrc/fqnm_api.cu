@@ -183,6 +183,7 @@ struct fqnm_plan {
     DevRule dry{};
     bool same_xy = false;
     bool stream2d = true;               // 2D: K9 streaming (1 step/launch) instead of K7
+    bool stream3d = false;              // 3D: K10 warp streaming instead of K8 (measured slower)
     // 3D plans (family 8): z-direction rule
     int64_t nz = 0;
     DevRule drz{};
@@ -1011,12 +1012,15 @@ extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
         a.nx = p->nx;
         a.ny = p->ny;
         a.nz = p->nz;
-        a.zchunk = step3d_zchunk(p->nx, p->ny, p->nz);
+        a.zchunk = p->stream3d ? step3d_s_zchunk(p->nx, p->ny, p->nz) : step3d_zchunk(p->nx, p->ny, p->nz);
         a.bmode = bm;
         for (int64_t s = 0; s < nsteps; ++s) {
             a.src = (const int32_t*)bufs[cur];
             a.dst = (int32_t*)bufs[cur ^ 1];
-            PROF_LAUNCH(launch_step3d(p->rule, p->same_xy, a, p->dr, p->dry, p->drz, p->st));
+            if (p->stream3d)
+                PROF_LAUNCH(launch_step3d_stream(p->rule, p->same_xy, a, p->dr, p->dry, p->drz, p->st));
+            else
+                PROF_LAUNCH(launch_step3d(p->rule, p->same_xy, a, p->dr, p->dry, p->drz, p->st));
             cur ^= 1;
         }
         if (cur != 0) CUDA_TRY(cudaMemcpyAsync(q, bufs[cur], bytes, cudaMemcpyDeviceToDevice, p->st));
@@ -1688,8 +1692,12 @@ extern "C" int fqnm_debug_override(fqnm_plan_t* p, int32_t kernel, int32_t k, in
         if (V) p->V = V;
         return FQNM_OK;
     }
-    if (p->family == 8 && (kernel || k || V))
-        return fail(FQNM_ERR_UNSUPPORTED, "3D plans have one kernel (K8, one step per launch)");
+    if (p->family == 8) {                 // 3D: kernel 8 = K8 CTA tiles, 10 = K10 warp streaming
+        if (k || V || (kernel && kernel != 8 && kernel != 10))
+            return fail(FQNM_ERR_UNSUPPORTED, "3D plans: kernel 8 or 10, one step per launch");
+        if (kernel) p->stream3d = kernel == 10;
+        return FQNM_OK;
+    }
     if (p->family == 7) {                 // 2D: kernel 7 = K7 smem-tiled (k <= 4), 9 = K9 streaming
         if (kernel == 9) p->stream2d = true;
         else if (kernel == 7) p->stream2d = false;

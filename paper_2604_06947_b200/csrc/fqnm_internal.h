@@ -131,6 +131,11 @@ struct Step3DArgs {
 cudaError_t launch_step3d(int rule, bool same, const Step3DArgs& a, const DevRule& rx,
                           const DevRule& ry, const DevRule& rz, cudaStream_t st);
 int64_t step3d_zchunk(int64_t nx, int64_t ny, int64_t nz);     // z planes per CTA
+// K10: 3D warp streaming (two rows of a 124-wide x strip per warp, no inter-warp
+// exchange; kernels_3d_s.cu)
+cudaError_t launch_step3d_stream(int rule, bool same, const Step3DArgs& a, const DevRule& rx,
+                                 const DevRule& ry, const DevRule& rz, cudaStream_t st);
+int64_t step3d_s_zchunk(int64_t nx, int64_t ny, int64_t nz);
 
 // level-space diagnostics (kernels_diag.cu)
 cudaError_t launch_histogram(const void* q, int dtype, int64_t n, int64_t lo, int64_t L,

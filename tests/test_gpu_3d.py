@@ -1,4 +1,4 @@
-"""GPU parity of the 3D directional composition (K8, fqnm_plan_3d; Thm P:364-401,
+"""GPU parity of the 3D directional composition (K8 and K10, fqnm_plan_3d; Thm P:364-401,
 d = 3) against the 3D oracle (oracle.Rule3D), bit-exact: several rules (same and
 different per-direction maps, LIN_HALF / EO P = 1 / generic paths), both boundaries,
 ragged shapes smaller and larger than one 32 x 8 tile, several step counts; plus
@@ -57,11 +57,15 @@ def test_3d_matches_oracle(F, case, boundary, shape):
     q0 = _field(rng, *shape, amp, off)
     r = oracle.Rule3D(kind, d, *lams, params=params)
     for nsteps in (1, 4, 11):
-        plan = _plan(F, case, shape, boundary)
-        assert plan.info()["kernel"] == 8
-        q = torch.tensor(q0, dtype=torch.int32, device=DEV)
-        F.fqnm_step(plan, q, nsteps)
-        assert np.array_equal(q.cpu().numpy().astype(np.int64), r.run(q0, nsteps, boundary)), nsteps
+        ref = r.run(q0, nsteps, boundary)
+        for kern in (0, 8, 10):                    # default, K8 CTA tiles, K10 warp streaming
+            plan = _plan(F, case, shape, boundary)
+            assert plan.info()["kernel"] == 8
+            if kern:
+                F.fqnm_debug_override(plan, kern)
+            q = torch.tensor(q0, dtype=torch.int32, device=DEV)
+            F.fqnm_step(plan, q, nsteps)
+            assert np.array_equal(q.cpu().numpy().astype(np.int64), ref), (nsteps, kern)
 
 
 def test_3d_large_sampled(F):
