@@ -182,7 +182,8 @@ struct fqnm_plan {
     HostMap hpy, hmy;
     DevRule dry{};
     bool same_xy = false;
-    bool stream2d = true;               // 2D: K9 streaming (1 step/launch) instead of K7
+    bool stream2d = true;               // 2D: K9 streaming instead of K7
+    int k2s = 2;                        // K9 steps per launch (1 or 2)
     bool stream3d = false;              // 3D: K10 warp streaming instead of K8 (measured slower)
     // 3D plans (family 8): z-direction rule
     int64_t nz = 0;
@@ -979,10 +980,17 @@ extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
         a.ny = p->ny;
         a.ksteps = (int32_t)step2d_stream_rows(p->nx, p->ny);
         a.bmode = bm;
-        for (int64_t s = 0; s < nsteps; ++s) {
+        for (int64_t s = 0; s < nsteps;) {
             a.src = (const int32_t*)bufs[cur];
             a.dst = (int32_t*)bufs[cur ^ 1];
-            PROF_LAUNCH(launch_step2d_stream(p->rule, p->same_xy, a, p->dr, p->dry, p->st));
+            // two steps per launch (8192^2: EO 804 vs 629, linear 786 vs 666 GCUPS)
+            if (p->k2s == 2 && s + 2 <= nsteps) {
+                PROF_LAUNCH(launch_step2d_stream2(p->rule, p->same_xy, a, p->dr, p->dry, p->st));
+                s += 2;
+            } else {
+                PROF_LAUNCH(launch_step2d_stream(p->rule, p->same_xy, a, p->dr, p->dry, p->st));
+                s += 1;
+            }
             cur ^= 1;
         }
         if (cur != 0) CUDA_TRY(cudaMemcpyAsync(q, bufs[cur], bytes, cudaMemcpyDeviceToDevice, p->st));
@@ -1698,14 +1706,18 @@ extern "C" int fqnm_debug_override(fqnm_plan_t* p, int32_t kernel, int32_t k, in
         if (kernel) p->stream3d = kernel == 10;
         return FQNM_OK;
     }
-    if (p->family == 7) {                 // 2D: kernel 7 = K7 smem-tiled (k <= 4), 9 = K9 streaming
+    if (p->family == 7) {                 // 2D: kernel 7 = K7 smem-tiled (k <= 4), 9 = K9 streaming (k <= 2)
         if (kernel == 9) p->stream2d = true;
         else if (kernel == 7) p->stream2d = false;
         else if (kernel) return fail(FQNM_ERR_UNSUPPORTED, "2D plans: kernel 7 or 9");
         if (k) {
-            if (k > STEP2D_KMAX) return fail(FQNM_ERR_ARG, "2D plans: k <= %d", STEP2D_KMAX);
-            p->k = k;
-            p->stream2d = false;
+            if (p->stream2d) {
+                if (k > 2) return fail(FQNM_ERR_ARG, "K9: k = 1 or 2");
+                p->k2s = k;
+            } else {
+                if (k > STEP2D_KMAX) return fail(FQNM_ERR_ARG, "2D plans: k <= %d", STEP2D_KMAX);
+                p->k = k;
+            }
         }
         return FQNM_OK;
     }

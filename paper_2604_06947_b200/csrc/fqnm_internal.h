@@ -118,6 +118,8 @@ cudaError_t launch_step2d(int rule, bool same, const Step2DArgs& a, const DevRul
 cudaError_t launch_step2d_stream(int rule, bool same, const Step2DArgs& a, const DevRule& rx,
                                  const DevRule& ry, cudaStream_t st);
 int64_t step2d_stream_rows(int64_t nx, int64_t ny);
+cudaError_t launch_step2d_stream2(int rule, bool same, const Step2DArgs& a, const DevRule& rx,
+                                  const DevRule& ry, cudaStream_t st);   // two steps per launch
 
 // K8: 3D directional composition, one step per launch, 2.5D z-streaming (kernels_3d.cu)
 struct Step3DArgs {

@@ -39,24 +39,94 @@ __device__ __forceinline__ int wrap_row(int r, int n, int bmode)
     return r < 0 ? 0 : (r >= n ? n - 1 : r);
 }
 
+// One row of a lane: the state and its maps.  SAME (one rule for x and y): the maps
+// are kept as g = phi+ + phi- (EO P = 1: biased by a constant, see maps.cuh eo_gm_p1),
+// m = phi- and pb = g - m = phi+ (+ bias); the update
+//   q' = q + (p_l + m_c) - (p_c + m_r) + (p_d + m_c) - (p_c + m_u)
+//      = q + pb_l + pb_d - m_r - m_u + 2 (2 m_c - g_c)
+// is free of the bias (+2 - 2 in the biased terms) and takes 5 operations per cell.
+// The (g, m, pb) form is used for the EO rules with one rule for both directions
+// (measured faster there); the linear and generic rules keep (phi+, phi-) per direction.
 template <int RULE, bool SAME>
-struct Maps2 {
-    int32_t px[K9_V], mx[K9_V], py[K9_V], my[K9_V];
-    __device__ __forceinline__ void eval(const int32_t (&q)[K9_V], const DevRule& rx,
-                                         const DevRule& ry)
+struct GForm { static constexpr bool value = SAME && (RULE == R_EO_P1 || RULE == R_EO_FAST); };
+
+template <int RULE, bool SAME>
+struct Row2 {
+    static constexpr bool G = GForm<RULE, SAME>::value;
+    int32_t q[K9_V];
+    int32_t g[G ? K9_V : 1], m[G ? K9_V : 1], pb[G ? K9_V : 1];
+    int32_t px[G ? 1 : K9_V], mx[G ? 1 : K9_V], py[G ? 1 : K9_V], my[G ? 1 : K9_V];
+    __device__ __forceinline__ void eval(const DevRule& rx, const DevRule& ry)
     {
 #pragma unroll
         for (int j = 0; j < K9_V; ++j) {
-            phi_pm<RULE>(q[j], px[j], mx[j], rx);
-            if (SAME) {
-                py[j] = px[j];
-                my[j] = mx[j];
+            if constexpr (G) {
+                if (j & 1) phi_gm<RULE, true, true>(q[j], g[j], m[j], rx);
+                else phi_gm<RULE, false, true>(q[j], g[j], m[j], rx);
+                pb[j] = g[j] - m[j];
             } else {
-                phi_pm<RULE>(q[j], py[j], my[j], ry);
+                phi_pm<RULE>(q[j], px[j], mx[j], rx);
+                if (SAME) {
+                    py[j] = px[j];
+                    my[j] = mx[j];
+                } else {
+                    phi_pm<RULE>(q[j], py[j], my[j], ry);
+                }
             }
         }
     }
 };
+
+// update of row C from rows B (below) and A (above); wall_* : transmissive ghost-copy
+// transfers (the edge cell's own maps) at the domain boundary
+template <int RULE, bool SAME, bool WALLS>
+__device__ __forceinline__ void update_row(const Row2<RULE, SAME>& B, const Row2<RULE, SAME>& C,
+                                           const Row2<RULE, SAME>& A, int xl, int nx, bool xwall,
+                                           bool wall_lo, bool wall_hi, int32_t (&out)[K9_V])
+{
+    constexpr int V = K9_V;
+    if constexpr (GForm<RULE, SAME>::value) {
+        const int32_t pl = __shfl_up_sync(FULL2, C.pb[V - 1], 1);     // lane 0: halo, unused
+        const int32_t mr = __shfl_down_sync(FULL2, C.m[0], 1);        // lane 31: halo, unused
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const int32_t pbl = j > 0 ? C.pb[j - 1] : pl;
+            const int32_t mrr = j + 1 < V ? C.m[j + 1] : mr;
+            const int32_t w = 2 * C.m[j] - C.g[j];
+            int32_t o = C.q[j] + pbl + B.pb[j] - mrr - A.m[j] + 2 * w;
+            if (WALLS) {
+                if (xwall) {
+                    const int x = xl + j;
+                    if (x == 0) o += C.pb[j] - pbl;                   // F_{-1/2} = phi+(q) + phi-(q)
+                    if (x == nx - 1) o += mrr - C.m[j];
+                }
+                if (wall_lo) o += C.pb[j] - B.pb[j];
+                if (wall_hi) o += A.m[j] - C.m[j];
+            }
+            out[j] = o;
+        }
+    } else {
+        const int32_t pl = __shfl_up_sync(FULL2, C.px[V - 1], 1);
+        const int32_t mr = __shfl_down_sync(FULL2, C.mx[0], 1);
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            int32_t txl = (j > 0 ? C.px[j - 1] : pl) + C.mx[j];
+            int32_t txr = C.px[j] + (j + 1 < V ? C.mx[j + 1] : mr);
+            int32_t tyl = B.py[j] + C.my[j];
+            int32_t tyr = C.py[j] + A.my[j];
+            if (WALLS) {
+                if (xwall) {
+                    const int x = xl + j;
+                    if (x == 0) txl = C.px[j] + C.mx[j];
+                    if (x == nx - 1) txr = C.px[j] + C.mx[j];
+                }
+                if (wall_lo) tyl = C.py[j] + C.my[j];
+                if (wall_hi) tyr = C.py[j] + C.my[j];
+            }
+            out[j] = C.q[j] + txl - txr + tyl - tyr;
+        }
+    }
+}
 
 template <int RULE, bool SAME>
 __global__ void __launch_bounds__(256) k_step2d_s(Step2DArgs a, DevRule rx, DevRule ry)
@@ -117,38 +187,25 @@ __global__ void __launch_bounds__(256) k_step2d_s(Step2DArgs a, DevRule rx, DevR
         v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
     };
 
-    Maps2<RULE, SAME> M0, M1, M2;
-    int32_t Q0[V], Q1[V], Q2[V];
+    // one step: the clamped halo loads already are the transmissive ghost copies
+    Row2<RULE, SAME> P0, P1, P2;
     for (int r = y0 - 1; r < y0 + L; ++r) issue(r, r - y0 + 1);   // rows y0 - 1 .. y0 + L - 1
     asm volatile("cp.async.wait_group %0;" :: "n"(L - 1) : "memory");   // rows y0 - 1, y0 landed
-    read(0, Q2);
-    M2.eval(Q2, rx, ry);                                   // row y0 - 1 (its phi+_y)
-    read(1, Q0);
-    M0.eval(Q0, rx, ry);
+    read(0, P2.q);
+    P2.eval(rx, ry);                                       // row y0 - 1
+    read(1, P0.q);
+    P0.eval(rx, ry);
     int sz = 1;                                            // stage of row r
-    // one row: Qc/Mc = row r, Qn/Mn = row r + 1 (read from the ring, maps evaluated
-    // here), Mp = row r - 1
-    auto body = [&](int r, int32_t (&Qc)[V], int32_t (&Qn)[V], Maps2<RULE, SAME>& Mp,
-                    Maps2<RULE, SAME>& Mc, Maps2<RULE, SAME>& Mn) {
+    // one row: C = row r, Nn = row r + 1 (read from the ring, maps evaluated here),
+    // Bp = row r - 1
+    auto body = [&](int r, Row2<RULE, SAME>& Bp, Row2<RULE, SAME>& C, Row2<RULE, SAME>& Nn) {
         const int sn = sz + 1 == S ? 0 : sz + 1, sl = sz == 0 ? S - 1 : sz - 1;
         asm volatile("cp.async.wait_group %0;" :: "n"(L - 2) : "memory");  // rows <= r + 1
-        read(sn, Qn);
+        read(sn, Nn.q);
         issue(r + L, sl);                                  // into row r - 1's stage
-        Mn.eval(Qn, rx, ry);
-        const int32_t pl = __shfl_up_sync(FULL2, Mc.px[V - 1], 1);   // lane 0: halo cell, unused
-        const int32_t mr = __shfl_down_sync(FULL2, Mc.mx[0], 1);     // lane 31: halo, unused
-        // transmissive walls need no special case: the clamped halo loads make the
-        // wall transfer phi+(q_e) + phi-(q_e) (ghost copy, reading A12)
+        Nn.eval(rx, ry);
         int32_t out[V];
-#pragma unroll
-        for (int j = 0; j < V; ++j) {
-            const int32_t txl = (j > 0 ? Mc.px[j - 1] : pl) + Mc.mx[j];        // F^x_{i-1/2}
-            const int32_t txr = Mc.px[j] + (j + 1 < V ? Mc.mx[j + 1] : mr);    // F^x_{i+1/2}
-            const int32_t tyl = Mp.py[j] + Mc.my[j];                           // F^y_{j-1/2}
-            const int32_t tyr = Mc.py[j] + Mn.my[j];                           // F^y_{j+1/2}
-            out[j] = Qc[j] + txl - txr + tyl - tyr;
-        }
-        // (transmissive rows: wrap_row clamps, so the ghost rows repeat the edge row)
+        update_row<RULE, SAME, false>(Bp, C, Nn, xl, nx, false, false, false, out);
         int32_t* row = a.dst + r * nx;
         if (vec) {
             if (lane > 0 && lane < 31) {
@@ -168,13 +225,151 @@ __global__ void __launch_bounds__(256) k_step2d_s(Step2DArgs a, DevRule rx, DevR
     };
     int r = y0;
     for (; r + 3 <= y1; r += 3) {
-        body(r, Q0, Q1, M2, M0, M1);
-        body(r + 1, Q1, Q2, M0, M1, M2);
-        body(r + 2, Q2, Q0, M1, M2, M0);
+        body(r, P2, P0, P1);
+        body(r + 1, P0, P1, P2);
+        body(r + 2, P1, P2, P0);
     }
-    if (r < y1) body(r, Q0, Q1, M2, M0, M1);
-    if (r + 1 < y1) body(r + 1, Q1, Q2, M0, M1, M2);
+    if (r < y1) body(r, P2, P0, P1);
+    if (r + 1 < y1) body(r + 1, P0, P1, P2);
     asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// K9 with two steps per launch (temporal blocking k = 2): the warp streams the step-0
+// rows, computes step-1 row t-1 as soon as step-0 row t has arrived and step-2 row t-2
+// as soon as step-1 row t-1 exists; only step-2 rows are stored, so one HBM round trip
+// advances two steps (4 B per cell-update).  The two halo columns on each side are
+// exactly the dependence of two steps; a chunk recomputes two step-1 rows beyond each
+// end.  Transmissive walls: the boundary transfer of every step uses the edge cell's
+// own maps (ghost copy, reading A12), as the clamped halo no longer carries it.
+template <int RULE, bool SAME>
+__global__ void __launch_bounds__(256) k_step2d_s2(Step2DArgs a, DevRule rx, DevRule ry)
+{
+    constexpr int V = K9_V, L = K9_LOOK;
+    const int lane = threadIdx.x & 31;
+    const int warp = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int nx = (int)a.nx, ny = (int)a.ny, bm = a.bmode;
+    const int nstrips = (nx + K9_S - 1) / K9_S;
+    const int yc = a.ksteps;                               // rows per chunk (launcher)
+    const int nchunks = (ny + yc - 1) / yc;
+    if (warp >= nstrips * nchunks) return;
+    const int strip = warp % nstrips, chunk = warp / nstrips;
+    const int x0 = strip * K9_S - K9_H;
+    const int y0 = chunk * yc, y1 = (y0 + yc < ny) ? y0 + yc : ny;
+    const int xl = x0 + lane * V;
+    const bool vec = x0 >= 0 && x0 + K9_W <= nx && (nx % 2 == 0);
+    const bool wall = bm == BM_TRANSMISSIVE;
+    const bool xwall = wall && (x0 <= 0 || x0 + K9_W - 1 >= nx - 1);      // a wall is in the strip
+    int xo[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) xo[j] = wrap2(xl + j, nx, bm);
+    bool stc[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        const int p = lane * V + j, x = xl + j;
+        stc[j] = p >= K9_H && p < K9_W - K9_H && x >= 0 && x < nx;
+    }
+    __shared__ int4 ring[L][256 / 32][32];
+    const int wib = threadIdx.x >> 5;
+    const unsigned ring0 = (unsigned)__cvta_generic_to_shared(&ring[0][wib][lane]);
+    constexpr unsigned RSTRIDE = sizeof(ring[0]);
+    const int t0 = y0 - 2, t1 = y1 + 1;                    // step-0 rows streamed
+    auto issue = [&](int t, int stg) {
+        if (t <= t1) {
+            const int32_t* row = a.src + wrap_row(t, ny, bm) * nx;
+            const unsigned d = ring0 + stg * RSTRIDE;
+            if (vec) {
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(d), "l"(row + xl) : "memory");
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(d + 8), "l"(row + xl + 2) : "memory");
+            } else {
+#pragma unroll
+                for (int j = 0; j < V; ++j)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(d + 4 * j), "l"(row + xo[j]) : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int i = 0; i < L; ++i) issue(t0 + i, i);
+    // three rotating slots per stage (step-0 rows t-2, t-1, t; step-1 rows t-3, t-2,
+    // t-1), the loop unrolled by three so the rotation needs no register moves
+    Row2<RULE, SAME> P0, P1, P2, Q0, Q1, Q2;
+    int stg = 0;
+    auto body = [&](int t, Row2<RULE, SAME>& A0, Row2<RULE, SAME>& B0, Row2<RULE, SAME>& C0,
+                    Row2<RULE, SAME>& A1, Row2<RULE, SAME>& B1, Row2<RULE, SAME>& C1) {
+        asm volatile("cp.async.wait_group %0;" :: "n"(L - 1) : "memory");  // row t landed
+        {
+            int4 v;
+            asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(ring0 + stg * RSTRIDE) : "memory");
+            C0.q[0] = v.x; C0.q[1] = v.y; C0.q[2] = v.z; C0.q[3] = v.w;
+        }
+        issue(t + L, stg);                                 // the row just read is free
+        stg = stg + 1 == L ? 0 : stg + 1;
+        C0.eval(rx, ry);
+        if (t >= y0) {                                     // step-1 row t - 1
+            const int r = t - 1;
+            if (wall) update_row<RULE, SAME, true>(A0, B0, C0, xl, nx, xwall, r == 0, r == ny - 1, C1.q);
+            else update_row<RULE, SAME, false>(A0, B0, C0, xl, nx, false, false, false, C1.q);
+            C1.eval(rx, ry);
+            if (t >= y0 + 2) {                             // step-2 row t - 2: store
+                const int r2 = t - 2;
+                int32_t out[V];
+                if (wall) update_row<RULE, SAME, true>(A1, B1, C1, xl, nx, xwall, r2 == 0, r2 == ny - 1, out);
+                else update_row<RULE, SAME, false>(A1, B1, C1, xl, nx, false, false, false, out);
+                int32_t* row = a.dst + r2 * nx;
+                if (vec) {
+                    if (lane > 0 && lane < 31) {
+                        *reinterpret_cast<int2*>(row + xl) = make_int2(out[0], out[1]);
+                        *reinterpret_cast<int2*>(row + xl + 2) = make_int2(out[2], out[3]);
+                    } else if (lane == 0) {
+                        *reinterpret_cast<int2*>(row + xl + 2) = make_int2(out[2], out[3]);
+                    } else {
+                        *reinterpret_cast<int2*>(row + xl) = make_int2(out[0], out[1]);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < V; ++j)
+                        if (stc[j]) row[xl + j] = out[j];
+                }
+            }
+        }
+    };
+    const int niter = t1 - t0 + 1;
+    int i = 0;
+    for (; i + 3 <= niter; i += 3) {
+        body(t0 + i, P1, P2, P0, Q0, Q1, Q2);
+        body(t0 + i + 1, P2, P0, P1, Q1, Q2, Q0);
+        body(t0 + i + 2, P0, P1, P2, Q2, Q0, Q1);
+    }
+    if (i < niter) body(t0 + i, P1, P2, P0, Q0, Q1, Q2);
+    if (i + 1 < niter) body(t0 + i + 1, P2, P0, P1, Q1, Q2, Q0);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+template <int RULE>
+static cudaError_t s2d2_rule(bool same, const Step2DArgs& a, const DevRule& rx, const DevRule& ry,
+                             cudaStream_t st)
+{
+    const int64_t strips = (a.nx + K9_S - 1) / K9_S;
+    const int64_t chunks = (a.ny + a.ksteps - 1) / a.ksteps;
+    const unsigned grid = (unsigned)((strips * chunks * 32 + 255) / 256);
+    if (same) k_step2d_s2<RULE, true><<<grid, 256, 0, st>>>(a, rx, ry);
+    else k_step2d_s2<RULE, false><<<grid, 256, 0, st>>>(a, rx, ry);
+    return cudaGetLastError();
+}
+
+// two time steps per launch (a.ksteps carries the rows per chunk)
+cudaError_t launch_step2d_stream2(int rule, bool same, const Step2DArgs& a, const DevRule& rx,
+                                  const DevRule& ry, cudaStream_t st)
+{
+    if (a.ksteps < 1) return cudaErrorInvalidValue;
+    switch (rule) {
+        case R_LIN_HALF: return s2d2_rule<R_LIN_HALF>(same, a, rx, ry, st);
+        case R_EO_FAST: return s2d2_rule<R_EO_FAST>(same, a, rx, ry, st);
+        case R_EO_P1: return s2d2_rule<R_EO_P1>(same, a, rx, ry, st);
+        case R_GENERIC: return s2d2_rule<R_GENERIC>(same, a, rx, ry, st);
+        case R_LIN_FAST: return s2d2_rule<R_LIN_FAST>(same, a, rx, ry, st);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 int64_t step2d_stream_rows(int64_t nx, int64_t ny)

@@ -498,8 +498,9 @@ def test_2d_matches_oracle(F, case, boundary, shape):
     rng = np.random.default_rng(ny * 7 + nx + case)
     q0 = _field2d(rng, ny, nx, amp, off)
     r = oracle.Rule2D(kind, d, lx, ly, ax, ay)
-    # K9 streaming (default, one step per launch) and K7 smem-tiled with k = 1, 3, 4
-    for nsteps, kern, k in ((1, 0, 0), (5, 9, 0), (13, 0, 0), (13, 7, 1), (9, 7, 3), (11, 7, 4)):
+    # K9 streaming (default k = 2 per launch, odd remainder with k = 1) and K7 smem-tiled
+    for nsteps, kern, k in ((1, 0, 0), (5, 9, 1), (13, 0, 0), (6, 9, 2), (13, 7, 1), (9, 7, 3),
+                            (11, 7, 4)):
         plan = F.fqnm_plan_2d(nx, ny, float(Fraction(d)), float(lx), float(ly), kind, boundary,
                               float(ax), float(ay))
         assert plan.info()["kernel"] == 7

@@ -78,7 +78,7 @@ def main():
                 q0 = torch.tensor(W.quantise(u, 1e-6), dtype=torch.int32, device="cuda")
                 plan = F.fqnm_plan_2d(nx, ny, 1e-6, 0.25, 0.25, F.LINEAR, F.PERIODIC)
             if os.environ.get("K2D"):
-                F.fqnm_debug_override(plan, 0, int(os.environ["K2D"]), 0)
+                F.fqnm_debug_override(plan, int(os.environ.get("KERN2D", 0)), int(os.environ["K2D"]), 0)
             steps, cells = 200, nx * ny
         elif name in ("godunov2", "godunov26"):
             # quantised two-point Godunov rule (Thm P:262-280) on cfg2 data (K6) and on
