@@ -1075,6 +1075,7 @@ extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
 static void halo_args(fqnm_plan_t* p, BlockedArgs& a, int ksteps, uint32_t tag)
 {
     const fqnm_plan_desc& d = p->d;
+    std::memset(&a, 0, sizeof a);                       // every field defined (guard = null)
     a.src = (const int32_t*)p->hbuf[p->hcur];
     a.dst = (int32_t*)p->hbuf[p->hcur ^ 1];
     a.n = d.n_local;
