@@ -52,19 +52,33 @@ __device__ __forceinline__ int wrap_z(int z, int n, int bmode)
 }
 
 // maps of one cell for the three directions (SAME: one evaluation serves all)
+// G form (one EO rule for all directions): g = phi+ + phi- kept with the constant
+// bias of maps.cuh eo_gm_p1, m = phi-, p* = g - m (phi+ plus the bias); the update
+//   q' = q + p_xl + p_yd + p_zd - m_xr - m_yu - m_zu + 3 (2 m_c - g_c)
+// is free of the bias (+3 from the three p terms, -3 from the last term).
+template <int RULE, bool SAME>
+struct GForm3 { static constexpr bool value = SAME && (RULE == R_EO_P1 || RULE == R_EO_FAST); };
+
 template <int RULE, bool SAME>
 struct Maps3 {
-    int32_t px, mx, py, my, pz, mz;
+    int32_t px, mx, py, my, pz, mz, g;
     __device__ __forceinline__ void eval(int32_t q, const DevRule& rx, const DevRule& ry,
                                          const DevRule& rz)
     {
-        phi_pm<RULE>(q, px, mx, rx);
-        if (SAME) {
+        if constexpr (GForm3<RULE, SAME>::value) {
+            phi_gm<RULE, false, true>(q, g, mx, rx);
+            px = g - mx;
             py = pz = px;
             my = mz = mx;
         } else {
-            phi_pm<RULE>(q, py, my, ry);
-            phi_pm<RULE>(q, pz, mz, rz);
+            phi_pm<RULE>(q, px, mx, rx);
+            if (SAME) {
+                py = pz = px;
+                my = mz = mx;
+            } else {
+                phi_pm<RULE>(q, py, my, ry);
+                phi_pm<RULE>(q, pz, mz, rz);
+            }
         }
     }
 };
@@ -194,10 +208,15 @@ __global__ void __launch_bounds__(32 * K8_WARPS) k_step3d(Step3DArgs a, DevRule 
             for (int j = 0; j < V; ++j) {
                 const int32_t pxl = j > 0 ? Mc[j - 1].px : pl;
                 const int32_t mxr = j + 1 < V ? Mc[j + 1].mx : mr;
-                const int32_t dF = (Mc[j].px + mxr) - (pxl + Mc[j].mx) +
-                                   (Mc[j].py + myu[j]) - (pyd[j] + Mc[j].my) +
-                                   (Mc[j].pz + Mn[j].mz) - (Mp[j].pz + Mc[j].mz);
-                out[j] = Qc[j] - dF;
+                if constexpr (GForm3<RULE, SAME>::value) {
+                    out[j] = Qc[j] + pxl + pyd[j] + Mp[j].pz - mxr - myu[j] - Mn[j].mz +
+                             3 * (2 * Mc[j].mx - Mc[j].g);
+                } else {
+                    const int32_t dF = (Mc[j].px + mxr) - (pxl + Mc[j].mx) +
+                                       (Mc[j].py + myu[j]) - (pyd[j] + Mc[j].my) +
+                                       (Mc[j].pz + Mn[j].mz) - (Mp[j].pz + Mc[j].mz);
+                    out[j] = Qc[j] - dF;
+                }
             }
             if (row_own) {
                 const int base = z * plane + row;
