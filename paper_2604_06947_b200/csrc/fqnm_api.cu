@@ -185,6 +185,13 @@ struct fqnm_plan {
     bool stream2d = true;               // 2D: K9 streaming instead of K7
     int k2s = 2;                        // K9 steps per launch (1 or 2)
     bool stream3d = false;              // 3D: K10 warp streaming instead of K8 (measured slower)
+    // K2P persistent stepper (one launch for all blocks): -1 auto, 0 off, 1 forced.
+    // Off by default: measured slower than launch-per-block K2 (cfg3 53 vs 27 ms)
+    int persist = 0;
+    unsigned int* pflags = nullptr;
+    unsigned long long* pcounter = nullptr;
+    int64_t pflags_n = 0;
+    uint32_t ptag = 1;
     // 3D plans (family 8): z-direction rule
     int64_t nz = 0;
     DevRule drz{};
@@ -830,6 +837,8 @@ extern "C" void fqnm_destroy(fqnm_plan_t* p)
     for (int i = 0; i < 2; ++i)
         if (p->hbuf[i]) cudaFree(p->hbuf[i]);
     if (p->hflags) cudaFree(p->hflags);
+    if (p->pflags) cudaFree(p->pflags);
+    if (p->pcounter) cudaFree(p->pcounter);
     for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
     pipe_release(p);
     delete p;
@@ -919,6 +928,63 @@ static int launch_block(fqnm_plan_t* p, const int32_t* src, int32_t* dst, int ks
     if (S < 4) return fail(FQNM_ERR_ARG, "k = %d too large for V = %d", ksteps, p->V);
     a.nwin = (d.n_local + S - 1) / S;
     PROF_LAUNCH(launch_blocked(p->rule, p->V, p->minb, a, p->dr, p->st, 148 * 32));
+    return FQNM_OK;
+}
+
+// K2P eligibility: one single-domain problem on the V = 32 / 2-CTA K2 variant with a rule
+// the persistent kernel is built for; auto mode when a launch would have few waves of
+// windows (the last partial wave of each launch is then a visible share of the time)
+static bool use_persist(fqnm_plan_t* p, int64_t nb)
+{
+    const fqnm_plan_desc& d = p->d;
+    if (p->persist == 0 || nb < 2) return false;
+    if (p->family != 2 || d.batch != 1 || d.boundary == FQNM_HALO || p->V != 32 || p->minb != 2 ||
+        !blocked_persist_has_rule(p->rule) || p->guard)
+        return false;
+    if (p->persist == 1) return true;
+    const int64_t S = 32 * p->V - (p->dep_left ? round4(p->k) : 0) - (p->dep_right ? round4(p->k) : 0);
+    const int64_t nwin = (d.n_local + S - 1) / S;
+    return nwin < 64 * 148 * 16;                     // fewer than 64 waves of resident warps
+}
+
+static int step_persist(fqnm_plan_t* p, void* q, int64_t nb, int64_t base, int64_t rem)
+{
+    const fqnm_plan_desc& d = p->d;
+    const int kmax = (int)(base + (rem > 0 ? 1 : 0));
+    PersistArgs a;
+    std::memset(&a, 0, sizeof a);
+    a.buf0 = (int32_t*)q;
+    a.buf1 = (int32_t*)p->scratch;
+    a.n = d.n_local;
+    a.KL = p->dep_left ? round4(kmax) : 0;
+    a.KR = p->dep_right ? round4(kmax) : 0;
+    a.S = 32 * p->V - a.KL - a.KR;
+    if (a.S < 4) return fail(FQNM_ERR_ARG, "k = %d too large for V = %d", kmax, p->V);
+    a.nwin = (a.n + a.S - 1) / a.S;
+    a.base = (int32_t)base;
+    a.rem = (int32_t)rem;
+    a.nblocks = (int32_t)nb;
+    a.bmode = bmode_of(d);
+    if (p->pflags_n < a.nwin) {
+        if (p->pflags) cudaFree(p->pflags);
+        p->pflags = nullptr;
+        CUDA_TRY(cudaMalloc(&p->pflags, (size_t)a.nwin * sizeof(unsigned int)));
+        CUDA_TRY(cudaMemsetAsync(p->pflags, 0, (size_t)a.nwin * sizeof(unsigned int), p->st));
+        p->pflags_n = a.nwin;
+        p->ptag = 1;
+    }
+    if (!p->pcounter) CUDA_TRY(cudaMalloc(&p->pcounter, sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemsetAsync(p->pcounter, 0, sizeof(unsigned long long), p->st));
+    // flags carry tag_base + blocks completed; tags strictly increase across calls
+    if (p->ptag > 0xF0000000u - (uint32_t)nb) {
+        CUDA_TRY(cudaMemsetAsync(p->pflags, 0, (size_t)p->pflags_n * sizeof(unsigned int), p->st));
+        p->ptag = 1;
+    }
+    a.flags = p->pflags;
+    a.counter = p->pcounter;
+    a.tag_base = p->ptag;
+    p->ptag += (uint32_t)nb + 1;
+    PROF_LAUNCH(launch_blocked_persist(p->rule, a, p->dr, p->st));
     return FQNM_OK;
 }
 
@@ -1061,6 +1127,12 @@ extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
         int64_t nb = (nsteps + p->k - 1) / p->k;
         if (nb % 2 == 1 && nsteps >= nb + 1) nb += 1;
         const int64_t base = nsteps / nb, rem = nsteps % nb;
+        if (use_persist(p, nb)) {
+            if ((rc = step_persist(p, q, nb, base, rem)) != FQNM_OK) return rc;
+            cur = (int)(nb & 1);
+            if (cur != 0) CUDA_TRY(cudaMemcpyAsync(q, bufs[cur], bytes, cudaMemcpyDeviceToDevice, p->st));
+            return FQNM_OK;
+        }
         for (int64_t b = 0; b < nb; ++b) {
             int ks = (int)(base + (b < rem ? 1 : 0));
             if ((rc = launch_block(p, (const int32_t*)bufs[cur], (int32_t*)bufs[cur ^ 1], ks)) != FQNM_OK)
@@ -1726,6 +1798,29 @@ extern "C" int fqnm_debug_override(fqnm_plan_t* p, int32_t kernel, int32_t k, in
         p->minb = kernel / 100;
         kernel = kernel % 100;
     }
+    if (kernel == 12) {                 // K2P persistent stepper (K2 geometry V = 32, 2 CTAs/SM)
+        if (d.nvar != 1 || p->family >= 7 || d.batch != 1 || d.boundary == FQNM_HALO ||
+            !blocked_persist_has_rule(p->rule))
+            return fail(FQNM_ERR_UNSUPPORTED, "K2P needs a single-domain 1D plan with a fast rule");
+        if (max_block_steps(p, 32) < 1 || d.n_local < 32 * 32)
+            return fail(FQNM_ERR_UNSUPPORTED, "K2P needs n >= one V = 32 window");
+        if (!p->scratch) {
+            p->scratch_bytes = state_elems(d) * elem_size(d);
+            CUDA_TRY(cudaMalloc(&p->scratch, p->scratch_bytes));
+        }
+        p->family = 2;
+        if (p->k < 1) p->k = 16;
+        if (p->k > max_block_steps(p, 32)) p->k = max_block_steps(p, 32);
+        p->V = 32;
+        p->minb = 2;
+        p->persist = 1;
+        if (k) {
+            if (k > max_block_steps(p, 32)) return fail(FQNM_ERR_ARG, "k too large for V = 32");
+            p->k = k;
+        }
+        return FQNM_OK;
+    }
+    if (kernel == 2) p->persist = 0;
     if (kernel) {
         if (d.boundary == FQNM_HALO && kernel != 2) return fail(FQNM_ERR_UNSUPPORTED, "split domains use K2");
         if (kernel == 3) {

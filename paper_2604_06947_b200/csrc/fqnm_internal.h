@@ -158,6 +158,21 @@ cudaError_t launch_blocked(int rule, int V, int minb, const BlockedArgs& a, cons
                            cudaStream_t st, int grid_cap);
 cudaError_t launch_resident(int rule, int V, const ResidentArgsHost& h, const DevRule& r,
                             cudaStream_t st);
+
+// K2P: persistent temporally blocked stepper (kernels_scalar.cu): all blocks of k steps in
+// one launch; warps claim (block, window) items in order from a counter, and an item of
+// block b waits (acquire) for the block b-1 items covering its input window (release flags)
+struct PersistArgs {
+    int32_t* buf0;              // block b reads buf[b & 1], writes buf[(b + 1) & 1]
+    int32_t* buf1;
+    int64_t n, nwin;
+    int32_t S, KL, KR, base, rem, nblocks, bmode, pad;   // block b: base + (b < rem) steps
+    unsigned int* flags;        // [nwin]: tag_base + (blocks completed) for the window
+    unsigned long long* counter;
+    uint32_t tag_base;
+};
+cudaError_t launch_blocked_persist(int rule, const PersistArgs& a, const DevRule& r, cudaStream_t st);
+bool blocked_persist_has_rule(int rule);
 cudaError_t launch_halo_prime(const BlockedArgs& a, cudaStream_t st);
 cudaError_t launch_naive(int rule, const int32_t* src, int32_t* dst, int64_t n, int64_t batch,
                          int bmode, const DevRule& r, cudaStream_t st);

@@ -467,6 +467,161 @@ __global__ void __launch_bounds__(256, MINB) k_blocked(BlockedArgs a, DevRule r)
 }
 
 // ---------------------------------------------------------------------------
+// K2P: persistent K2.  One launch runs all nblocks blocks of k steps: warps claim items
+// (block b, window w) in increasing order from a global counter; an item of block b > 0
+// first acquires the flags of the block b-1 windows whose owned cells overlap its input
+// window (they are earlier items, claimed by running warps, so the wait always ends),
+// then steps the window exactly as K2 and releases its own flag.  Loads bypass L1
+// (ld.global.cg): the inputs were written inside this launch by other SMs.  The wait
+// set is widened symmetrically (max(KL, KR) on both sides) so it also orders the
+// write-after-read on the ping-pong buffer (see persist_wait_cover).
+// Removes the per-launch tail (the last partial wave of windows) and launch gaps.
+// Wait for the block b-1 windows whose owned cells overlap [wS - E, wS + S + E),
+// E = max(KL, KR) (periodic wrap / clamped walls): they cover the item's input window
+// (read after write) and include every block b-1 item that reads the cells this item
+// overwrites in the other buffer (write after read: those items' input windows reach
+// KL/KR cells into this window's owned range).  The whole warp takes part (lane i
+// polls the i-th window) so it never diverges around the hot loop; relaxed polling,
+// one acquire fence at the end.
+static __device__ __forceinline__ void persist_wait_cover(const PersistArgs& a, int64_t w,
+                                                          uint32_t target, int lane)
+{
+    const int64_t n = a.n, S = a.S, nwin = a.nwin;
+    const int64_t E = a.KL > a.KR ? a.KL : a.KR;
+    const int64_t span = (S + 2 * E + S - 1) / S + 1;          // windows touched, upper bound
+    // the range in window units, relative to w; walls clamp, periodic wraps
+    const int64_t lo = w * S - E, hi = w * S + S + E - 1;
+    int64_t my = -1;
+    if (lane < 2 * span + 2) {
+        // lane i -> the window containing cell lo + i * S (and the last cell for the last lane)
+        int64_t x = lo + (int64_t)lane * S;
+        if (x > hi) x = hi;
+        if (a.bmode == BM_PERIODIC) { x %= n; if (x < 0) x += n; }
+        else x = x < 0 ? 0 : (x >= n ? n - 1 : x);
+        my = x / S;
+        if (my >= nwin) my = nwin - 1;
+    }
+    // the last window may be short: also cover the window before the wrap point
+    if (lane == 31 && a.bmode == BM_PERIODIC && (lo < 0 || hi >= n)) my = nwin - 1 > 0 ? nwin - 2 : 0;
+    if (lane == 30 && a.bmode == BM_PERIODIC && (lo < 0 || hi >= n)) my = nwin - 1;
+    const long long t0 = clock64();
+    for (;;) {
+        bool ok = true;
+        if (my >= 0) {
+            unsigned int f;
+            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(a.flags + my) : "memory");
+            ok = (int)(f - target) >= 0;
+        }
+        if (__all_sync(0xffffffffu, ok)) break;
+        if (clock64() - t0 > SPIN_TRAP_CYCLES) __trap();
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");   // acquire: the relaxed reads above
+}
+
+// windows that wrap or touch a wall: scalar L1-bypassing loads through wrap_index
+template <int RULE, int V>
+static __device__ __noinline__ void persist_slow(const int32_t* src, int32_t* dst, int64_t ws,
+                                                 int64_t n, int bmode, int ks, const DevRule& r,
+                                                 int lo, int hi, int lane)
+{
+    const int64_t g0 = ws + lane * V;
+    int32_t q[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) q[j] = __ldcg(src + wrap_index(g0 + j, n, bmode, 0));
+    if (bmode == BM_TRANSMISSIVE) run_window_steps<RULE, V, true>(q, ks, r, g0, n);
+    else run_window_steps<RULE, V, false>(q, ks, r, g0, n);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        const int pos = lane * V + j;
+        const int64_t gi = g0 + j;
+        if (pos >= lo && pos < hi && gi >= 0 && gi < n) __stcg(dst + gi, q[j]);
+    }
+}
+
+template <int RULE, int V, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_blocked_persist(PersistArgs a, DevRule r)
+{
+    constexpr int W = 32 * V;
+    const int lane = threadIdx.x & 31;
+    const int64_t n = a.n, nwin = a.nwin, S = a.S;
+    const unsigned long long total = (unsigned long long)a.nblocks * (unsigned long long)nwin;
+    const int lo = a.KL, hi = W - a.KR;
+    for (;;) {
+        unsigned long long item = 0;
+        if (lane == 0) item = atomicAdd(a.counter, 1ull);
+        item = __shfl_sync(FULL, item, 0);
+        if (item >= total) return;
+        const int b = (int)(item / (unsigned long long)nwin);
+        const int64_t w = (int64_t)(item - (unsigned long long)b * (unsigned long long)nwin);
+        const int64_t ws = w * S - a.KL;                           // first cell of the window
+        const int32_t* src = (b & 1) ? a.buf1 : a.buf0;
+        int32_t* dst = (b & 1) ? a.buf0 : a.buf1;
+#ifndef FQNM_PERSIST_NOWAIT
+        if (b > 0) persist_wait_cover(a, w, a.tag_base + (uint32_t)b, lane);
+#endif
+        const int ks = a.base + (b < a.rem ? 1 : 0);
+        int32_t q[V];
+        if (ws >= 0 && ws + W <= n) {
+            const int4* s4 = reinterpret_cast<const int4*>(src + ws) + lane * (V / 4);
+#pragma unroll
+            for (int j = 0; j < V / 4; ++j) {
+                const int4 v = __ldcg(s4 + j);
+                q[4 * j] = v.x; q[4 * j + 1] = v.y; q[4 * j + 2] = v.z; q[4 * j + 3] = v.w;
+            }
+            run_window_steps<RULE, V, false>(q, ks, r, 0, 0);
+            int4* d4 = reinterpret_cast<int4*>(dst + ws) + lane * (V / 4);
+#pragma unroll
+            for (int j = 0; j < V / 4; ++j) {
+                const int pos = lane * V + 4 * j;
+                if (pos >= lo && pos < hi)
+                    __stcg(d4 + j, make_int4(q[4 * j], q[4 * j + 1], q[4 * j + 2], q[4 * j + 3]));
+            }
+        } else {
+            persist_slow<RULE, V>(src, dst, ws, n, a.bmode, ks, r, lo, hi, lane);
+        }
+        __syncwarp();
+        if (lane == 0) {
+#ifndef FQNM_PERSIST_NOFENCE
+            __threadfence();
+#endif
+            asm volatile("st.release.gpu.global.u32 [%0], %1;"
+                         :: "l"(a.flags + w), "r"(a.tag_base + (uint32_t)b + 1u) : "memory");
+        }
+    }
+}
+
+#if FQNM_PART(5)
+bool blocked_persist_has_rule(int rule)
+{
+    return rule == R_LIN_HALF || rule == R_EO_P1 || rule == R_EO_FAST || rule == R_LIN_FAST;
+}
+
+template <int RULE>
+static cudaError_t persist_rule(const PersistArgs& a, const DevRule& r, cudaStream_t st)
+{
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blocked_persist<RULE, 32, 2>,
+                                                                  256, 0);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    k_blocked_persist<RULE, 32, 2><<<per_sm * sms, 256, 0, st>>>(a, r);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_blocked_persist(int rule, const PersistArgs& a, const DevRule& r, cudaStream_t st)
+{
+    switch (rule) {
+        case R_LIN_HALF: return persist_rule<R_LIN_HALF>(a, r, st);
+        case R_EO_P1: return persist_rule<R_EO_P1>(a, r, st);
+        case R_EO_FAST: return persist_rule<R_EO_FAST>(a, r, st);
+        case R_LIN_FAST: return persist_rule<R_LIN_FAST>(a, r, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+#endif
+
+// ---------------------------------------------------------------------------
 // K1: naive, one thread per cell, one step per launch
 template <int RULE>
 __global__ void k_naive(const int32_t* __restrict__ src, int32_t* __restrict__ dst, int64_t n,
