@@ -1367,7 +1367,22 @@ static int pipe_setup(fqnm_plan_t* p, int64_t nsteps)
     return FQNM_OK;
 }
 
+static int step_host_pipelined_impl(fqnm_plan_t* p, int32_t* qh, int64_t nsteps);
+
+// on any failure, drain the three streams before returning so no copy into the caller's
+// host buffer is still in flight
 static int step_host_pipelined(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
+{
+    const int rc = step_host_pipelined_impl(p, qh, nsteps);
+    if (rc != FQNM_OK) {
+        cudaStreamSynchronize(p->pipe_h2d);
+        cudaStreamSynchronize(p->st);
+        cudaStreamSynchronize(p->pipe_d2h);
+    }
+    return rc;
+}
+
+static int step_host_pipelined_impl(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
 {
     const int64_t n = p->d.n_local, C = p->pipe_C, H = p->pipe_H, m = p->pipe_m, E = C + 2 * H;
     fqnm_plan_t* ch = p->pipe_child;
