@@ -21,7 +21,10 @@
 namespace fqnm {
 
 static constexpr unsigned FULL2 = 0xffffffffu;
-static constexpr int K9_V = 4;                  // x cells per lane
+#ifndef FQNM_K9_V
+#define FQNM_K9_V 4
+#endif
+static constexpr int K9_V = FQNM_K9_V;          // x cells per lane (even)
 static constexpr int K9_W = 32 * K9_V;          // loaded strip width
 static constexpr int K9_H = 2;                  // halo columns per side
 static constexpr int K9_S = K9_W - 2 * K9_H;    // strip stride (stored columns)
@@ -47,6 +50,54 @@ __device__ __forceinline__ int wrap_row(int r, int n, int bmode)
 // is free of the bias (+2 - 2 in the biased terms) and takes 5 operations per cell.
 // The (g, m, pb) form is used for the EO rules with one rule for both directions
 // (measured faster there); the linear and generic rules keep (phi+, phi-) per direction.
+// Per-warp row ring in shared memory: lane l's V cells of a row as V/2 int2 slots at
+// [h][l] (conflict-free 8-byte accesses), filled by the lane itself with cp.async.
+struct K9Ring {
+    unsigned base;                                  // this lane's slot 0 of stage 0
+    static constexpr unsigned HSTRIDE = 32 * 8;     // bytes between the int2 slots of a lane
+    static constexpr unsigned STAGE = (K9_V / 2) * HSTRIDE * (256 / 32);
+    __device__ __forceinline__ unsigned at(int stg, int h) const { return base + stg * STAGE + h * HSTRIDE; }
+    // copy the lane's cells of `row` (fast: 8-byte pieces at xl; else scalar through xo)
+    __device__ __forceinline__ void issue(int stg, const int32_t* row, bool vec, int xl,
+                                          const int (&xo)[K9_V]) const
+    {
+        if (vec) {
+#pragma unroll
+            for (int h = 0; h < K9_V / 2; ++h)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(at(stg, h)), "l"(row + xl + 2 * h) : "memory");
+        } else {
+#pragma unroll
+            for (int j = 0; j < K9_V; ++j)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(at(stg, j / 2) + 4 * (j & 1)), "l"(row + xo[j]) : "memory");
+        }
+    }
+    __device__ __forceinline__ void read(int stg, int32_t (&v)[K9_V]) const
+    {
+#pragma unroll
+        for (int h = 0; h < K9_V / 2; ++h)
+            asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v[2 * h]), "=r"(v[2 * h + 1]) : "r"(at(stg, h)) : "memory");
+    }
+};
+
+// store the lane's cells of an output row: 8-byte pieces on the fast path (the halo
+// pairs at the strip ends are skipped), guarded scalar stores otherwise
+__device__ __forceinline__ void k9_store(int32_t* row, bool vec, int lane, int xl,
+                                         const int32_t (&out)[K9_V], const bool (&st)[K9_V])
+{
+    if (vec) {
+#pragma unroll
+        for (int h = 0; h < K9_V / 2; ++h) {
+            const int p = lane * K9_V + 2 * h;
+            if (p >= K9_H && p < K9_W - K9_H)
+                *reinterpret_cast<int2*>(row + xl + 2 * h) = make_int2(out[2 * h], out[2 * h + 1]);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < K9_V; ++j)
+            if (st[j]) row[xl + j] = out[j];
+    }
+}
+
 template <int RULE, bool SAME>
 struct GForm { static constexpr bool value = SAME && (RULE == R_EO_P1 || RULE == R_EO_FAST); };
 
@@ -161,31 +212,14 @@ __global__ void __launch_bounds__(256) k_step2d_s(Step2DArgs a, DevRule rx, DevR
     // row; a lane reads only the slots it filled, so no barrier is needed.
     // Stage of row r: (r - y0 + 1) % S.
     constexpr int L = K9_LOOK, S = K9_LOOK + 1;
-    __shared__ int4 ring[S][256 / 32][32];
-    const int wib = threadIdx.x >> 5;
-    const unsigned ring0 = (unsigned)__cvta_generic_to_shared(&ring[0][wib][lane]);
-    constexpr unsigned RSTRIDE = sizeof(ring[0]);
+    __shared__ int2 ring[S][256 / 32][K9_V / 2][32];
+    K9Ring rg;
+    rg.base = (unsigned)__cvta_generic_to_shared(&ring[0][threadIdx.x >> 5][0][lane]);
     auto issue = [&](int r, int stg) {
-        if (r <= y1) {                                     // rows beyond y1 are never read
-            const int32_t* row = a.src + wrap_row(r, ny, bm) * nx;
-            const unsigned d = ring0 + stg * RSTRIDE;
-            if (vec) {
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(d), "l"(row + xl) : "memory");
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(d + 8), "l"(row + xl + 2) : "memory");
-            } else {
-#pragma unroll
-                for (int j = 0; j < V; ++j)
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(d + 4 * j), "l"(row + xo[j]) : "memory");
-            }
-        }
+        if (r <= y1) rg.issue(stg, a.src + wrap_row(r, ny, bm) * nx, vec, xl, xo);   // rows beyond y1 are never read
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    auto read = [&](int stg, int32_t (&v)[V]) {
-        int4 t;
-        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(t.x), "=r"(t.y), "=r"(t.z), "=r"(t.w) : "r"(ring0 + stg * RSTRIDE) : "memory");
-        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-    };
+    auto read = [&](int stg, int32_t (&v)[V]) { rg.read(stg, v); };
 
     // one step: the clamped halo loads already are the transmissive ghost copies
     Row2<RULE, SAME> P0, P1, P2;
@@ -206,21 +240,7 @@ __global__ void __launch_bounds__(256) k_step2d_s(Step2DArgs a, DevRule rx, DevR
         Nn.eval(rx, ry);
         int32_t out[V];
         update_row<RULE, SAME, false>(Bp, C, Nn, xl, nx, false, false, false, out);
-        int32_t* row = a.dst + r * nx;
-        if (vec) {
-            if (lane > 0 && lane < 31) {
-                *reinterpret_cast<int2*>(row + xl) = make_int2(out[0], out[1]);
-                *reinterpret_cast<int2*>(row + xl + 2) = make_int2(out[2], out[3]);
-            } else if (lane == 0) {
-                *reinterpret_cast<int2*>(row + xl + 2) = make_int2(out[2], out[3]);
-            } else {
-                *reinterpret_cast<int2*>(row + xl) = make_int2(out[0], out[1]);
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < V; ++j)
-                if (st[j]) row[xl + j] = out[j];
-        }
+        k9_store(a.dst + r * nx, vec, lane, xl, out, st);
         sz = sn;
     };
     int r = y0;
@@ -268,24 +288,12 @@ __global__ void __launch_bounds__(256) k_step2d_s2(Step2DArgs a, DevRule rx, Dev
         const int p = lane * V + j, x = xl + j;
         stc[j] = p >= K9_H && p < K9_W - K9_H && x >= 0 && x < nx;
     }
-    __shared__ int4 ring[L][256 / 32][32];
-    const int wib = threadIdx.x >> 5;
-    const unsigned ring0 = (unsigned)__cvta_generic_to_shared(&ring[0][wib][lane]);
-    constexpr unsigned RSTRIDE = sizeof(ring[0]);
+    __shared__ int2 ring[L][256 / 32][K9_V / 2][32];
+    K9Ring rg;
+    rg.base = (unsigned)__cvta_generic_to_shared(&ring[0][threadIdx.x >> 5][0][lane]);
     const int t0 = y0 - 2, t1 = y1 + 1;                    // step-0 rows streamed
     auto issue = [&](int t, int stg) {
-        if (t <= t1) {
-            const int32_t* row = a.src + wrap_row(t, ny, bm) * nx;
-            const unsigned d = ring0 + stg * RSTRIDE;
-            if (vec) {
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(d), "l"(row + xl) : "memory");
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(d + 8), "l"(row + xl + 2) : "memory");
-            } else {
-#pragma unroll
-                for (int j = 0; j < V; ++j)
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(d + 4 * j), "l"(row + xo[j]) : "memory");
-            }
-        }
+        if (t <= t1) rg.issue(stg, a.src + wrap_row(t, ny, bm) * nx, vec, xl, xo);
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     for (int i = 0; i < L; ++i) issue(t0 + i, i);
@@ -296,12 +304,7 @@ __global__ void __launch_bounds__(256) k_step2d_s2(Step2DArgs a, DevRule rx, Dev
     auto body = [&](int t, Row2<RULE, SAME>& A0, Row2<RULE, SAME>& B0, Row2<RULE, SAME>& C0,
                     Row2<RULE, SAME>& A1, Row2<RULE, SAME>& B1, Row2<RULE, SAME>& C1) {
         asm volatile("cp.async.wait_group %0;" :: "n"(L - 1) : "memory");  // row t landed
-        {
-            int4 v;
-            asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(ring0 + stg * RSTRIDE) : "memory");
-            C0.q[0] = v.x; C0.q[1] = v.y; C0.q[2] = v.z; C0.q[3] = v.w;
-        }
+        rg.read(stg, C0.q);
         issue(t + L, stg);                                 // the row just read is free
         stg = stg + 1 == L ? 0 : stg + 1;
         C0.eval(rx, ry);
@@ -315,21 +318,7 @@ __global__ void __launch_bounds__(256) k_step2d_s2(Step2DArgs a, DevRule rx, Dev
                 int32_t out[V];
                 if (wall) update_row<RULE, SAME, true>(A1, B1, C1, xl, nx, xwall, r2 == 0, r2 == ny - 1, out);
                 else update_row<RULE, SAME, false>(A1, B1, C1, xl, nx, false, false, false, out);
-                int32_t* row = a.dst + r2 * nx;
-                if (vec) {
-                    if (lane > 0 && lane < 31) {
-                        *reinterpret_cast<int2*>(row + xl) = make_int2(out[0], out[1]);
-                        *reinterpret_cast<int2*>(row + xl + 2) = make_int2(out[2], out[3]);
-                    } else if (lane == 0) {
-                        *reinterpret_cast<int2*>(row + xl + 2) = make_int2(out[2], out[3]);
-                    } else {
-                        *reinterpret_cast<int2*>(row + xl) = make_int2(out[0], out[1]);
-                    }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < V; ++j)
-                        if (stc[j]) row[xl + j] = out[j];
-                }
+                k9_store(a.dst + r2 * nx, vec, lane, xl, out, stc);
             }
         }
     };
