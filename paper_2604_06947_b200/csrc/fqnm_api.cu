@@ -416,7 +416,7 @@ static int build_rule(fqnm_plan_t* p)
         // EO magnitude g(x) = RHA(kappa x^2) evaluated by the closed form (maps.cuh)
         tp_fast = (tp_kind == FQNM_BURGERS_GODUNOV && (p->rule == R_EO_P1 || p->rule == R_EO_FAST))
                       ? (p->rule == R_EO_P1 ? 1 : 2) : 0;
-        p->rule = R_TWOPOINT;
+        p->rule = tp_fast ? R_TP_FAST : R_TWOPOINT;
         p->dep_left = p->dep_right = true;
     }
     p->lo = lo;
@@ -442,7 +442,7 @@ static int build_rule(fqnm_plan_t* p)
         while ((double)cf > target) cf = std::nextafterf(cf, 0.0f);
         r.eo_cf = cf;
     }
-    if (p->rule == R_TWOPOINT) {
+    if (p->rule == R_TWOPOINT || p->rule == R_TP_FAST) {
         r.tp_kind = tp_kind;
         r.tp_c2 = p->hp.c2;
         r.tp_c1 = tp_kind == FQNM_BURGERS_LF2 ? p->hp.c1 : 0;
@@ -505,7 +505,9 @@ static int choose_kernel(fqnm_plan_t* p)
     if (p->family == 2) {
         const bool two = p->dep_left && p->dep_right;
         if (p->rule == R_LIN_HALF) { p->V = 32; p->k = 64; p->minb = 2; }
-        else if (p->rule == R_EO_FAST || p->rule == R_EO_P1) { p->V = 32; p->k = 24; p->minb = 2; }
+        else if (p->rule == R_EO_FAST || p->rule == R_EO_P1 || p->rule == R_TP_FAST) {
+            p->V = 32; p->k = 24; p->minb = 2;
+        }
         else { p->V = 8; p->k = two ? 8 : 16; }
         if (d.k > 0) p->k = d.k;
         if (d.boundary == FQNM_HALO && p->k > d.halo) p->k = (int)d.halo;
@@ -1591,7 +1593,7 @@ extern "C" int fqnm_transfer(const fqnm_plan_t* p, int64_t q, int64_t* phi_plus,
 {
     if (!p || !phi_plus || !phi_minus) return fail(FQNM_ERR_ARG, "null argument");
     if (p->d.nvar != 1) return fail(FQNM_ERR_ARG, "scalar plans only");
-    if (p->rule == R_TWOPOINT)
+    if (p->rule == R_TWOPOINT || p->rule == R_TP_FAST)
         return fail(FQNM_ERR_UNSUPPORTED, "two-point rule has no split maps: use fqnm_transfer2");
     *phi_plus = host_phi(p->hp, q, p->d.rounding);
     *phi_minus = host_phi(p->hm, q, p->d.rounding);
@@ -1612,7 +1614,7 @@ extern "C" int fqnm_transfer_device(const fqnm_plan_t* p, const int32_t* q, int3
 static int64_t host_transfer2(const fqnm_plan_t* p, int64_t qL, int64_t qR)
 {
     const int rd = p->d.rounding;
-    if (p->rule != R_TWOPOINT) return host_phi(p->hp, qL, rd) + host_phi(p->hm, qR, rd);
+    if (p->rule != R_TWOPOINT && p->rule != R_TP_FAST) return host_phi(p->hp, qL, rd) + host_phi(p->hm, qR, rd);
     const DevRule& r = p->dr;
     const i128 L = qL, R = qR;
     i128 num;

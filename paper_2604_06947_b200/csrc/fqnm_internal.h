@@ -18,6 +18,8 @@ enum RuleKind : int32_t {
                       // (q^2 - Q est) form, one instruction shorter (maps.cuh eo_gm_p1)
     R_TWOPOINT = 6,   // quantised two-point rule Phi(qL, qR) rounded once (Godunov / EO2 / LF2),
                       // exact int64 evaluation (maps.cuh tp_phi)
+    R_TP_FAST = 7,    // two-point Godunov on the EO closed-form domain: Phi = g(max(qL+, -qR-))
+                      // with the EO magnitude g (maps.cuh tp_godunov_fast)
     R_LIN_FAST = 4    // LINEAR any |kappa| <= 1, RHA: g(|q|) = floor((2P|q| + Q)/(2Q)) by the
                       // same estimate + remainder scheme as EO (eo_* constants), sign restored
 };

@@ -172,6 +172,7 @@ __device__ __forceinline__ int32_t transfer_any(int rule, int32_t qL, int32_t qR
         case R_EO_P1: return transfer_lr<R_EO_P1>(qL, qR, r);
         case R_LIN_FAST: return transfer_lr<R_LIN_FAST>(qL, qR, r);
         case R_TWOPOINT: return transfer_lr<R_TWOPOINT>(qL, qR, r);
+        case R_TP_FAST: return transfer_lr<R_TP_FAST>(qL, qR, r);
         default: return transfer_lr<R_GENERIC>(qL, qR, r);
     }
 }

@@ -103,7 +103,7 @@ __device__ __forceinline__ void one_step(int32_t (&q)[V], const DevRule& r, int 
         q[0] = pl * r.one + h[0];
 #pragma unroll
         for (int j = 1; j < V; ++j) q[j] = p[j - 1] * r.one + h[j];
-    } else if (RULE == R_TWOPOINT) {
+    } else if (RULE == R_TWOPOINT || RULE == R_TP_FAST) {
         // two-point rule: T_{j+1/2} = Phi(q_j, q_{j+1}); needs the right neighbour's state
         const int32_t qr = NB == 0 ? __shfl_down_sync(FULL, q[0], 1)
                                    : __shfl_sync(FULL, q[0], (lane + 1) & 31);
@@ -112,13 +112,13 @@ __device__ __forceinline__ void one_step(int32_t (&q)[V], const DevRule& r, int 
         for (int j = 0; j < V; ++j) {
             int32_t qn = (j + 1 < V) ? q[j + 1] : qr;
             if (WALL && g0 + j == n - 1) qn = q[j];             // ghost q_N = q_{N-1}
-            T[j] = tp_phi(q[j], qn, r);
+            T[j] = tp_eval<RULE>(q[j], qn, r);
         }
         int32_t Tl = NB == 0 ? __shfl_up_sync(FULL, T[V - 1], 1)
                              : __shfl_sync(FULL, T[V - 1], (lane + 31) & 31);
 #pragma unroll
         for (int j = 0; j < V; ++j) {
-            if (WALL && g0 + j == 0) Tl = tp_phi(q[j], q[j], r);  // ghost q_{-1} = q_0
+            if (WALL && g0 + j == 0) Tl = tp_eval<RULE>(q[j], q[j], r);  // ghost q_{-1} = q_0
             const int32_t t = T[j];
             q[j] = q[j] + Tl - t;
             Tl = t;
@@ -212,7 +212,7 @@ __device__ __forceinline__ void run_window_steps(int32_t (&q)[V], int ksteps, co
                                                  int64_t g0, int64_t n)
 {
     const int lane = threadIdx.x & 31;
-    if (FQNM_FUSED_STEPS && RULE != R_TWOPOINT && !WALL && ksteps > 0) {
+    if (FQNM_FUSED_STEPS && RULE != R_TWOPOINT && RULE != R_TP_FAST && !WALL && ksteps > 0) {
         int32_t g[V], m[V];
         if (RULE == R_LIN_HALF) {
 #pragma unroll
@@ -640,8 +640,8 @@ __global__ void k_naive(const int32_t* __restrict__ src, int32_t* __restrict__ d
             if (il < 0) il = 0;
             if (ir >= n) ir = n - 1;
         }
-        if (RULE == R_TWOPOINT) {
-            dst[b * n + i] = s[i] - (tp_phi(s[i], s[ir], r) - tp_phi(s[il], s[i], r));
+        if (RULE == R_TWOPOINT || RULE == R_TP_FAST) {
+            dst[b * n + i] = s[i] - (tp_eval<RULE>(s[i], s[ir], r) - tp_eval<RULE>(s[il], s[i], r));
             continue;
         }
         int32_t pl, ml, pc, mc, pr, mr;
@@ -959,17 +959,17 @@ __global__ void __launch_bounds__(1024) k_cta_ensemble(int32_t* __restrict__ q, 
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) Q[i] = qb[i];
     __syncthreads();
     for (int64_t s = 0; s < nsteps; ++s) {
-        if constexpr (RULE == R_TWOPOINT) {
+        if constexpr (RULE == R_TWOPOINT || RULE == R_TP_FAST) {
             // P[i] = T_{i+1/2} = Phi(q_i, q_{i+1}) (ghost/wrap as the boundary says)
             for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
                 int64_t ir = i + 1;
                 if (ir >= n) ir = (bmode == BM_PERIODIC) ? 0 : n - 1;
-                P[i] = tp_phi(Q[i], Q[ir], r);
+                P[i] = tp_eval<RULE>(Q[i], Q[ir], r);
             }
             __syncthreads();
             for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
                 const int32_t Fl = (i > 0) ? P[i - 1]
-                                 : (bmode == BM_PERIODIC ? P[n - 1] : tp_phi(Q[0], Q[0], r));
+                                 : (bmode == BM_PERIODIC ? P[n - 1] : tp_eval<RULE>(Q[0], Q[0], r));
                 Q[i] = Q[i] - (P[i] - Fl);
             }
             __syncthreads();
@@ -1103,6 +1103,7 @@ template <>
 cudaError_t blocked_rule<R_TWOPOINT>(int V, int minb, const BlockedArgs& a, const DevRule& r,
                                      cudaStream_t st, int cap);
 #if FQNM_PART(9)
+template cudaError_t blocked_rule<R_TP_FAST>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
 template <>
 cudaError_t blocked_rule<R_TWOPOINT>(int V, int minb, const BlockedArgs& a, const DevRule& r,
                                      cudaStream_t st, int cap)
@@ -1123,6 +1124,7 @@ extern template cudaError_t blocked_rule<R_EO_FAST>(int, int, const BlockedArgs&
 extern template cudaError_t blocked_rule<R_EO_P1>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
 extern template cudaError_t blocked_rule<R_GENERIC>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
 extern template cudaError_t blocked_rule<R_LIN_FAST>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
+extern template cudaError_t blocked_rule<R_TP_FAST>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
 #endif
 bool blocked_has_V(int V) { return V == 8 || V == 16 || V == 32; }
 bool blocked_rule_has_V(int rule, int V) { return rule == R_TWOPOINT ? (V == 8 || V == 16) : blocked_has_V(V); }
@@ -1138,6 +1140,7 @@ cudaError_t launch_blocked(int rule, int V, int minb, const BlockedArgs& a, cons
         case R_GENERIC: return blocked_rule<R_GENERIC>(V, minb, a, r, st, grid_cap);
         case R_LIN_FAST: return blocked_rule<R_LIN_FAST>(V, minb, a, r, st, grid_cap);
         case R_TWOPOINT: return blocked_rule<R_TWOPOINT>(V, minb, a, r, st, grid_cap);
+        case R_TP_FAST: return blocked_rule<R_TP_FAST>(V, minb, a, r, st, grid_cap);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -1154,6 +1157,7 @@ cudaError_t launch_naive(int rule, const int32_t* src, int32_t* dst, int64_t n, 
         case R_GENERIC: k_naive<R_GENERIC><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
         case R_LIN_FAST: k_naive<R_LIN_FAST><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
         case R_TWOPOINT: k_naive<R_TWOPOINT><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
+        case R_TP_FAST: k_naive<R_TP_FAST><<<g, threads, 0, st>>>(src, dst, n, batch, bmode, r); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -1197,6 +1201,7 @@ template cudaError_t warp_rule<R_LIN_FAST>(int, int32_t*, int64_t, int64_t, int,
 #endif
 #if FQNM_PART(10)
 template cudaError_t warp_rule<R_TWOPOINT>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
+template cudaError_t warp_rule<R_TP_FAST>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
 #endif
 #if FQNM_PART(4)
 template cudaError_t warp_rule<R_GENERIC>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
@@ -1234,6 +1239,7 @@ int resident_capacity_warps(int rule, int V)
           : rule == R_EO_P1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_EO_P1, 8>, 256, 0)
           : rule == R_LIN_FAST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_LIN_FAST, 8>, 256, 0)
           : rule == R_TWOPOINT ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_TWOPOINT, 8>, 256, 0)
+          : rule == R_TP_FAST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_TP_FAST, 8>, 256, 0)
           : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_GENERIC, 8>, 256, 0);
     } else {
         e = rule == R_LIN_HALF ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_LIN_HALF, 4>, 256, 0)
@@ -1241,6 +1247,7 @@ int resident_capacity_warps(int rule, int V)
           : rule == R_EO_P1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_EO_P1, 4>, 256, 0)
           : rule == R_LIN_FAST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_LIN_FAST, 4>, 256, 0)
           : rule == R_TWOPOINT ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_TWOPOINT, 4>, 256, 0)
+          : rule == R_TP_FAST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_TP_FAST, 4>, 256, 0)
           : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<R_GENERIC, 4>, 256, 0);
     }
     if (e != cudaSuccess) return 0;
@@ -1260,6 +1267,7 @@ cudaError_t launch_resident(int rule, int V, const ResidentArgsHost& h, const De
         case R_GENERIC: return V == 8 ? resident_v<R_GENERIC, 8>(h, r, st) : resident_v<R_GENERIC, 4>(h, r, st);
         case R_LIN_FAST: return V == 8 ? resident_v<R_LIN_FAST, 8>(h, r, st) : resident_v<R_LIN_FAST, 4>(h, r, st);
         case R_TWOPOINT: return V == 8 ? resident_v<R_TWOPOINT, 8>(h, r, st) : resident_v<R_TWOPOINT, 4>(h, r, st);
+        case R_TP_FAST: return V == 8 ? resident_v<R_TP_FAST, 8>(h, r, st) : resident_v<R_TP_FAST, 4>(h, r, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -1270,6 +1278,7 @@ cudaError_t launch_resident(int rule, int V, const ResidentArgsHost& h, const De
 #if FQNM_SCALAR_PART == 3
 extern template cudaError_t warp_rule<R_GENERIC>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
 extern template cudaError_t warp_rule<R_TWOPOINT>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
+extern template cudaError_t warp_rule<R_TP_FAST>(int, int32_t*, int64_t, int64_t, int, const DevRule&, cudaStream_t);
 #endif
 bool warp_ensemble_has_V(int V) { return V == 1 || V == 2 || V == 4 || V == 8 || V == 16 || V == 32; }
 
@@ -1283,6 +1292,7 @@ cudaError_t launch_warp_ensemble(int rule, int V, int32_t* q, int64_t batch, int
         case R_GENERIC: return warp_rule<R_GENERIC>(V, q, batch, nsteps, bmode, r, st);
         case R_LIN_FAST: return warp_rule<R_LIN_FAST>(V, q, batch, nsteps, bmode, r, st);
         case R_TWOPOINT: return warp_rule<R_TWOPOINT>(V, q, batch, nsteps, bmode, r, st);
+        case R_TP_FAST: return warp_rule<R_TP_FAST>(V, q, batch, nsteps, bmode, r, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -1313,6 +1323,7 @@ cudaError_t launch_cta_ensemble(int rule, int32_t* q, int64_t n, int64_t batch, 
         case R_GENERIC: return cta_rule<R_GENERIC>(q, n, batch, nsteps, bmode, r, st);
         case R_LIN_FAST: return cta_rule<R_LIN_FAST>(q, n, batch, nsteps, bmode, r, st);
         case R_TWOPOINT: return cta_rule<R_TWOPOINT>(q, n, batch, nsteps, bmode, r, st);
+        case R_TP_FAST: return cta_rule<R_TP_FAST>(q, n, batch, nsteps, bmode, r, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -1340,6 +1351,7 @@ cudaError_t launch_transfer2(int rule, const int32_t* qL, const int32_t* qR, int
         case R_GENERIC: k_transfer2<R_GENERIC><<<g, 256, 0, st>>>(qL, qR, T, n, r); break;
         case R_LIN_FAST: k_transfer2<R_LIN_FAST><<<g, 256, 0, st>>>(qL, qR, T, n, r); break;
         case R_TWOPOINT: k_transfer2<R_TWOPOINT><<<g, 256, 0, st>>>(qL, qR, T, n, r); break;
+        case R_TP_FAST: k_transfer2<R_TP_FAST><<<g, 256, 0, st>>>(qL, qR, T, n, r); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -204,17 +204,6 @@ __device__ __forceinline__ void phi_pm(int32_t q, int32_t& p, int32_t& m, const 
 // evaluated exactly in int64 (headroom validated by the planner).
 __device__ __forceinline__ int32_t tp_phi(int32_t qL, int32_t qR, const DevRule& r)
 {
-    if (r.tp_fast) {
-        // Godunov for Burgers: Phi = RHA(kappa max(max(qL,0)^2, min(qR,0)^2)) = g(x) with
-        // x = max(max(qL,0), -min(qR,0)) and the EO magnitude g (closed form, exact on the
-        // planner-proved domain |q| < 2^22, kappa q^2 <= 2^20)
-        const int32_t a = qL > 0 ? qL : 0, b = qR < 0 ? -qR : 0;
-        const int32_t x = a > b ? a : b;
-        int32_t g, m;
-        if (r.tp_fast == 1) eo_gm_p1<0, false>(x, g, m, r);
-        else eo_gm(x, g, m, r);
-        return g;
-    }
     const int64_t L = qL, R = qR;
     int64_t num;
     if (r.tp_kind == 7) {
@@ -227,12 +216,33 @@ __device__ __forceinline__ int32_t tp_phi(int32_t qL, int32_t qR, const DevRule&
     return (int32_t)round_div_i64(num, r.tp_den, r.rounding);
 }
 
+// Godunov for Burgers on the EO fast path's domain (rule R_TP_FAST):
+// Phi = RHA(kappa max(max(qL,0)^2, min(qR,0)^2)) = g(x), x = max(max(qL,0), -min(qR,0)),
+// with the EO magnitude g in closed form (exact for |q| < 2^22, kappa q^2 <= 2^20,
+// proved by the planner); tp_fast = 1: P = 1 form, 2: general P
+__device__ __forceinline__ int32_t tp_godunov_fast(int32_t qL, int32_t qR, const DevRule& r)
+{
+    const int32_t a = qL > 0 ? qL : 0, b = qR < 0 ? -qR : 0;
+    const int32_t x = a > b ? a : b;
+    int32_t g, m;
+    if (r.tp_fast == 1) eo_gm_p1<0, false>(x, g, m, r);
+    else eo_gm(x, g, m, r);
+    return g;
+}
+
+template <int RULE>
+__device__ __forceinline__ int32_t tp_eval(int32_t qL, int32_t qR, const DevRule& r)
+{
+    if (RULE == R_TP_FAST) return tp_godunov_fast(qL, qR, r);
+    return tp_phi(qL, qR, r);
+}
+
 // Interface transfer T = Phi(qL, qR) of any scalar rule: split rules
 // phi+(qL) + phi-(qR), two-point rules tp_phi.
 template <int RULE>
 __device__ __forceinline__ int32_t transfer_lr(int32_t qL, int32_t qR, const DevRule& r)
 {
-    if (RULE == R_TWOPOINT) return tp_phi(qL, qR, r);
+    if (RULE == R_TWOPOINT || RULE == R_TP_FAST) return tp_eval<RULE>(qL, qR, r);
     int32_t pL, mL, pR, mR;
     phi_pm<RULE>(qL, pL, mL, r);
     phi_pm<RULE>(qR, pR, mR, r);
