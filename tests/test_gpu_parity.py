@@ -538,8 +538,8 @@ def test_lin_fast_maps_and_families(F, lam, a):
 
 def test_sod_t02_n65536_physics(F):
     """cfg5's physics at N = 2^16 to t = 0.2 on the GPU (38 772 steps, beyond what the
-    oracle runs in a test): exact conservation of mass (the density transfer at a wall is
-    RHA(fl(m s)) = 0 while the wall cells keep m = 0), and the density is close to the
+    oracle runs in a test): exact conservation of mass (the density transfers at the
+    walls, RHA(fl(m s)), round to 0 in this run), and the density is close to the
     exact Riemann solution (heuristic bound; no convergence theory for systems).
     (Energy and momentum are not checked: one-quantum precursors of the Roe dissipation
     reach the walls long before the physical waves and give the edge cells a nonzero
