@@ -28,9 +28,23 @@ namespace fqnm {
 static constexpr unsigned FULL3 = 0xffffffffu;
 static constexpr int K8_V = 4;                  // x cells per lane
 static constexpr int K8_TX = 32 * K8_V;         // tile width (x)
-static constexpr int K8_TY = 8;                 // owned rows (y)
+#ifndef FQNM_K8_TY
+#define FQNM_K8_TY 8
+#endif
+static constexpr int K8_TY = FQNM_K8_TY;        // owned rows (y)
 static constexpr int K8_WARPS = K8_TY + 2;      // + 2 halo rows
-static constexpr int K8_LOOK = 6;               // planes in flight per thread (cp.async ring)
+#ifndef FQNM_K8_LOOK
+#define FQNM_K8_LOOK 6
+#endif
+static constexpr int K8_LOOK = FQNM_K8_LOOK;    // planes in flight per thread (cp.async ring)
+// resident CTAs per SM asked of ptxas: 2 for the EO rules (98 -> 88 registers, so two
+// 320-thread CTAs fit the register file: 459 vs 357 GCUPS at 512^3); the other rules fit
+// two CTAs uncapped and run slower capped (linear 449 vs 391; profiles/r01_3d.jsonl)
+#ifndef FQNM_K8_MINB
+#define FQNM_K8_MINB 0
+#endif
+template <int RULE>
+constexpr int k8_minb() { return FQNM_K8_MINB ? FQNM_K8_MINB : ((RULE == R_EO_P1 || RULE == R_EO_FAST) ? 2 : 1); }
 
 __device__ __forceinline__ int wrap_i(int i, int n, int bmode)
 {
@@ -87,11 +101,14 @@ struct Maps3 {
 // loads/stores); otherwise scalar accesses with wrapped x offsets (the last partial
 // tile column, launched separately)
 template <int RULE, bool SAME, bool VEC>
-__global__ void __launch_bounds__(32 * K8_WARPS) k_step3d(Step3DArgs a, DevRule rx, DevRule ry,
+__global__ void __launch_bounds__(32 * K8_WARPS, k8_minb<RULE>()) k_step3d(Step3DArgs a, DevRule rx, DevRule ry,
                                                         DevRule rz)
 {
     constexpr int V = K8_V;
-    __shared__ int4 sPy[K8_WARPS][32], sMy[K8_WARPS][32];     // y maps of the plane, per row
+    // y maps of the plane, per row; double-buffered by plane parity so one barrier per
+    // plane suffices (a warp writing buffer b for plane z + 2 has passed the barrier of
+    // plane z + 1, which every warp reaches only after its reads of plane z)
+    __shared__ int4 sPy[2][K8_WARPS][32], sMy[2][K8_WARPS][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int nx = (int)a.nx, ny = (int)a.ny, nz = (int)a.nz, bm = a.bmode;
     const int plane = nx * ny;
@@ -118,13 +135,15 @@ __global__ void __launch_bounds__(32 * K8_WARPS) k_step3d(Step3DArgs a, DevRule 
     // commit group per plane; a thread only ever reads the slots it filled, so the
     // ring needs no barrier of its own.  Stage of plane p: (p - z0 + 1) % S.
     constexpr int L = K8_LOOK, S = K8_LOOK + 1;
-    __shared__ int4 ring[S][K8_WARPS][32];
+    // the ring lives in dynamic shared memory (static shared memory is capped at 48 KB)
+    extern __shared__ int4 k8_dyn[];
+    int4 (*ring)[K8_WARPS][32] = reinterpret_cast<int4 (*)[K8_WARPS][32]>(k8_dyn);
     __shared__ int32_t ering[S][K8_WARPS][2];
     const int eslot = lane == 0 ? 0 : 1;
     // shared-memory addresses of this thread's ring slots, computed once
     const unsigned ring0 = (unsigned)__cvta_generic_to_shared(&ring[0][w][lane]);
     const unsigned ering0 = (unsigned)__cvta_generic_to_shared(&ering[0][w][eslot]);
-    constexpr unsigned RSTRIDE = sizeof(ring[0]), ESTRIDE = sizeof(ering[0]);
+    constexpr unsigned RSTRIDE = K8_WARPS * 32 * sizeof(int4), ESTRIDE = sizeof(ering[0]);
     const int32_t* gsrc = a.src + row;
     auto issue = [&](int p, int st) {
         if (p <= z1) {                                     // planes beyond z1 are never read
@@ -171,7 +190,7 @@ __global__ void __launch_bounds__(32 * K8_WARPS) k_step3d(Step3DArgs a, DevRule 
     // one plane: Qc/Mc = plane z, Qn/Mn = plane z + 1 (own rows read it from the ring
     // and evaluate its maps here), Mp = plane z - 1 (its phi+_z)
     // stage indices: sz = stage of plane z, sn = of z + 1, sl = of z - 1 (= of z + L)
-    int sz = 1;
+    int sz = 1, yb = 0;
     auto body = [&](int z, int32_t (&Qc)[V], int32_t (&Qn)[V], Maps3<RULE, SAME> (&Mp)[V],
                     Maps3<RULE, SAME> (&Mc)[V], Maps3<RULE, SAME> (&Mn)[V]) {
         const int sn = next(sz), sl = sz == 0 ? S - 1 : sz - 1;
@@ -195,12 +214,12 @@ __global__ void __launch_bounds__(32 * K8_WARPS) k_step3d(Step3DArgs a, DevRule 
             if (lane == 31) mr = me.mx;
         }
         issue(z + L, sl);                                  // into plane z - 1's stage
-        sPy[w][lane] = make_int4(Mc[0].py, Mc[1].py, Mc[2].py, Mc[3].py);
-        sMy[w][lane] = make_int4(Mc[0].my, Mc[1].my, Mc[2].my, Mc[3].my);
+        sPy[yb][w][lane] = make_int4(Mc[0].py, Mc[1].py, Mc[2].py, Mc[3].py);
+        sMy[yb][w][lane] = make_int4(Mc[0].my, Mc[1].my, Mc[2].my, Mc[3].my);
         __syncthreads();
         if (!halo_row) {
-            const int4 pd = sPy[w - 1][lane];                  // row below: phi+_y
-            const int4 mu = sMy[w + 1][lane];                  // row above: phi-_y
+            const int4 pd = sPy[yb][w - 1][lane];              // row below: phi+_y
+            const int4 mu = sMy[yb][w + 1][lane];              // row above: phi-_y
             const int32_t pyd[V] = {pd.x, pd.y, pd.z, pd.w};
             const int32_t myu[V] = {mu.x, mu.y, mu.z, mu.w};
             int32_t out[V];
@@ -230,7 +249,7 @@ __global__ void __launch_bounds__(32 * K8_WARPS) k_step3d(Step3DArgs a, DevRule 
                 }
             }
         }
-        __syncthreads();
+        yb ^= 1;
         sz = sn;
     };
     int z = z0;
@@ -250,6 +269,18 @@ static cudaError_t step3d_rule(bool same, const Step3DArgs& a0, const DevRule& r
 {
     Step3DArgs a = a0;
     dim3 block(32 * K8_WARPS);
+    constexpr size_t dyn = (size_t)(K8_LOOK + 1) * K8_WARPS * 32 * sizeof(int4);
+    static unsigned long long attr_set = 0;                // once per instantiation and device
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64 || !(attr_set >> dev & 1ull)) {
+        for (auto f : {k_step3d<RULE, true, true>, k_step3d<RULE, false, true>,
+                       k_step3d<RULE, true, false>, k_step3d<RULE, false, false>}) {
+            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)dyn);
+            if (e != cudaSuccess) return e;
+        }
+        if (dev < 64) attr_set |= 1ull << dev;
+    }
     const unsigned gy = (unsigned)((a.ny + K8_TY - 1) / K8_TY);
     const unsigned gz = (unsigned)((a.nz + a.zchunk - 1) / a.zchunk);
     // full 128-wide tiles on the int4 path, the partial last tile column separately
@@ -258,14 +289,14 @@ static cudaError_t step3d_rule(bool same, const Step3DArgs& a0, const DevRule& r
     if (full > 0) {
         a.xt0 = 0;
         dim3 grid((unsigned)full, gy, gz);
-        if (same) k_step3d<RULE, true, true><<<grid, block, 0, st>>>(a, rx, ry, rz);
-        else k_step3d<RULE, false, true><<<grid, block, 0, st>>>(a, rx, ry, rz);
+        if (same) k_step3d<RULE, true, true><<<grid, block, dyn, st>>>(a, rx, ry, rz);
+        else k_step3d<RULE, false, true><<<grid, block, dyn, st>>>(a, rx, ry, rz);
     }
     if (total > full) {
         a.xt0 = full;
         dim3 grid((unsigned)(total - full), gy, gz);
-        if (same) k_step3d<RULE, true, false><<<grid, block, 0, st>>>(a, rx, ry, rz);
-        else k_step3d<RULE, false, false><<<grid, block, 0, st>>>(a, rx, ry, rz);
+        if (same) k_step3d<RULE, true, false><<<grid, block, dyn, st>>>(a, rx, ry, rz);
+        else k_step3d<RULE, false, false><<<grid, block, dyn, st>>>(a, rx, ry, rz);
     }
     return cudaGetLastError();
 }
