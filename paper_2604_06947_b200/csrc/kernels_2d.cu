@@ -21,6 +21,19 @@
 namespace fqnm {
 
 static constexpr unsigned FULL2 = 0xffffffffu;
+// resident CTAs per SM asked of ptxas (variant sweeps only): unset = __launch_bounds__(256)
+// with no minimum, which measured fastest -- a minimum of 1 alone changes the register
+// allocation of the k = 2 kernel and costs 23 % (8192^2 EO 892 -> 687 GCUPS), 3 spills
+#if defined(FQNM_K9_MINB1)
+#define K9_LB1 __launch_bounds__(256, FQNM_K9_MINB1)
+#else
+#define K9_LB1 __launch_bounds__(256)
+#endif
+#if defined(FQNM_K9_MINB2)
+#define K9_LB2 __launch_bounds__(256, FQNM_K9_MINB2)
+#else
+#define K9_LB2 __launch_bounds__(256)
+#endif
 #ifndef FQNM_K9_V
 #define FQNM_K9_V 4
 #endif
@@ -180,7 +193,7 @@ __device__ __forceinline__ void update_row(const Row2<RULE, SAME>& B, const Row2
 }
 
 template <int RULE, bool SAME>
-__global__ void __launch_bounds__(256) k_step2d_s(Step2DArgs a, DevRule rx, DevRule ry)
+__global__ void K9_LB1 k_step2d_s(Step2DArgs a, DevRule rx, DevRule ry)
 {
     constexpr int V = K9_V;
     const int lane = threadIdx.x & 31;
@@ -262,7 +275,7 @@ __global__ void __launch_bounds__(256) k_step2d_s(Step2DArgs a, DevRule rx, DevR
 // end.  Transmissive walls: the boundary transfer of every step uses the edge cell's
 // own maps (ghost copy, reading A12), as the clamped halo no longer carries it.
 template <int RULE, bool SAME>
-__global__ void __launch_bounds__(256) k_step2d_s2(Step2DArgs a, DevRule rx, DevRule ry)
+__global__ void K9_LB2 k_step2d_s2(Step2DArgs a, DevRule rx, DevRule ry)
 {
     constexpr int V = K9_V, L = K9_LOOK;
     const int lane = threadIdx.x & 31;
