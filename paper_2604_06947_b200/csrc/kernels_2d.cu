@@ -29,10 +29,14 @@ static constexpr unsigned FULL2 = 0xffffffffu;
 #else
 #define K9_LB1 __launch_bounds__(256)
 #endif
+// k = 2 kernel: a minimum of 2 for the EO rules (8192^2 EO 894 -> 920 GCUPS; linear
+// 871 -> 864 with it, so none there; a minimum of 0 is the same as none)
+template <int RULE>
+constexpr int k9_minb2() { return (RULE == R_EO_P1 || RULE == R_EO_FAST) ? 2 : 0; }
 #if defined(FQNM_K9_MINB2)
 #define K9_LB2 __launch_bounds__(256, FQNM_K9_MINB2)
 #else
-#define K9_LB2 __launch_bounds__(256)
+#define K9_LB2 __launch_bounds__(256, k9_minb2<RULE>())
 #endif
 #ifndef FQNM_K9_V
 #define FQNM_K9_V 4
