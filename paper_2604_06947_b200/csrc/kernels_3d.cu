@@ -304,10 +304,19 @@ static cudaError_t step3d_rule(bool same, const Step3DArgs& a0, const DevRule& r
 int64_t step3d_zchunk(int64_t nx, int64_t ny, int64_t nz)
 {
     const int64_t tiles = ((nx + K8_TX - 1) / K8_TX) * ((ny + K8_TY - 1) / K8_TY);
-    int64_t zc = tiles * nz / (148 * 12);                  // ~12 CTAs per SM in total
+#ifndef FQNM_K8_CTAS_PER_SM
+#define FQNM_K8_CTAS_PER_SM 12
+#endif
+#ifndef FQNM_K8_ZMAX
+#define FQNM_K8_ZMAX 128
+#endif
+    int64_t zc = tiles * nz / (148 * FQNM_K8_CTAS_PER_SM);   // ~12 CTAs per SM in total
     if (zc < 16) zc = 16;
-    if (zc > 128) zc = 128;
-    return zc < nz ? zc : nz;
+    if (zc > FQNM_K8_ZMAX) zc = FQNM_K8_ZMAX;
+    if (zc >= nz) return nz;
+    // equal chunks (no short last chunk: 512 planes in chunks of 73 left one of 1 plane)
+    const int64_t nch = (nz + zc - 1) / zc;
+    return (nz + nch - 1) / nch;
 }
 
 cudaError_t launch_step3d(int rule, bool same, const Step3DArgs& a, const DevRule& rx,
