@@ -381,10 +381,18 @@ cudaError_t launch_step2d_stream2(int rule, bool same, const Step2DArgs& a, cons
 int64_t step2d_stream_rows(int64_t nx, int64_t ny)
 {
     const int64_t strips = (nx + K9_S - 1) / K9_S;
-    int64_t yc = strips * ny / (148 * 48);                 // ~48 warps per SM in total
+#ifndef FQNM_K9_WARPS_PER_SM
+#define FQNM_K9_WARPS_PER_SM 48
+#endif
+    int64_t yc = strips * ny / (148 * FQNM_K9_WARPS_PER_SM);   // ~48 warps per SM in total
     if (yc < 8) yc = 8;
     if (yc > 512) yc = 512;
-    return yc < ny ? yc : ny;
+    if (yc >= ny) return ny;
+#ifndef FQNM_K9_RAGGED
+    const int64_t nch = (ny + yc - 1) / yc;                // equal chunks, no short tail
+    yc = (ny + nch - 1) / nch;
+#endif
+    return yc;
 }
 
 template <int RULE>
