@@ -97,3 +97,18 @@ def test_3d_argument_checks(F):
     plan = F.fqnm_plan_3d(4, 4, 4, 1e-3, 0.5, 0.5, 0.5)
     with pytest.raises(F.FqnmError):
         F.fqnm_debug_override(plan, 2)
+
+
+@pytest.mark.parametrize("case", [1, 3])
+@pytest.mark.parametrize("boundary", [W.PERIODIC, W.TRANSMISSIVE])
+def test_3d_many_z_chunks(F, case, boundary):
+    """A deep z extent (several equal z chunks per tile column, step3d_zchunk) with a
+    partial last tile column in x and a partial last tile row in y, against the oracle."""
+    kind, d, lams, params, amp, off = RULES3D[case]
+    shape = (150, 17, 130)
+    q0 = _field(np.random.default_rng(77 + case), *shape, amp, off)
+    ref = oracle.Rule3D(kind, d, *lams, params=params).run(q0, 3, boundary)
+    plan = _plan(F, case, shape, boundary)
+    q = torch.tensor(q0, dtype=torch.int32, device=DEV)
+    F.fqnm_step(plan, q, 3)
+    assert np.array_equal(q.cpu().numpy().astype(np.int64), ref)
