@@ -1060,6 +1060,11 @@ cudaError_t blocked_v(const BlockedArgs& a, const DevRule& r, cudaStream_t st, i
     return cudaGetLastError();
 }
 
+#ifndef FQNM_BLOCKED_MINB0
+#define FQNM_BLOCKED_MINB0 0      // launch-bounds minimum of the uncapped (minb = 0) variants:
+                                  // none (exact two-point EO2 132 vs 124 GCUPS with 1, LF 65.6 vs
+                                  // 65.1, generic linear 194 vs 195; tools/sweep_generic.py)
+#endif
 // minb: __launch_bounds__ min blocks per SM (register cap), 0 = default
 template <int RULE>
 cudaError_t blocked_rule(int V, int minb, const BlockedArgs& a, const DevRule& r,
@@ -1072,9 +1077,9 @@ cudaError_t blocked_rule(int V, int minb, const BlockedArgs& a, const DevRule& r
         if (V == 8 && minb == 4) return blocked_v<RULE, 8, 4>(a, r, st, cap);
     }
     switch (V) {
-        case 8: return blocked_v<RULE, 8, 1>(a, r, st, cap);
-        case 16: return blocked_v<RULE, 16, 1>(a, r, st, cap);
-        case 32: return blocked_v<RULE, 32, 1>(a, r, st, cap);
+        case 8: return blocked_v<RULE, 8, FQNM_BLOCKED_MINB0>(a, r, st, cap);
+        case 16: return blocked_v<RULE, 16, FQNM_BLOCKED_MINB0>(a, r, st, cap);
+        case 32: return blocked_v<RULE, 32, FQNM_BLOCKED_MINB0>(a, r, st, cap);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -1088,12 +1093,12 @@ template cudaError_t blocked_rule<R_EO_FAST>(int, int, const BlockedArgs&, const
 template cudaError_t blocked_rule<R_EO_P1>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
 #endif
 #if FQNM_PART(8)
-template cudaError_t blocked_v<R_GENERIC, 32, 1>(const BlockedArgs&, const DevRule&, cudaStream_t, int);
+template cudaError_t blocked_v<R_GENERIC, 32, FQNM_BLOCKED_MINB0>(const BlockedArgs&, const DevRule&, cudaStream_t, int);
 template cudaError_t blocked_v<R_GENERIC, 32, 2>(const BlockedArgs&, const DevRule&, cudaStream_t, int);
 #endif
 #if FQNM_PART(6)
 #if FQNM_SCALAR_PART == 6
-extern template cudaError_t blocked_v<R_GENERIC, 32, 1>(const BlockedArgs&, const DevRule&, cudaStream_t, int);
+extern template cudaError_t blocked_v<R_GENERIC, 32, FQNM_BLOCKED_MINB0>(const BlockedArgs&, const DevRule&, cudaStream_t, int);
 extern template cudaError_t blocked_v<R_GENERIC, 32, 2>(const BlockedArgs&, const DevRule&, cudaStream_t, int);
 #endif
 template cudaError_t blocked_rule<R_GENERIC>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
@@ -1109,8 +1114,8 @@ cudaError_t blocked_rule<R_TWOPOINT>(int V, int minb, const BlockedArgs& a, cons
                                      cudaStream_t st, int cap)
 {
     if (minb) return cudaErrorInvalidValue;
-    if (V == 8) return blocked_v<R_TWOPOINT, 8, 1>(a, r, st, cap);
-    if (V == 16) return blocked_v<R_TWOPOINT, 16, 1>(a, r, st, cap);
+    if (V == 8) return blocked_v<R_TWOPOINT, 8, FQNM_BLOCKED_MINB0>(a, r, st, cap);
+    if (V == 16) return blocked_v<R_TWOPOINT, 16, FQNM_BLOCKED_MINB0>(a, r, st, cap);
     return cudaErrorInvalidValue;
 }
 #endif
