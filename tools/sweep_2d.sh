@@ -1,3 +1,4 @@
+# K9 variant sweep: usage bash tools/sweep_2d.sh tag1 tag2 ... (variants/libfqnm_<tag>.so)
 # K9 variant sweep: default (k = 2) and k = 1 on 8192^2 EO / linear for each variant lib
 B=variants
 for rep in 1 2; do for v in "$@"; do
