@@ -675,8 +675,16 @@ struct ResidentArgs {
     uint32_t tag_base;
 };
 
+// launch-bounds minimum of K6: 1 for the two-point Godunov fast path (cfg2 data 166 -> 191
+// GCUPS), none for the rest (EO cfg2 371 with none, 358 with 1); -1 = this per-rule choice
+#ifndef FQNM_K6_MINB
+#define FQNM_K6_MINB -1
+#endif
+template <int RULE>
+constexpr int k6_minb() { return FQNM_K6_MINB >= 0 ? FQNM_K6_MINB : (RULE == R_TP_FAST ? 1 : 0); }
+
 template <int RULE, int V>
-__global__ void __launch_bounds__(256) k_resident(ResidentArgs a, DevRule r)
+__global__ void __launch_bounds__(256, k6_minb<RULE>()) k_resident(ResidentArgs a, DevRule r)
 {
     const int lane = threadIdx.x & 31;
     const int w = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
