@@ -915,8 +915,11 @@ cudaError_t launch_step2d(int rule, bool same, const Step2DArgs& a, const DevRul
 
 // ---------------------------------------------------------------------------
 // K3: one problem of 32*V cells per warp, all steps in registers
+#ifndef FQNM_K3_MINB
+#define FQNM_K3_MINB 0                    // launch-bounds minimum of K3 (0 = none)
+#endif
 template <int RULE, int V, bool WALL>
-__global__ void __launch_bounds__(128) k_warp_ensemble(int32_t* __restrict__ q, int64_t batch,
+__global__ void __launch_bounds__(128, FQNM_K3_MINB) k_warp_ensemble(int32_t* __restrict__ q, int64_t batch,
                                                         int64_t nsteps, DevRule r)
 {
     constexpr int N = 32 * V;
