@@ -1,24 +1,32 @@
 #!/usr/bin/env python
-"""FQNM bench: integer cell-updates/s of the B200 stepper on BASELINE.json's
-single-domain Burgers configuration (BJ.cfg4: N = 2^31 cells, int32, EO split,
-delta = 1e-6, Courant 0.4, 1000 time steps), split contiguously across the
-ranks for N > 1 GPUs (strong scaling: total work fixed).
+"""FQNM bench: integer cell-updates/s of the B200 stepper.
 
-One bench "step" = one pass of the whole hot path over the workload: the
-1000 explicit time steps of cfg4 (every row of SURVEY §8(a): plan constants,
-staging, map evaluation, interface transfer, update, temporal blocks, write
-back, halo exchange for N > 1), continuing from the previous state.
+Workloads (`--workload`):
+  cfg4 (default, the headline)  BASELINE.json's single-domain Burgers configuration
+        (BJ.cfg4: N = 2^31 cells, int32, EO split, delta = 1e-6, Courant 0.4, 1000 time
+        steps per bench step), split contiguously across the ranks for N > 1 GPUs
+        (strong scaling: total work fixed; one k-deep halo exchange per temporal block).
+  ens1  SURVEY §8(d)-D2 ENS-1, the north star's batched-ensemble mode: 2^16 independent
+        cfg1-like problems (1024 cells, linear kappa = 1/2, 2000 time steps) PER GPU;
+        rank r owns problems [r B, (r+1) B) of a P B-problem ensemble, no data-path
+        collective (weak scaling, SURVEY §8(e) "Ensembles").
 
-Contract (see task): W >= 3 warm-up steps, K timed steps bracketed by a
-barrier + synchronize on both sides, CUDA-event time on the launching stream,
-max over ranks, one JSON line from rank 0.  `--impl reference` times the CPU
-oracle (the paper has no reference implementation) on a bounded sample.
+One bench "step" = one pass of the whole hot path over the workload (every row of
+SURVEY §8(a): plan constants, staging, map evaluation, interface transfer, update,
+temporal blocks, write back, halo exchange for N > 1), continuing from the previous
+state.
+
+Contract (see task): W >= 3 warm-up steps, K timed steps bracketed by a barrier +
+synchronize on both sides, CUDA-event time on the launching stream, max over ranks, one
+JSON line from rank 0.  Every run is then verified against the CPU oracle (parity
+windows / sampled problems, bit-exact) and by whole-state invariants, at any N.
+`--impl reference` times the CPU oracle (the paper has no reference implementation) on
+a bounded sample.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -44,6 +52,7 @@ OPS_ALG = {"burgers_eo": 10, "burgers_eo_general_p": 11, "linear": 4}
 RULE_NAMES = {1: "LIN_HALF", 2: "EO_FAST", 3: "GENERIC", 4: "LIN_FAST", 5: "EO_P1"}
 SM_COUNT = 148
 LANES_PER_SM_CLK = 128                          # 4 SMSPs x 32 lanes, 1 warp-instr/clk each
+WINDOW = 2048                                   # cells per parity window
 
 
 def _peaks():
@@ -53,6 +62,17 @@ def _peaks():
         return mp, "measured"
     except Exception:
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def _micro_peaks():
+    """Per-pipe issue rates measured on a B200 by tools/micro.py (committed under
+    profiles/*_micro.json): lane-operations per second at the clock they ran at."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_micro.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as f:
+        return json.load(f), os.path.relpath(files[-1], ROOT)
 
 
 class Clocks:
@@ -122,7 +142,7 @@ def ncu_traffic(n_local: int):
         return None, None
     with open(files[-1]) as f:
         cap = json.load(f)
-    scale = n_local / float(1 << 31)           # the capture is of the N = 2^31 bench launch
+    scale = n_local / float(cap.get("n_cells", 1 << 31))
     return cap["dram_bytes_per_launch"] * scale, os.path.relpath(files[-1], ROOT)
 
 
@@ -132,65 +152,87 @@ def init_dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
     if world > 1:
-        torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(local)
     return rank, world, local
 
 
-def cpu_oracle_rate(q_sample: np.ndarray, qmax: int, target_s: float = 12.0):
-    """The oracle as it stands, on host cores, on a bounded periodic slice of cfg4."""
+def host_cpu():
+    """Host CPU model and sockets (lscpu), for the oracle timing context."""
+    info = {"model": None, "sockets": None, "affinity_cores": len(os.sched_getaffinity(0))}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() == "Model name":
+                info["model"] = v.strip()
+            elif k.strip() == "Socket(s)":
+                info["sockets"] = int(v.strip()) if v.strip().isdigit() else v.strip()
+    except Exception:
+        pass
+    return info
+
+
+def time_oracle(run, cells: int, target_s: float):
+    """Cell-updates/s of run(steps) on `cells` cells, sized to about target_s seconds."""
+    t = time.perf_counter()
+    run(2)
+    dt = max(time.perf_counter() - t, 1e-6)
+    steps = max(2, int(target_s / (dt / 2)))
+    t = time.perf_counter()
+    run(steps)
+    dt = time.perf_counter() - t
+    return cells * steps / dt / 1e9, steps, dt
+
+
+def cpu_baseline_cfg4(qmax: int):
+    """The oracle as it stands on the host: all cores (OpenMP) on a periodic 2^20-cell slice
+    of cfg4 and one thread on a 2^17-cell slice."""
     import oracle
     import workloads as W
     w = W.cfg("cfg4")
     rule = oracle.Rule(oracle.BURGERS_EO, w.delta, W.dt_dx(w, qmax))
-    n = len(q_sample)
-    t = time.perf_counter()
-    rule.run(q_sample, 2)
-    dt = max(time.perf_counter() - t, 1e-6)
-    steps = max(2, int(target_s / (dt / 2)))
-    t = time.perf_counter()
-    rule.run(q_sample, steps)
-    dt = time.perf_counter() - t
-    return n * steps / dt / 1e9, steps, dt, oracle.max_threads()
+    qa = W.q0_cfg4(n=w.n, count=1 << 20).numpy().astype(np.int64)
+    q1 = qa[:1 << 17].copy()
+    rate, steps, secs = time_oracle(lambda s: rule.run(qa, s), qa.size, 12.0)
+    rate1, steps1, secs1 = time_oracle(lambda s: rule.run(q1, s, nthreads=1), q1.size, 5.0)
+    return {"value": rate, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+            "sample": f"periodic cfg4 slice of 2^20 cells x {steps} time steps ({secs:.1f} s)",
+            "one_thread": {"value": rate1, "unit": UNIT,
+                           "sample": f"2^17 cells x {steps1} time steps ({secs1:.1f} s)"},
+            "host": host_cpu()}
 
 
-def state_invariants(q, chunk=1 << 28):
-    """Sum (int64), min, max and periodic total variation of a 1-D int32 CUDA state,
-    by plain torch reductions in chunks (independent of the FQNM kernels)."""
-    import torch
-    n = q.numel()
-    tot, mn, mx, tv = 0, None, None, 0
-    for i in range(0, n, chunk):
-        c = q[i:i + chunk]
-        tot += int(c.sum(dtype=torch.int64))
-        cmin, cmax = int(c.min()), int(c.max())
-        mn = cmin if mn is None else min(mn, cmin)
-        mx = cmax if mx is None else max(mx, cmax)
-        j = min(i + chunk + 1, n)
-        seg = q[i:j].to(torch.int64)
-        tv += int((seg[1:] - seg[:-1]).abs().sum())
-    tv += abs(int(q[0]) - int(q[n - 1]))
-    return {"sum": tot, "min": mn, "max": mx, "tv": tv}
-
-
+# ---------------------------------------------------------------------------
+# --impl reference: the CPU oracle (rank 0 only)
 def run_reference(args):
-    """--impl reference: the CPU oracle timed on host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     import oracle
     import workloads as W
-    import torch
-    w = W.cfg("cfg4")
-    n_sample = 1 << 20
-    q = W.q0_cfg4(n=w.n, count=n_sample).numpy().astype(np.int64)
-    qmax = 344848                      # max |q0| of cfg4 (the GPU arm's kappa = 1/(5 Q_max) = 1/1724240)
-    rule = oracle.Rule(oracle.BURGERS_EO, w.delta, W.dt_dx(w, qmax))
-    steps_per = 1000                   # the time steps of one cfg4 bench step
+    cores = oracle.max_threads()
+    if args.workload == "ens1":
+        w = W.cfg("ens1")
+        B = 64                               # problems per sample (the GPU arm: 2^16 per GPU)
+        q = W.q0_ensemble(1 << 16, n=w.n, count=B).astype(np.int64)
+        rule = oracle.Rule(oracle.LINEAR, w.delta, W.dt_dx(w))
+        steps_per = w.steps
+        cells = B * w.n
+        sample = f"ens1: {B} of the 2^16 problems x {w.n} cells x {steps_per} time steps per bench step"
+        config = {"workload": "ens1", "sample_problems": B, "n_cells": w.n,
+                  "time_steps_per_step": steps_per}
+    else:
+        w = W.cfg("cfg4")
+        cells = 1 << 20
+        q = W.q0_cfg4(n=w.n, count=cells).numpy().astype(np.int64)
+        qmax = 344848                  # max |q0| of cfg4 (the GPU arm's kappa = 1/(5 Q_max) = 1/1724240)
+        rule = oracle.Rule(oracle.BURGERS_EO, w.delta, W.dt_dx(w, qmax))
+        steps_per = 1000                   # the time steps of one cfg4 bench step
+        sample = f"cfg4 slice of {cells} cells x {steps_per} time steps per bench step (periodic)"
+        config = {"workload": "cfg4", "sample_cells": cells, "time_steps_per_step": steps_per}
     for _ in range(args.warmup):
         q = rule.run(q, 1)
     times = []
@@ -199,42 +241,96 @@ def run_reference(args):
         q = rule.run(q, steps_per)
         times.append(time.perf_counter() - t)
     tot = sum(times)
-    val = n_sample * steps_per * args.steps / tot / 1e9
-    cores = oracle.max_threads()
-    sample = f"cfg4 slice of {n_sample} cells x {steps_per} time steps per bench step (periodic)"
+    val = cells * steps_per * args.steps / tot / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
-            "data": "synthetic", "config": {"workload": "cfg4", "sample_cells": n_sample,
-                                             "time_steps_per_step": steps_per},
+            "higher_is_better": True, "scaling": "weak" if args.workload == "ens1" else "strong",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic", "config": config,
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "host": host_cpu()},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="fqnm", choices=["fqnm", "reference"])
-    ap.add_argument("--n", type=int, default=1 << 31, help="cells (default: BJ.cfg4 2^31)")
-    ap.add_argument("--time-steps", type=int, default=1000, help="time steps per bench step")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-parity", action="store_true")
-    ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"],
-                    help="N > 1: fused peer-memory halo exchange inside the kernel (p2p) "
-                         "or torch.distributed NCCL send/recv between launches")
-    args = ap.parse_args()
-    if args.impl == "reference":
-        return run_reference(args)
-
+# ---------------------------------------------------------------------------
+def timed(do_step, args, world, local, plan, stepper_plans):
+    """W untimed warm-up steps, then exactly K steps between barrier + sync, CUDA events
+    on the launching stream; device time max over ranks."""
     import torch
     import torch.distributed as dist
     import paper_2604_06947_b200 as F
-    from paper_2604_06947_b200 import halo
+    for _ in range(max(args.warmup, 0)):
+        do_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    launches0 = sum(p.launches() for p in stepper_plans)
+    F.fqnm_profile_enable(plan, True)
+    F.fqnm_profile_read(plan)                  # reset accumulators
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        do_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    kern_ms, kern_launches = F.fqnm_profile_read(plan)
+    F.fqnm_profile_enable(plan, False)
+    launches = sum(p.launches() for p in stepper_plans) - launches0
+    dev = torch.device("cuda", local)
+    t = torch.tensor([ms, kern_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t[0]), float(t[1]), kern_ms, kern_launches, launches, clk, ms
+
+
+def alu_roofline(kernel: str, ops_alg: int, updates_per_launch: float, per_launch_ms: float,
+                 hbm_bytes_per_launch: float, extra: dict):
+    peaks, peak_src = _peaks()
+    f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    peak_ops = SM_COUNT * LANES_PER_SM_CLK * f_max                    # int lane-ops/s at max clock
+    achieved_ops = ops_alg * updates_per_launch / (per_launch_ms / 1e3)
+    roof = {
+        "bound": "alu", "kernel": kernel,
+        "achieved": achieved_ops / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s",
+        "frac": achieved_ops / peak_ops,
+        "ops_alg_per_cell_update": ops_alg,
+        "peak_basis": "148 SMs x 128 int lanes/clk x sm_max_mhz (%s)" % peak_src,
+        "traffic": None, "traffic_source": None,
+        "algorithmic_bytes_per_launch": hbm_bytes_per_launch,
+        "kernel_ms_per_launch": per_launch_ms,
+        "hbm_achieved_gbs": hbm_bytes_per_launch / (per_launch_ms / 1e3) / 1e9,
+        "hbm_peak_gbs": float(peaks.get("hbm_gbs", 6650.0)),
+    }
+    roof.update(extra)
+    micro, src = _micro_peaks()
+    if micro:
+        # the same achieved rate against the issue rate measured on a B200 by
+        # microbenchmarks (the mixed ALU + FMA integer stream, scaled to sm_max_mhz)
+        m = micro.get("mixed_alu_fma_int", {})
+        if m.get("lane_ops_per_clk_per_sm"):
+            mp = m["lane_ops_per_clk_per_sm"] * SM_COUNT * f_max
+            roof["measured_issue_peak"] = mp / 1e12
+            roof["frac_vs_measured_issue_peak"] = achieved_ops / mp
+            roof["measured_peak_source"] = src
+    return roof
+
+
+# ---------------------------------------------------------------------------
+def run_cfg4(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2604_06947_b200 as F
+    from paper_2604_06947_b200 import checks, halo
     import workloads as W
 
     rank, world, local = init_dist()
@@ -244,6 +340,7 @@ def main():
     N = args.n
     T = args.time_steps
     off, n_local = halo.partition(N, world, rank)
+    offsets = [halo.partition(N, world, r)[0] for r in range(world)]
 
     # ---- inputs (seeded, synthetic, generated on the device; D5) ----
     q = W.q0_cfg4(n=N, offset=off, count=n_local, device=dev)
@@ -252,21 +349,24 @@ def main():
         dist.all_reduce(qmax_t, op=dist.ReduceOp.MAX)
     qmax = int(qmax_t)
     dt_dx = W.dt_dx_double(w, qmax)           # Courant 0.4 with alpha = delta max|q0| (A3)
+    # invariants of the initial state (independent torch reductions, all ranks)
+    inv0 = checks.invariants(q)
 
     # ---- plan (the public C-ABI entry points) ----
+    ring = sd = None
     if world == 1:
         plan = F.fqnm_plan(N, 1e-6, dt_dx, F.BURGERS_EO, F.PERIODIC)     # north-star signature
         info = plan.info()
-        k = info["k"]
 
         def do_step():
             F.fqnm_step(plan, q, T)
-        stepper_plans = [plan]
+
+        def owned():
+            return q
     else:
         probe = F.fqnm_plan_validate(N, 1e-6, dt_dx, F.BURGERS_EO)
         k = probe["k"]
         halo_mode = args.halo
-        ring = None
         if halo_mode == "p2p":
             ring, why = halo.P2PRing.distributed(
                 lambda: F.fqnm_plan_ex(n_local, 1e-6, dt_dx, F.BURGERS_EO, F.HALO, halo=k,
@@ -296,82 +396,34 @@ def main():
                 ring.step(T)
             else:
                 sd.step(T)
-        stepper_plans = [plan]
 
-    # invariants of the initial state (independent torch reductions)
-    inv0 = state_invariants(q) if world == 1 else None
-
-    # ---- warm-up ----
-    for _ in range(max(args.warmup, 0)):
-        do_step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-
-    # ---- timed region ----
-    clocks = Clocks(local)
-    launches0 = sum(p.launches() for p in stepper_plans)
-    F.fqnm_profile_enable(plan, True)
-    F.fqnm_profile_read(plan)                  # reset accumulators
-    stream = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks.start()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0.record(stream)
-    for _ in range(args.steps):
-        do_step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ms = e0.elapsed_time(e1)
-    clk = clocks.stop()
-    kern_ms, kern_launches = F.fqnm_profile_read(plan)
-    F.fqnm_profile_enable(plan, False)
-    launches = sum(p.launches() for p in stepper_plans) - launches0
-    t = torch.tensor([ms, kern_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max, kern_ms_max = float(t[0]), float(t[1])
-
+    ms_max, kern_ms_max, kern_ms, kern_launches, launches, clk, ms = timed(
+        do_step, args, world, local, plan, [plan])
     cell_updates = N * T * args.steps
     value = cell_updates / (ms_max / 1e3) / 1e9
 
     # ---- roofline of the dominant kernel (k_blocked, EO fast path) ----
-    peaks, peak_src = _peaks()
-    f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
-    peak_ops = SM_COUNT * LANES_PER_SM_CLK * f_max                    # int lane-ops/s at max clock
     per_launch_ms = kern_ms / max(kern_launches, 1)
     updates_per_launch = n_local * T * args.steps / max(kern_launches, 1)
     ops_alg = OPS_ALG["burgers_eo"] if info["rule"] == 5 else OPS_ALG["burgers_eo_general_p"]
-    achieved_ops = ops_alg * updates_per_launch / (per_launch_ms / 1e3)
     hbm_bytes_per_launch = 8.0 * n_local                               # read + write int32 once per block
-    roofline = {
-        "bound": "alu", "kernel": "k_blocked<%s,V=%d>" % (RULE_NAMES.get(info["rule"], "?"),
-                                                           info["cells_per_thread"]),
-        "achieved": achieved_ops / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s",
-        "frac": achieved_ops / peak_ops,
-        "ops_alg_per_cell_update": ops_alg,
-        "peak_basis": "148 SMs x 128 int lanes/clk x sm_max_mhz (%s)" % peak_src,
-        "traffic": None,
-        "traffic_source": None,
-        "algorithmic_bytes_per_launch": hbm_bytes_per_launch,
-        "kernel_ms_per_launch": per_launch_ms, "kernel_launches": kern_launches,
-        "kernel_share_of_step": kern_ms / ms if ms > 0 else None,
-        "hbm_achieved_gbs": hbm_bytes_per_launch / (per_launch_ms / 1e3) / 1e9,
-        "hbm_peak_gbs": float(peaks.get("hbm_gbs", 6650.0)),
-        "k": info["k"], "V": info["cells_per_thread"],
-    }
-
+    roofline = alu_roofline(
+        "k_blocked<%s,V=%d>" % (RULE_NAMES.get(info["rule"], "?"), info["cells_per_thread"]),
+        ops_alg, updates_per_launch, per_launch_ms, hbm_bytes_per_launch,
+        {"kernel_launches": kern_launches, "kernel_share_of_step": kern_ms / ms if ms > 0 else None,
+         "k": info["k"], "V": info["cells_per_thread"]})
     tr, tr_src = ncu_traffic(n_local)
     if tr is not None:
         roofline["traffic"] = tr
         roofline["traffic_source"] = tr_src
         roofline["traffic_over_algorithmic"] = tr / hbm_bytes_per_launch
 
-    inv1 = state_invariants(q) if world == 1 else None
+    # ---- verification of the benchmarked state (every run, any N) ----
+    total = T * (args.warmup + args.steps)
+    parity = None
+    if not args.no_parity:
+        parity = verify_cfg4(args, owned(), off, n_local, N, offsets, total, qmax, inv0, dev, world,
+                             rank)
 
     # ---- end-to-end through the public API with host buffers (H2D + steps + D2H) ----
     e2e = None
@@ -379,7 +431,7 @@ def main():
         if world == 1:
             qh = torch.empty(N, dtype=torch.int32, pin_memory=True)
             qh.copy_(q.cpu())
-            F.fqnm_step_host(plan, qh, T)              # warm (allocates the e2e buffer)
+            F.fqnm_step_host(plan, qh, T)              # warm (allocates the e2e pipeline)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             for _ in range(args.steps):
@@ -404,43 +456,10 @@ def main():
             e2e = {"value": N * T * args.steps / float(tt) / 1e9, "unit": UNIT,
                    "h2d_bytes_per_step": 4 * N, "d2h_bytes_per_step": 4 * N}
 
-    # ---- parity spot check (light-cone windows vs the oracle; rank 0) ----
-    parity = None
-    if rank == 0 and not args.no_parity and world == 1:
-        try:
-            import oracle
-            total = T * (args.warmup + args.steps)
-            parity = {"checked_windows": 0, "ok": True, "time_steps": total}
-            if total <= 20000:
-                rule = oracle.Rule(oracle.BURGERS_EO, w.delta, W.dt_dx(w, qmax))
-                for a in (0, N // 3, N - 2048):
-                    a = (a // 4) * 4
-                    lo, hi = a - total, a + 2048 + total
-                    qin = W.q0_cfg4_at(np.arange(lo, hi) % N, n=N, device=dev)
-                    ref = rule.run(qin, total)[total:total + 2048]
-                    got = q[a:a + 2048].cpu().numpy()
-                    parity["checked_windows"] += 1
-                    parity["ok"] &= bool(np.array_equal(ref, got))
-        except Exception as ex:       # never let the spot check kill the bench line
-            parity = {"ok": None, "error": str(ex)[:200]}
-        if inv0 is not None and inv1 is not None:
-            # exact conservation, maximum principle and TVD of the whole 2^31-cell state
-            # after warm-up + timed steps (Lemma P:197-238, Thm conservation)
-            parity["invariants"] = {
-                "sum_conserved": inv1["sum"] == inv0["sum"],
-                "max_principle": inv1["min"] >= inv0["min"] and inv1["max"] <= inv0["max"],
-                "tv_nonincreasing": inv1["tv"] <= inv0["tv"],
-                "initial": inv0, "final": inv1}
-            parity["ok"] = bool(parity["ok"]) and all(
-                parity["invariants"][k] for k in ("sum_conserved", "max_principle", "tv_nonincreasing"))
-
     # ---- CPU baseline (oracle on host cores; rank 0, N = 1 only) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        sample = W.q0_cfg4(n=N, count=1 << 20).numpy().astype(np.int64)
-        rate, steps_c, secs, cores = cpu_oracle_rate(sample, qmax)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"periodic cfg4 slice of 2^20 cells x {steps_c} time steps ({secs:.1f} s)"}
+        cpu = cpu_baseline_cfg4(qmax)
 
     if rank == 0:
         line = {
@@ -460,6 +479,191 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def verify_cfg4(args, q, off, n_local, N, offsets, total, qmax, inv0, dev, world, rank):
+    """Bit-exact light-cone windows vs the oracle (wrap, every split point, middle, random;
+    SURVEY §8(c)-C6, §8(e)), whole-domain invariants before/after (with the cross-rank
+    edge pairs), and the number of cells the run changed.  Collective over the ranks;
+    the oracle runs on rank 0."""
+    import torch
+    import torch.distributed as dist
+    from paper_2604_06947_b200 import checks
+    import workloads as W
+    out = {"time_steps": total, "checked_windows": 0, "ok": True}
+    try:
+        inv1 = checks.invariants(q)
+        changed = checks.changed_cells(
+            q, lambda i, m: W.q0_cfg4(n=N, offset=off + i, count=m, device=dev))
+        starts = checks.window_starts(N, offsets, WINDOW, n_random=1, seed=args.seed)
+        got = checks.gather_windows(q, off, N, starts, WINDOW).cpu().numpy()
+        if rank == 0:
+            import oracle
+            w = W.cfg("cfg4")
+            rule = oracle.Rule(oracle.BURGERS_EO, w.delta, W.dt_dx(w, qmax))
+            mism = []
+            t0 = time.perf_counter()
+            for i, a in enumerate(starts):
+                # dependence cone: `total` cells on each side; the oracle's periodic wrap
+                # inside the window buffer only corrupts cells outside [total, total + W)
+                idx = np.arange(a - total, a + WINDOW + total)
+                qin = W.q0_cfg4_at(idx % N, n=N, device=dev)
+                ref = rule.run(qin, total)[total:total + WINDOW]
+                out["checked_windows"] += 1
+                if not np.array_equal(ref, got[i]):
+                    mism.append({"start": int(a), "cells": int((ref != got[i]).sum())})
+            out["oracle_s"] = time.perf_counter() - t0
+            out["window_starts"] = [int(s) for s in starts]
+            out["window_cells"] = WINDOW
+            out["mismatches"] = mism
+            out["ok"] = not mism
+            out["cells_changed"] = changed
+            out["invariants"] = {
+                "sum_conserved": inv1["sum"] == inv0["sum"],
+                "max_principle": inv1["min"] >= inv0["min"] and inv1["max"] <= inv0["max"],
+                "tv_nonincreasing": inv1["tv"] <= inv0["tv"],
+                "initial": inv0, "final": inv1,
+                "tv_includes": "all adjacent pairs incl. %d cross-rank edges and the periodic wrap"
+                               % max(world - 1, 0)}
+            out["ok"] = bool(out["ok"]) and changed > 0 and all(
+                out["invariants"][k] for k in ("sum_conserved", "max_principle", "tv_nonincreasing"))
+    except Exception as ex:       # never let the check kill the bench line
+        out = {"ok": None, "error": repr(ex)[:300]}
+    if world > 1:
+        dist.barrier()
+    return out
+
+
+# ---------------------------------------------------------------------------
+def run_ens1(args):
+    """ENS-1: B = 2^16 independent cfg1-like problems per GPU (weak scaling)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2604_06947_b200 as F
+    from paper_2604_06947_b200 import shard
+    import workloads as W
+
+    rank, world, local = init_dist()
+    dev = torch.device("cuda", local)
+    w = W.cfg("ens1")
+    B = args.batch
+    Bt = B * world
+    n = w.n
+    T = args.time_steps if args.time_steps_set else w.steps
+    first, cnt = shard.ensemble_range(Bt, world, rank)   # [r B, (r+1) B): no communication
+    assert cnt == B
+    q0 = W.q0_ensemble(Bt, n=n, first=first, count=B)
+    q = torch.tensor(q0, dtype=torch.int32, device=dev).reshape(-1)
+    plan = F.fqnm_plan_ex(n, float(w.delta), W.dt_dx_double(w), F.LINEAR, F.PERIODIC, batch=B)
+    info = plan.info()
+
+    def do_step():
+        F.fqnm_step(plan, q, T)
+
+    ms_max, _, kern_ms, kern_launches, launches, clk, ms = timed(do_step, args, world, local,
+                                                                 plan, [plan])
+    value = Bt * n * T * args.steps / (ms_max / 1e3) / 1e9
+    per_launch_ms = kern_ms / max(kern_launches, 1)
+    updates_per_launch = B * n * T * args.steps / max(kern_launches, 1)
+    roofline = alu_roofline("k_warp_ensemble<LIN_HALF,V=%d>" % info["cells_per_thread"],
+                            OPS_ALG["linear"], updates_per_launch, per_launch_ms, 8.0 * B * n,
+                            {"kernel_launches": kern_launches,
+                             "kernel_share_of_step": kern_ms / ms if ms > 0 else None})
+
+    # ---- verification: sampled problems vs the oracle (bit-exact) + per-problem sums ----
+    total = T * (args.warmup + args.steps)
+    parity = None
+    if not args.no_parity:
+        parity = {"time_steps": total, "ok": True}
+        try:
+            import oracle
+            qv = q.view(B, n)
+            sums_ok = bool(torch.equal(qv.sum(1, dtype=torch.int64),
+                                       torch.tensor(q0, device=dev).sum(1)))
+            rng = np.random.default_rng(args.seed + rank)
+            pick = np.unique(np.concatenate([[0, B - 1], rng.integers(0, B, 30)]))
+            ref = oracle.Rule(oracle.LINEAR, w.delta, W.dt_dx(w)).run(q0[pick], total)
+            got = qv[torch.as_tensor(pick, device=dev)].cpu().numpy().astype(np.int64)
+            ok = bool(np.array_equal(ref, got)) and sums_ok
+            flag = torch.tensor([0 if ok else 1, len(pick)], dtype=torch.int64, device=dev)
+            if world > 1:
+                dist.all_reduce(flag)
+            parity.update(ok=int(flag[0]) == 0, checked_problems=int(flag[1]),
+                          per_problem_sums_conserved=sums_ok if world == 1 else None)
+        except Exception as ex:
+            parity = {"ok": None, "error": repr(ex)[:300]}
+
+    e2e = None
+    if not args.no_e2e:
+        qh = torch.empty(B * n, dtype=torch.int32, pin_memory=True)
+        qh.copy_(q.cpu())
+        F.fqnm_step_host(plan, qh, T)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            F.fqnm_step_host(plan, qh, T)
+        e2e_s = shard.max_over_ranks(time.perf_counter() - t0, dev)
+        e2e = {"value": Bt * n * T * args.steps / e2e_s / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": 4 * Bt * n, "d2h_bytes_per_step": 4 * Bt * n}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle
+        qs = q0[:64].astype(np.int64)
+        rule = oracle.Rule(oracle.LINEAR, w.delta, W.dt_dx(w))
+        rate, steps_c, secs = time_oracle(lambda s: rule.run(qs, s), qs.size, 10.0)
+        cpu = {"value": rate, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+               "sample": f"64 problems x {n} cells x {steps_c} time steps ({secs:.1f} s)",
+               "host": host_cpu()}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int32", "data": "synthetic",
+            "config": {"workload": "ens1", "problems": Bt, "problems_per_gpu": B, "n_cells": n,
+                       "time_steps_per_step": T, "flux": "linear", "kappa": [1, 2],
+                       "l2": "state %.0f MiB per GPU, HBM touched once per bench step "
+                             "(all time steps in registers)" % (4 * B * n / 2**20),
+                       "parallelism": "ensemble shard x%d (no data-path collective)" % world},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "gpu_launches": launches, "parity": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="fqnm", choices=["fqnm", "reference"])
+    ap.add_argument("--workload", default="cfg4", choices=["cfg4", "ens1"])
+    ap.add_argument("--n", type=int, default=1 << 31, help="cfg4 cells (default: BJ.cfg4 2^31)")
+    ap.add_argument("--batch", type=int, default=1 << 16, help="ens1 problems per GPU")
+    ap.add_argument("--time-steps", type=int, default=None,
+                    help="time steps per bench step (cfg4 1000, ens1 2000)")
+    ap.add_argument("--seed", type=int, default=0, help="seed of the random parity samples")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"],
+                    help="cfg4, N > 1: fused peer-memory halo exchange inside the kernel (p2p) "
+                         "or torch.distributed NCCL send/recv between launches")
+    args = ap.parse_args()
+    args.time_steps_set = args.time_steps is not None
+    if args.time_steps is None:
+        args.time_steps = 1000
+    if args.impl == "reference":
+        return run_reference(args)
+    if args.workload == "ens1":
+        return run_ens1(args)
+    return run_cfg4(args)
 
 
 if __name__ == "__main__":

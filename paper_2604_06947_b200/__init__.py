@@ -34,6 +34,7 @@ LINEAR, BURGERS_EO, BURGERS_LF, EULER_ROE, EULER_ROE_DENSITY = 0, 1, 2, 3, 4
 BURGERS_GODUNOV, BURGERS_EO2, BURGERS_LF2 = 5, 6, 7      # two-point rules (Thm P:262-280)
 PERIODIC, TRANSMISSIVE, HALO = 0, 1, 2
 I32, I64 = 0, 1
+ABI_VERSION = 2                                           # include/fqnm.h FQNM_ABI_VERSION
 ROUND_HALF_AWAY, ROUND_FLOOR, ROUND_HALF_EVEN = 0, 1, 2
 STATUS = {0: "FQNM_OK", 1: "FQNM_ERR_ARG", 2: "FQNM_ERR_CFL", 3: "FQNM_ERR_RANGE",
           4: "FQNM_ERR_CUDA", 5: "FQNM_ERR_UNSUPPORTED", 6: "FQNM_ERR_NOMEM"}
@@ -73,6 +74,7 @@ class PlanInfo(ctypes.Structure):
         ("rule", ctypes.c_int32), ("k", ctypes.c_int32), ("cells_per_thread", ctypes.c_int32),
         ("kernel", ctypes.c_int32), ("scratch_bytes", ctypes.c_int64),
         ("s_euler", ctypes.c_double), ("g1_euler", ctypes.c_double),
+        ("d8_lim", ctypes.c_int64),
     ]
 
     def as_dict(self):
@@ -394,13 +396,21 @@ def fqnm_observe(plan: Plan, q, u=None):
 
 
 def fqnm_step_host(plan: Plan, q_host, nsteps: int):
-    """End-to-end: host buffer (pinned torch CPU tensor or numpy array) stepped in place."""
+    """End-to-end: host buffer (pinned torch CPU tensor or numpy array) stepped in place.
+    The C side copies state_elems x sizeof(dtype) bytes into and out of the pointer, so the
+    buffer's element count and dtype are checked against the plan here."""
     L = _load()
+    want = _numel(plan)
+    is_i64 = plan.desc.dtype == I64
     try:
         import torch
         if isinstance(q_host, torch.Tensor):
             if q_host.is_cuda or not q_host.is_contiguous():
                 raise ValueError("q_host must be a contiguous CPU tensor")
+            if q_host.dtype != (torch.int64 if is_i64 else torch.int32):
+                raise TypeError(f"q_host must be {'int64' if is_i64 else 'int32'}, got {q_host.dtype}")
+            if q_host.numel() != want:
+                raise ValueError(f"q_host has {q_host.numel()} elements, plan expects {want}")
             ptr = ctypes.c_void_p(q_host.data_ptr())
             _check(L.fqnm_set_stream(plan.handle, _stream_ptr()))
             _check(L.fqnm_step_host(plan.handle, ptr, int(nsteps)))
@@ -411,6 +421,10 @@ def fqnm_step_host(plan: Plan, q_host, nsteps: int):
     a = q_host
     if not (isinstance(a, np.ndarray) and a.flags.c_contiguous):
         raise TypeError("q_host must be a contiguous numpy array or CPU tensor")
+    if a.dtype != (np.int64 if is_i64 else np.int32):
+        raise TypeError(f"q_host must be {'int64' if is_i64 else 'int32'}, got {a.dtype}")
+    if a.size != want:
+        raise ValueError(f"q_host has {a.size} elements, plan expects {want}")
     _check(L.fqnm_step_host(plan.handle, ctypes.c_void_p(a.ctypes.data), int(nsteps)))
     return a
 

@@ -19,11 +19,13 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", CSRC, "-I", INCLUDE]
+COMMON = ["-O3", "-lineinfo", "-std=c++17", "-diag-suppress", "177", "-Xcompiler", "-fPIC", "-I", CSRC, "-I", INCLUDE]
+# (object name, source, extra flags)
 UNITS = {
     "fqnm_api.cu": [],
-    # kernels_scalar.cu is compiled as 10 parts (separate translation units) in parallel
-    **{f"kernels_scalar_p{k}.cu": [] for k in range(1, 11)},
+    # kernels_scalar.cu is compiled as 10 parts (separate objects, -DFQNM_SCALAR_PART=k) in
+    # parallel: each part holds a subset of the launchers' template instantiations
+    **{f"kernels_scalar_p{k}.cu": [f"-DFQNM_SCALAR_PART={k}"] for k in range(1, 11)},
     "kernels_euler.cu": ["-fmad=false"],
     "kernels_diag.cu": [],
     "kernels_3d.cu": [],
@@ -49,7 +51,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False,
     objs = []
     cmds = []
     for unit, extra in UNITS.items():
-        src = os.path.join(CSRC, unit)
+        src = os.path.join(CSRC, "kernels_scalar.cu" if unit.startswith("kernels_scalar_p") else unit)
         obj = os.path.join(objdir, unit.replace(".cu", ".o"))
         objs.append(obj)
         if force or _stale(obj, src):

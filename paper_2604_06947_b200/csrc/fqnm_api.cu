@@ -95,7 +95,8 @@ static int64_t gcd64(int64_t a, int64_t b)
 }
 
 // exact rational nearest a positive or negative double: simplest convergent of
-// the exact continued fraction of x with den <= 2^31 and |x - p/q| <= 2^-48 |x|
+// the exact continued fraction of x with den <= 2^31 and |x - p/q| <= 2^-50 |x|
+// (a double product of the config's decimals is within 2^-52 of the exact rational)
 static bool rationalize(double x, int64_t* pnum, int64_t* pden)
 {
     if (!std::isfinite(x) || x == 0.0) return false;
@@ -125,10 +126,10 @@ static bool rationalize(double x, int64_t* pnum, int64_t* pden)
         h0 = h1; h1 = h2; k0 = k1; k1 = k2;
         i128 r = a - t * b;
         a = b; b = r;
-        // |num/den - h1/k1| <= 2^-48 num/den  <=>  |num k1 - h1 den| 2^48 <= num k1
+        // |num/den - h1/k1| <= 2^-50 num/den  <=>  |num k1 - h1 den| 2^50 <= num k1
         i128 diff = num * k1 - h1 * den;
         if (diff < 0) diff = -diff;
-        if (diff <= ((num * k1) >> 48)) {
+        if (diff <= ((num * k1) >> 50)) {
             if (h1 > INT64_MAX || k1 > INT64_MAX) return false;
             *pnum = neg ? -(int64_t)h1 : (int64_t)h1;
             *pden = (int64_t)k1;
@@ -153,6 +154,12 @@ struct fqnm_plan {
     int V = 0;
     int k = 0;
     int minb = 0;         // K2 register cap variant (0 = default)
+    // EO plans whose derived D8 range exceeds the fast closed form's domain: [lo, hi] is the
+    // fast domain and d8_lim the largest |q| D8 admits; a range-checked step whose state
+    // leaves [lo, hi] but stays within +-d8_lim runs on the exact int64 rule (child plan)
+    int64_t d8_lim = 0;
+    fqnm_plan_t* generic_child = nullptr;
+    bool trusted_range = false;         // declared range already D8-validated by the parent
     // Euler constants
     double s_e = 0, g1_e = 0;
     // memory
@@ -202,6 +209,8 @@ struct fqnm_plan {
     fqnm_plan_t* pipe_child = nullptr;
     int64_t pipe_H = 0, pipe_C = 0, pipe_m = 0;
     void* pipe_buf[3] = {nullptr, nullptr, nullptr};
+    int32_t* pipe_head = nullptr;        // copy of q_host[0, H) taken before any D2H (the last
+                                         // chunk's periodic right halo)
     int* pipe_guard = nullptr;           // one flag per chunk
     int* pipe_guard_host = nullptr;
     int64_t pipe_guard_n = 0;
@@ -214,7 +223,8 @@ struct fqnm_plan {
 };
 
 static void fill_info(const fqnm_plan_t* p, fqnm_plan_info* info);
-static int plan_build(fqnm_plan_t** out, const fqnm_plan_desc* din, bool allocate);
+static int plan_build(fqnm_plan_t** out, const fqnm_plan_desc* din, bool allocate,
+                      bool trusted_range = false);
 
 // K6 geometry: V = 8 (W = 256 cells per warp), H = round4(k) halo cells per side,
 // at most 1184 warps (one 256-thread CTA per SM: always co-resident)
@@ -263,6 +273,49 @@ static bool generic_headroom(const HostMap& m, int64_t a)
     i128 A = a;
     i128 num = (i128)(m.c2 < 0 ? -m.c2 : m.c2) * A * A + (i128)(m.c1 < 0 ? -m.c1 : m.c1) * A;
     return 2 * num + m.den < ((i128)1 << 62);
+}
+
+// Largest A such that D8 holds on [-A, A] (and the int64 generic path has headroom, and
+// A fits the int32 state); 0 if D8 fails already at |q| <= 1.
+// EO (c1 = 0, both maps |phi| = round(kappa q^2) on their half-lines): the increment
+// round(kappa (a+1)^2) - round(kappa a^2) of a monotone rounding is <= 1 whenever
+// kappa (2a + 1) < 1, so the scan starts at a0 = max{a : P (2a + 1) < Q} and only the part
+// beyond it (where increments of 2 first appear within ~1/(kappa(2a+1) - 1) steps) is walked.
+static int64_t d8_symmetric_limit(const fqnm_plan_t* p, bool eo)
+{
+    const int rd = p->d.rounding;
+    const int64_t cap = INT32_MAX - 1;
+    auto room = [&](int64_t a) { return generic_headroom(p->hp, a) && generic_headroom(p->hm, a); };
+    int64_t A = 0;
+    if (eo) {
+        const i128 P = p->kap_num, Q = p->kap_den;
+        i128 a0 = Q > P ? (Q - 1 - P) / (2 * P) : 0;
+        if (a0 > cap) a0 = cap;
+        A = (int64_t)a0;
+        if (!room(A)) {                                    // headroom binds first: bisect it
+            int64_t lo_ok = 0, hi_bad = A;
+            while (hi_bad - lo_ok > 1) {
+                const int64_t mid = lo_ok + (hi_bad - lo_ok) / 2;
+                (room(mid) ? lo_ok : hi_bad) = mid;
+            }
+            return lo_ok;
+        }
+    }
+    int64_t ppp = host_phi(p->hp, A, rd), pmp = host_phi(p->hm, A, rd);
+    int64_t ppn = host_phi(p->hp, -A, rd), pmn = host_phi(p->hm, -A, rd);
+    const int64_t stop = A + ((int64_t)1 << 24) < cap ? A + ((int64_t)1 << 24) : cap;
+    while (A < stop) {
+        const int64_t a1 = A + 1;
+        const int64_t pp1 = host_phi(p->hp, a1, rd), pm1 = host_phi(p->hm, a1, rd);
+        const int64_t ppm = host_phi(p->hp, -a1, rd), pmm = host_phi(p->hm, -a1, rd);
+        const int64_t dp = pp1 - ppp, dm = pm1 - pmp;            // step A -> A+1
+        const int64_t dpn = ppn - ppm, dmn = pmn - pmm;          // step -A-1 -> -A
+        if (dp < 0 || dm > 0 || dp - dm > 1 || dpn < 0 || dmn > 0 || dpn - dmn > 1) break;
+        if (!room(a1)) break;
+        ppp = pp1; pmp = pm1; ppn = ppm; pmn = pmm;
+        A = a1;
+    }
+    return A;
 }
 
 static int build_rule(fqnm_plan_t* p)
@@ -368,33 +421,26 @@ static int build_rule(fqnm_plan_t* p)
         }
     } else {
         if (lo == 0 && hi == 0) {
-            // derive the largest symmetric range on which D8 holds (and the device path is exact)
-            int64_t cap = eo_fast_ok ? a_fast : (1 << 24);
-            int64_t A = 0;
-            int rd = d.rounding;
-            int64_t pp0 = host_phi(p->hp, 0, rd), pm0 = host_phi(p->hm, 0, rd);
-            int64_t ppp = pp0, pmp = pm0, ppn = pp0, pmn = pm0;
-            while (A < cap) {
-                int64_t a1 = A + 1;
-                int64_t pp1 = host_phi(p->hp, a1, rd), pm1 = host_phi(p->hm, a1, rd);
-                int64_t ppm = host_phi(p->hp, -a1, rd), pmm = host_phi(p->hm, -a1, rd);
-                int64_t dp = pp1 - ppp, dm = pm1 - pmp;            // step A -> A+1
-                int64_t dpn = ppn - ppm, dmn = pmn - pmm;          // step -A-1 -> -A
-                if (dp < 0 || dm > 0 || dp - dm > 1 || dpn < 0 || dmn > 0 || dpn - dmn > 1) break;
-                if (!generic_headroom(p->hp, a1) || !generic_headroom(p->hm, a1)) break;
-                ppp = pp1; pmp = pm1; ppn = ppm; pmn = pmm;
-                A = a1;
+            // derive the largest symmetric range on which D8 holds
+            int64_t A = d8_symmetric_limit(p, kind == FQNM_BURGERS_EO);
+            if (eo_fast_ok && A > a_fast) {
+                // the fast closed form is exact only on |q| <= a_fast: that is the plan's
+                // range; range-checked steps beyond it fall back to the int64 rule
+                if (A >= 1) p->d8_lim = A;
+                A = a_fast;
             }
             if (A < 1) return fail(FQNM_ERR_CFL, "D8 fails already at |q| <= 1");
             lo = -A; hi = A;
         } else {
             if (lo >= hi) return fail(FQNM_ERR_ARG, "q_lo must be < q_hi");
             if (lo < i32lo || hi > i32hi) return fail(FQNM_ERR_RANGE, "range exceeds int32 state");
-            if (hi - lo > ((int64_t)1 << 27))
-                return fail(FQNM_ERR_UNSUPPORTED, "declared range too wide to validate D8");
-            int64_t bad = d8_first_violation(p, lo, hi);
-            if (bad >= lo)
-                return fail(FQNM_ERR_CFL, "D8 (integer monotonicity) fails at q = %lld", (long long)bad);
+            if (!p->trusted_range) {
+                if (hi - lo > ((int64_t)1 << 27))
+                    return fail(FQNM_ERR_UNSUPPORTED, "declared range too wide to validate D8");
+                int64_t bad = d8_first_violation(p, lo, hi);
+                if (bad >= lo)
+                    return fail(FQNM_ERR_CFL, "D8 (integer monotonicity) fails at q = %lld", (long long)bad);
+            }
             int64_t amax = (lo < 0 ? -lo : lo) > hi ? (lo < 0 ? -lo : lo) : hi;
             if (!generic_headroom(p->hp, amax) || !generic_headroom(p->hm, amax))
                 return fail(FQNM_ERR_RANGE, "int64 headroom exceeded on the declared range");
@@ -566,7 +612,7 @@ static int max_block_steps(const fqnm_plan_t* p, int V)
     return k & ~3;
 }
 
-static int plan_build(fqnm_plan_t** out, const fqnm_plan_desc* din, bool allocate)
+static int plan_build(fqnm_plan_t** out, const fqnm_plan_desc* din, bool allocate, bool trusted_range)
 {
     if (!out || !din) return fail(FQNM_ERR_ARG, "null argument");
     *out = nullptr;
@@ -579,6 +625,7 @@ static int plan_build(fqnm_plan_t** out, const fqnm_plan_desc* din, bool allocat
     if (d.rounding < 0 || d.rounding > 2) return fail(FQNM_ERR_ARG, "unknown rounding %d", d.rounding);
     fqnm_plan_t* p = new (std::nothrow) fqnm_plan_t();
     if (!p) return fail(FQNM_ERR_NOMEM, "out of host memory");
+    p->trusted_range = trusted_range;
     p->d = d;
     p->d.n_global = d.n_global ? d.n_global : d.n_local;
     p->st = (cudaStream_t)d.stream;
@@ -814,6 +861,8 @@ static void pipe_release(fqnm_plan_t* p)
         if (p->pipe_buf[i]) cudaFree(p->pipe_buf[i]);
         p->pipe_buf[i] = nullptr;
     }
+    if (p->pipe_head) cudaFree(p->pipe_head);
+    p->pipe_head = nullptr;
     if (p->pipe_guard) cudaFree(p->pipe_guard);
     if (p->pipe_guard_host) cudaFreeHost(p->pipe_guard_host);
     p->pipe_guard = nullptr;
@@ -830,6 +879,7 @@ extern "C" void fqnm_destroy(fqnm_plan_t* p)
 {
     if (!p) return;
     cudaStreamSynchronize(p->st);
+    if (p->generic_child) fqnm_destroy(p->generic_child);
     if (p->scratch) cudaFree(p->scratch);
     if (p->d_minmax) cudaFree(p->d_minmax);
     if (p->h_minmax) cudaFreeHost(p->h_minmax);
@@ -856,8 +906,9 @@ extern "C" int fqnm_set_stream(fqnm_plan_t* p, void* stream)
 static bool aligned16(const void* x) { return ((uintptr_t)x & 15u) == 0; }
 
 // ---------------------------------------------------------------------------
-static int check_range(fqnm_plan_t* p, const void* q)
+static int check_range(fqnm_plan_t* p, const void* q, bool* use_generic = nullptr)
 {
+    if (use_generic) *use_generic = false;
     const fqnm_plan_desc& d = p->d;
     long long init[2] = {LLONG_MAX, LLONG_MIN};
     p->h_minmax[0] = init[0];
@@ -868,6 +919,12 @@ static int check_range(fqnm_plan_t* p, const void* q)
     CUDA_TRY(cudaMemcpyAsync(p->h_minmax + 2, p->d_minmax, 2 * sizeof(long long), cudaMemcpyDeviceToHost, p->st));
     CUDA_TRY(cudaStreamSynchronize(p->st));
     long long mn = p->h_minmax[2], mx = p->h_minmax[3];
+    const bool one_d = p->family == 2 || p->family == 3 || p->family == 4 || p->family == 6;
+    if ((mn < p->lo || mx > p->hi) && use_generic && one_d && p->d8_lim > 0 && mn >= -p->d8_lim &&
+        mx <= p->d8_lim) {
+        *use_generic = true;            // inside the D8 range, beyond the fast closed form's domain
+        return FQNM_OK;
+    }
     if (mn < p->lo || mx > p->hi)
         return fail(FQNM_ERR_RANGE, "state range [%lld, %lld] outside the plan's admissible "
                     "range [%lld, %lld]", mn, mx, (long long)p->lo, (long long)p->hi);
@@ -992,6 +1049,35 @@ static int step_persist(fqnm_plan_t* p, void* q, int64_t nb, int64_t base, int64
 
 static int halo_step_blocks(fqnm_plan_t* const* plans, int nplans, int64_t nsteps);
 
+// A range-checked EO step whose state left the fast closed form's domain but stays within
+// the D8 range (+-d8_lim): the same problem on a plan with the exact int64 rule, created
+// on first use.  The maximum principle (Lemma P:210-212, under D8) keeps the state in
+// [min q, max q] for the whole call, so one check decides the call.
+static int step_generic_child(fqnm_plan_t* p, void* q, int64_t nsteps)
+{
+    if (!p->generic_child) {
+        fqnm_plan_desc d = p->d;
+        d.kappa_num = p->kap_num;
+        d.kappa_den = p->kap_den;
+        d.q_lo = -p->d8_lim;
+        d.q_hi = p->d8_lim;
+        d.check_range = 0;
+        d.k = 0;
+        d.stream = (void*)p->st;
+        fqnm_plan_t* c = nullptr;
+        const int rc = plan_build(&c, &d, true, /*trusted_range=*/true);
+        if (rc != FQNM_OK) return rc;
+        if (c->rule != R_GENERIC) { fqnm_destroy(c); return fail(FQNM_ERR_UNSUPPORTED, "no int64 fallback rule"); }
+        p->generic_child = c;
+    }
+    fqnm_plan_t* c = p->generic_child;
+    c->st = p->st;
+    const int64_t l0 = c->launches;
+    const int rc = fqnm_step(c, q, nsteps);
+    p->launches += c->launches - l0;
+    return rc;
+}
+
 extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
 {
     if (p && p->d.boundary == FQNM_HALO && p->d.p2p) {
@@ -1006,7 +1092,11 @@ extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
         return fail(FQNM_ERR_UNSUPPORTED, "split-domain plans step through fqnm_step_block");
     if (nsteps == 0) return FQNM_OK;
     int rc;
-    if (d.check_range && d.nvar == 1 && (rc = check_range(p, q)) != FQNM_OK) return rc;
+    if (d.check_range && d.nvar == 1) {
+        bool gen = false;
+        if ((rc = check_range(p, q, &gen)) != FQNM_OK) return rc;
+        if (gen) return step_generic_child(p, q, nsteps);
+    }
     const int bm = bmode_of(d);
     const int64_t n = d.n_local;
     const size_t bytes = state_elems(d) * elem_size(d);
@@ -1355,6 +1445,7 @@ static int pipe_setup(fqnm_plan_t* p, int64_t nsteps)
     p->pipe_m = m;
     cudaError_t e = cudaSuccess;
     for (int i = 0; i < 3 && e == cudaSuccess; ++i) e = cudaMalloc(&p->pipe_buf[i], (size_t)(C + 2 * H) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&p->pipe_head, (size_t)H * 4);
     if (e == cudaSuccess) e = cudaMalloc(&p->pipe_guard, (size_t)m * sizeof(int));
     if (e == cudaSuccess) e = cudaMallocHost(&p->pipe_guard_host, (size_t)m * sizeof(int));
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->pipe_h2d, cudaStreamNonBlocking);
@@ -1384,6 +1475,14 @@ static int step_host_pipelined(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
     return rc;
 }
 
+// The host buffer is updated in place, so every read of q_host must precede the D2H that
+// overwrites those cells:
+//  * chunk c+1's left halo [(c+1)C - H, (c+1)C) is chunk c's output: H2D(c+1) is issued
+//    before D2H(c) and D2H(c) waits on its event;
+//  * the last chunk's right halo wraps to [0, H), chunk 0's output: it is copied into
+//    pipe_head on the H2D stream before H2D(0) (so before D2H(0)) and taken from there;
+//  * chunk c's right halo and chunk 0's left halo are outputs of later D2Hs, which follow
+//    that chunk's H2D through the compute dependency.
 static int step_host_pipelined_impl(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
 {
     const int64_t n = p->d.n_local, C = p->pipe_C, H = p->pipe_H, m = p->pipe_m, E = C + 2 * H;
@@ -1396,19 +1495,34 @@ static int step_host_pipelined_impl(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
     CUDA_TRY(cudaMemsetAsync(p->pipe_guard, 0, (size_t)m * sizeof(int), p->st));
     CUDA_TRY(cudaEventRecord(ev_comp[0], p->st));                 // guard reset before any use
     CUDA_TRY(cudaStreamWaitEvent(p->pipe_h2d, ev_comp[0], 0));
-    for (int64_t c = 0; c < m; ++c) {
+    CUDA_TRY(cudaMemcpyAsync(p->pipe_head, qh, (size_t)H * 4, cudaMemcpyHostToDevice, p->pipe_h2d));
+    auto h2d = [&](int64_t c) -> int {
         const int b = (int)(c % 3);
         int32_t* buf = (int32_t*)p->pipe_buf[b];
-        // H2D of the extended region (wraps around the periodic domain)
-        if (c >= 3) CUDA_TRY(cudaStreamWaitEvent(p->pipe_h2d, ev_out[b], 0));
+        if (c >= 3) CUDA_TRY(cudaStreamWaitEvent(p->pipe_h2d, ev_out[b], 0));   // buffer free
         int64_t s0 = c * C - H;
         if (s0 < 0) s0 += n;
         const int64_t first = (s0 + E <= n) ? E : n - s0;
         CUDA_TRY(cudaMemcpyAsync(buf, qh + s0, (size_t)first * 4, cudaMemcpyHostToDevice, p->pipe_h2d));
-        if (first < E)
-            CUDA_TRY(cudaMemcpyAsync(buf + first, qh, (size_t)(E - first) * 4, cudaMemcpyHostToDevice,
+        if (first < E) {
+            // wrapped part: [0, E - first) of the domain; its first H cells may already be
+            // chunk 0's output in q_host, so they come from the saved head
+            const int64_t w = E - first, wh = w < H ? w : H;
+            CUDA_TRY(cudaMemcpyAsync(buf + first, p->pipe_head, (size_t)wh * 4, cudaMemcpyDeviceToDevice,
                                      p->pipe_h2d));
+            if (w > wh)
+                CUDA_TRY(cudaMemcpyAsync(buf + first + wh, qh + wh, (size_t)(w - wh) * 4,
+                                         cudaMemcpyHostToDevice, p->pipe_h2d));
+        }
         CUDA_TRY(cudaEventRecord(ev_in[b], p->pipe_h2d));
+        return FQNM_OK;
+    };
+    int rc = h2d(0);
+    if (rc != FQNM_OK) return rc;
+    for (int64_t c = 0; c < m; ++c) {
+        const int b = (int)(c % 3);
+        int32_t* buf = (int32_t*)p->pipe_buf[b];
+        if (c + 1 < m && (rc = h2d(c + 1)) != FQNM_OK) return rc;  // reads chunk c's cells: first
         // range check + stepping on the compute stream
         CUDA_TRY(cudaStreamWaitEvent(p->st, ev_in[b], 0));
         if (check) {
@@ -1419,13 +1533,14 @@ static int step_host_pipelined_impl(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
             ch->guard = nullptr;
         }
         const int64_t l0 = ch->launches;
-        int rc = fqnm_step(ch, buf, nsteps);
+        rc = fqnm_step(ch, buf, nsteps);
         p->launches += ch->launches - l0;
         ch->guard = nullptr;
         if (rc != FQNM_OK) return rc;
         CUDA_TRY(cudaEventRecord(ev_comp[b], p->st));
-        // D2H of the inner C cells
+        // D2H of the inner C cells, after the stepping and after H2D(c+1) read their tail
         CUDA_TRY(cudaStreamWaitEvent(p->pipe_d2h, ev_comp[b], 0));
+        if (c + 1 < m) CUDA_TRY(cudaStreamWaitEvent(p->pipe_d2h, ev_in[(c + 1) % 3], 0));
         CUDA_TRY(cudaMemcpyAsync(qh + c * C, buf + H, (size_t)C * 4, cudaMemcpyDeviceToHost, p->pipe_d2h));
         CUDA_TRY(cudaEventRecord(ev_out[b], p->pipe_d2h));
     }
@@ -1745,6 +1860,7 @@ static void fill_info(const fqnm_plan_t* p, fqnm_plan_info* info)
     info->scratch_bytes = (int64_t)p->scratch_bytes;
     info->s_euler = p->s_e;
     info->g1_euler = p->g1_e;
+    info->d8_lim = p->d8_lim;
 }
 
 extern "C" int fqnm_plan_validate(const fqnm_plan_desc* d, fqnm_plan_info* info)

@@ -72,3 +72,50 @@ def test_plain_step_host_paths(F):
         qh = torch.tensor(q0).pin_memory()
         F.fqnm_step_host(plan, qh, 33)
         assert torch.equal(qh, ref.cpu())
+
+
+def _right_dependent_plans(F, n):
+    """Plans whose update reads the right neighbour (the pipelined path's right
+    halo must be exact, which strictly positive EO data never exercises)."""
+    rng = np.random.default_rng(11)
+    q_signed = W.smooth_random(rng, n, 100000, 0).astype(np.int32)      # changes sign
+    qmax = int(np.abs(q_signed).max())
+    lam_eo = W.dt_dx_double(W.cfg("cfg2"), qmax)
+    yield "eo_signed", F.fqnm_plan(n, 1e-5, lam_eo, F.BURGERS_EO, F.PERIODIC), q_signed
+    yield "lf", F.fqnm_plan_ex(n, 1e-3, 0.5, F.BURGERS_LF, flux_param=1.0,
+                               q_range=(-900, 900)), np.clip(q_signed // 100, -900, 900)
+    yield "linear_neg", F.fqnm_plan_ex(n, 1e-5, 0.5, F.LINEAR, flux_param=-1.0), q_signed
+    yield "godunov", F.fqnm_plan_ex(n, 1e-5, lam_eo, F.BURGERS_GODUNOV), q_signed
+
+
+@pytest.mark.parametrize("nsteps", [1, 37, 200])
+def test_pipelined_step_host_right_neighbour_rules(F, nsteps):
+    n = 1 << 24
+    for name, plan, q0 in _right_dependent_plans(F, n):
+        ref = torch.tensor(np.ascontiguousarray(q0, dtype=np.int32), device="cuda")
+        l0 = plan.launches()
+        F.fqnm_step(plan, ref, nsteps)
+        dev_launches = plan.launches() - l0
+        qh = torch.tensor(np.ascontiguousarray(q0, dtype=np.int32)).pin_memory()
+        l0 = plan.launches()
+        F.fqnm_step_host(plan, qh, nsteps)
+        host_launches = plan.launches() - l0
+        assert torch.equal(qh, ref.cpu()), name
+        if name == "eo_signed":
+            assert host_launches > 2 * dev_launches, "expected the chunked pipeline"
+        # twice in a row (reused pipeline, continued trajectory)
+        F.fqnm_step(plan, ref, nsteps)
+        F.fqnm_step_host(plan, qh, nsteps)
+        assert torch.equal(qh, ref.cpu()), name
+
+
+def test_step_host_checks_buffer(F):
+    plan = F.fqnm_plan(4096, 1e-5, 0.25, F.BURGERS_EO, F.PERIODIC)
+    with pytest.raises(TypeError):
+        F.fqnm_step_host(plan, torch.zeros(4096, dtype=torch.int64), 1)
+    with pytest.raises(ValueError):
+        F.fqnm_step_host(plan, torch.zeros(4095, dtype=torch.int32), 1)
+    with pytest.raises(TypeError):
+        F.fqnm_step_host(plan, np.zeros(4096, dtype=np.float32), 1)
+    with pytest.raises(ValueError):
+        F.fqnm_step_host(plan, np.zeros(8192, dtype=np.int32), 1)

@@ -571,3 +571,35 @@ def test_repetitions_bitwise_identical(F):
     F.fqnm_step(plan, a, 300)
     F.fqnm_step(plan, b, 300)
     assert torch.equal(a, b)
+
+
+# ---------------------------------------------------------------------------
+# EO plans whose D8 range is wider than the fast closed form's domain (kappa < 1/(4 2^20)):
+# a range-checked step with data in (fast domain, D8 range] runs on the exact int64 rule
+# instead of failing; beyond the D8 range it still fails
+@pytest.mark.parametrize("n", [1024, 4096 + 13, 50_000, 300_007])
+def test_eo_beyond_fast_domain_falls_back_to_int64(F, n):
+    Q = 4186126
+    lam = Fraction(2, Q)                                  # kappa = delta lam / 2 = 1/Q
+    plan = F.fqnm_plan_ex(n, 1.0, float(lam), F.BURGERS_EO, kappa=(1, Q), check_range=True)
+    info = plan.info()
+    A, D = info["q_hi"], info["d8_lim"]
+    assert info["rule"] == 5 and D > A                    # fast rule on +-A, D8 up to +-D
+    rng = np.random.default_rng(n)
+    u = W.smooth_random(rng, n, 1000, 0).astype(np.float64)
+    q0 = np.rint(u / np.abs(u).max() * D).astype(np.int64)
+    assert np.abs(q0).max() == D
+    q = to_dev(q0)
+    F.fqnm_step(plan, q, 40)
+    ref = oracle.Rule(oracle.BURGERS_EO, 1, lam).run(q0, 40)
+    assert np.array_equal(host(q), ref)
+    # data inside the fast domain still takes the fast rule and stays exact
+    q1 = np.rint(u / np.abs(u).max() * A).astype(np.int64)
+    q = to_dev(q1)
+    F.fqnm_step(plan, q, 40)
+    assert np.array_equal(host(q), oracle.Rule(oracle.BURGERS_EO, 1, lam).run(q1, 40))
+    q2 = q0.copy()
+    q2[n // 2] = D + 1
+    with pytest.raises(F.FqnmError) as e:
+        F.fqnm_step(plan, to_dev(q2), 1)
+    assert e.value.status == 3
