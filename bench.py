@@ -44,11 +44,14 @@ METRIC = "integer cell-updates/sec (GCUPS)"
 UNIT = "GCUPS"
 # Algorithmic operations per cell-update (DESIGN.md §6 "ops_alg"): the exact closed form's
 # own operations, not counting redundant halo work, shuffles, loads/stores or loop control.
-# EO with P = 1 (every BJ Burgers config): int->float, q^2 (FMUL), estimate (FFMA), remainder
-# (2 IMAD), correction (LEA), sign mask (SHF), phi- (LOP3), interface transfer + update
-# (2 IADD3) = 10.  SURVEY §8(d)-D3's a-priori 16 over-counts this closed form (it made the
-# fraction exceed 1.0).  General P adds one IMAD (11).  Linear kappa = 1/2: 4.
-OPS_ALG = {"burgers_eo": 10, "burgers_eo_general_p": 11, "linear": 4}
+# EO with P = 1 (every BJ Burgers config), mixed-sign data: int->float, q^2 (FMUL), estimate
+# (FFMA), remainder (2 IMAD), correction (LEA), sign mask (SHF), phi- (LOP3), interface
+# transfer + update (2 IADD3) = 10.  Sign-uniform data (every cell >= 0, as BJ.cfg4's
+# u0 = 0.2 + ... > 0; DESIGN §K2 "sign-uniform windows"): phi- = 0, the transfer is g alone:
+# int->float, FMUL, FFMA, 2 IMAD, LEA, one IADD3 = 7.  General P adds one IMAD.
+# Linear kappa = 1/2: 4.  SURVEY §8(d)-D3's a-priori 16 over-counts these closed forms.
+OPS_ALG = {"burgers_eo": 10, "burgers_eo_general_p": 11, "burgers_eo_sign_uniform": 7,
+           "burgers_eo_sign_uniform_general_p": 8, "linear": 4}
 RULE_NAMES = {1: "LIN_HALF", 2: "EO_FAST", 3: "GENERIC", 4: "LIN_FAST", 5: "EO_P1"}
 SM_COUNT = 148
 LANES_PER_SM_CLK = 128                          # 4 SMSPs x 32 lanes, 1 warp-instr/clk each
@@ -195,9 +198,10 @@ def cpu_baseline_cfg4(qmax: int):
     rule = oracle.Rule(oracle.BURGERS_EO, w.delta, W.dt_dx(w, qmax))
     qa = W.q0_cfg4(n=w.n, count=1 << 20).numpy().astype(np.int64)
     q1 = qa[:1 << 17].copy()
-    rate, steps, secs = time_oracle(lambda s: rule.run(qa, s), qa.size, 12.0)
+    cores = oracle.max_threads()              # the OpenMP default the all-core run uses
+    rate, steps, secs = time_oracle(lambda s: rule.run(qa, s, nthreads=cores), qa.size, 12.0)
     rate1, steps1, secs1 = time_oracle(lambda s: rule.run(q1, s, nthreads=1), q1.size, 5.0)
-    return {"value": rate, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+    return {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"periodic cfg4 slice of 2^20 cells x {steps} time steps ({secs:.1f} s)",
             "one_thread": {"value": rate1, "unit": UNIT,
                            "sample": f"2^17 cells x {steps1} time steps ({secs1:.1f} s)"},
@@ -405,13 +409,20 @@ def run_cfg4(args):
     # ---- roofline of the dominant kernel (k_blocked, EO fast path) ----
     per_launch_ms = kern_ms / max(kern_launches, 1)
     updates_per_launch = n_local * T * args.steps / max(kern_launches, 1)
-    ops_alg = OPS_ALG["burgers_eo"] if info["rule"] == 5 else OPS_ALG["burgers_eo_general_p"]
+    # the K2 path every window takes: sign-uniform when the whole state is >= 0 (or <= 0),
+    # which the maximum principle keeps for the whole run (Lemma CFL)
+    uniform = inv0["min"] >= 0 or inv0["max"] <= 0
+    ops_key = ("burgers_eo_sign_uniform" if uniform else "burgers_eo") + (
+        "" if info["rule"] == 5 else "_general_p")
+    ops_alg = OPS_ALG[ops_key]
     hbm_bytes_per_launch = 8.0 * n_local                               # read + write int32 once per block
     roofline = alu_roofline(
         "k_blocked<%s,V=%d>" % (RULE_NAMES.get(info["rule"], "?"), info["cells_per_thread"]),
         ops_alg, updates_per_launch, per_launch_ms, hbm_bytes_per_launch,
         {"kernel_launches": kern_launches, "kernel_share_of_step": kern_ms / ms if ms > 0 else None,
-         "k": info["k"], "V": info["cells_per_thread"]})
+         "k": info["k"], "V": info["cells_per_thread"], "ops_basis": ops_key,
+         "windows_redundancy": 32.0 * info["cells_per_thread"] / (
+             32.0 * info["cells_per_thread"] - 2 * ((info["k"] + 3) // 4 * 4))})
     tr, tr_src = ncu_traffic(n_local)
     if tr is not None:
         roofline["traffic"] = tr

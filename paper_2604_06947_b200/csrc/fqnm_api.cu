@@ -552,7 +552,7 @@ static int choose_kernel(fqnm_plan_t* p)
         const bool two = p->dep_left && p->dep_right;
         if (p->rule == R_LIN_HALF) { p->V = 32; p->k = 64; p->minb = 2; }
         else if (p->rule == R_EO_FAST || p->rule == R_EO_P1 || p->rule == R_TP_FAST) {
-            p->V = 32; p->k = 24; p->minb = 2;
+            p->V = 32; p->k = p->rule == R_TP_FAST ? 24 : 32; p->minb = 2;   // EO: sweep r02_tune_sign.jsonl
         }
         else { p->V = 8; p->k = two ? 8 : 16; }
         if (d.k > 0) p->k = d.k;

@@ -84,11 +84,80 @@ __device__ __forceinline__ void eval_maps(const int32_t (&q)[V], int32_t (&g)[V]
 // One explicit step of the lane's V cells.  NB = 0: neighbours by shfl.up/down
 // (window edges produce garbage that the caller cuts off); NB = 1: periodic
 // wrap inside the warp (K3, the warp holds a whole problem).
-template <int RULE, int V, bool WALL, int NB>
+//
+// SIGN (EO rules, no walls): 1 = every cell of the window has q >= 0, 2 = every cell has
+// q <= 0.  By the monotonicity the planner proves (D8: the update is non-decreasing in
+// each argument and keeps constants, Lemma CFL) a window whose cells are all
+// >= 0 stays >= 0 inside its dependence cone for all k steps, so there phi- = 0 and the
+// interface transfer is F_{j+1/2} = phi+(q_j) = g_j; for q <= 0, F_{j+1/2} = phi-(q_{j+1})
+// = g_{j+1}.  Cells outside the cone are cut off by the caller either way.
+#ifndef FQNM_SIGN_STREAM
+#define FQNM_SIGN_STREAM 1     // sign-uniform step: maps evaluated cell by cell (no map array)
+#endif
+template <int RULE, int V, bool WALL, int NB, int SIGN = 0>
 __device__ __forceinline__ void one_step(int32_t (&q)[V], const DevRule& r, int lane, int64_t g0,
                                          int64_t n)
 {
-    if (RULE == R_LIN_HALF && !WALL) {
+    if (FQNM_SIGN_STREAM && SIGN != 0 && !WALL && (RULE == R_EO_P1 || RULE == R_EO_FAST)) {
+        // streamed: the lane-edge map first (for the shuffle), then each cell's map right
+        // before its update, so the ALU-pipe updates interleave with the map evaluation
+        // and no array of maps is live
+        if (SIGN == 1) {                   // q_j += g_{j-1} - g_j
+            const int32_t glast = eo_g_biased<RULE, true>(q[V - 1], r);
+            int32_t gp = NB == 0 ? __shfl_up_sync(FULL, glast, 1)
+                                 : __shfl_sync(FULL, glast, (lane + 31) & 31);
+#pragma unroll
+            for (int j = 0; j + 1 < V; j += 2) {         // V even: j + 1 <= V - 2 here
+                const int32_t g0 = eo_g_biased<RULE, false>(q[j], r);
+                q[j] = q[j] + gp - g0;
+                if (j + 2 < V) {
+                    const int32_t g1 = eo_g_biased<RULE, true>(q[j + 1], r);
+                    q[j + 1] = q[j + 1] + g0 - g1;
+                    gp = g1;
+                } else {
+                    gp = g0;
+                }
+            }
+            q[V - 1] = q[V - 1] + gp - glast;
+        } else {                           // q_j += g_j - g_{j+1}
+            const int32_t g0 = eo_g_biased<RULE, false>(q[0], r);
+            const int32_t gr = NB == 0 ? __shfl_down_sync(FULL, g0, 1)
+                                       : __shfl_sync(FULL, g0, (lane + 1) & 31);
+            int32_t gc = g0;
+#pragma unroll
+            for (int j = 0; j + 1 < V; j += 2) {
+                const int32_t g1 = eo_g_biased<RULE, true>(q[j + 1], r);
+                q[j] = q[j] + gc - g1;
+                gc = g1;
+                if (j + 2 < V) {
+                    const int32_t g2 = eo_g_biased<RULE, false>(q[j + 2], r);
+                    q[j + 1] = q[j + 1] + gc - g2;
+                    gc = g2;
+                }
+            }
+            q[V - 1] = q[V - 1] + gc - gr;
+        }
+    } else if (SIGN != 0 && !WALL && (RULE == R_EO_P1 || RULE == R_EO_FAST)) {
+        int32_t g[V];
+#pragma unroll
+        for (int j = 0; j < V; j += 2) {
+            g[j] = eo_g_biased<RULE, false>(q[j], r);
+            if (j + 1 < V) g[j + 1] = eo_g_biased<RULE, true>(q[j + 1], r);
+        }
+        if (SIGN == 1) {                   // q_j += g_{j-1} - g_j
+            const int32_t gl = NB == 0 ? __shfl_up_sync(FULL, g[V - 1], 1)
+                                       : __shfl_sync(FULL, g[V - 1], (lane + 31) & 31);
+            q[0] = q[0] + gl - g[0];
+#pragma unroll
+            for (int j = 1; j < V; ++j) q[j] = q[j] + g[j - 1] - g[j];
+        } else {                           // q_j += g_j - g_{j+1}
+            const int32_t gr = NB == 0 ? __shfl_down_sync(FULL, g[0], 1)
+                                       : __shfl_sync(FULL, g[0], (lane + 1) & 31);
+#pragma unroll
+            for (int j = 0; j + 1 < V; ++j) q[j] = q[j] + g[j] - g[j + 1];
+            q[V - 1] = q[V - 1] + g[V - 1] - gr;
+        }
+    } else if (RULE == R_LIN_HALF && !WALL) {
         // kappa = 1/2: q'_j = trunc(q_j/2) + phi+(q_{j-1}), phi+ = q - trunc(q/2).
         // The runtime r.one turns the two adds into IMADs (FMA pipe) so the
         // ALU pipe only carries the halving (LEA.HI + SHF): 2 ALU + 2 FMA ops.
@@ -207,11 +276,20 @@ __device__ __forceinline__ void fused_step_lin_half(int32_t (&q)[V], int32_t (&h
 }
 
 // K2: temporally blocked stencil
-template <int RULE, int V, bool WALL>
+template <int RULE, int V, bool WALL, int SIGN = 0>
 __device__ __forceinline__ void run_window_steps(int32_t (&q)[V], int ksteps, const DevRule& r,
                                                  int64_t g0, int64_t n)
 {
     const int lane = threadIdx.x & 31;
+    if (SIGN != 0) {
+        int s = 0;
+        for (; s + 2 <= ksteps; s += 2) {
+            one_step<RULE, V, WALL, 0, SIGN>(q, r, lane, g0, n);
+            one_step<RULE, V, WALL, 0, SIGN>(q, r, lane, g0, n);
+        }
+        if (s < ksteps) one_step<RULE, V, WALL, 0, SIGN>(q, r, lane, g0, n);
+        return;
+    }
     if (FQNM_FUSED_STEPS && RULE != R_TWOPOINT && RULE != R_TP_FAST && !WALL && ksteps > 0) {
         int32_t g[V], m[V];
         if (RULE == R_LIN_HALF) {
@@ -248,6 +326,34 @@ __device__ __forceinline__ void run_window_steps(int32_t (&q)[V], int ksteps, co
         one_step<RULE, V, WALL, 0>(q, r, lane, g0, n);
     }
     if (s < ksteps) one_step<RULE, V, WALL, 0>(q, r, lane, g0, n);
+}
+
+#ifndef FQNM_SIGN_WINDOWS
+#define FQNM_SIGN_WINDOWS 1    // K2/K2P/K6 EO: sign-uniform windows step on g alone (one_step SIGN)
+#endif
+
+// k steps of a window without walls (neighbours by shfl, edges cut off by the caller).
+// EO rules: one warp vote per window on the sign of its cells picks the sign-uniform
+// step (one_step SIGN) where it applies
+template <int RULE, int V>
+__device__ __forceinline__ void run_window_steps_signed(int32_t (&q)[V], int ksteps,
+                                                        const DevRule& r)
+{
+#ifdef FQNM_FORCE_SIGN
+    // experiment builds only: every window taken as sign-uniform (valid for such data only)
+    if (RULE == R_EO_P1 || RULE == R_EO_FAST) {
+        run_window_steps<RULE, V, false, FQNM_FORCE_SIGN>(q, ksteps, r, 0, 0);
+        return;
+    }
+#endif
+    if (FQNM_SIGN_WINDOWS && (RULE == R_EO_P1 || RULE == R_EO_FAST)) {
+        int32_t lo = q[0], hi = q[0];
+#pragma unroll
+        for (int j = 1; j < V; ++j) { lo = min(lo, q[j]); hi = max(hi, q[j]); }
+        if (__all_sync(FULL, lo >= 0)) { run_window_steps<RULE, V, false, 1>(q, ksteps, r, 0, 0); return; }
+        if (__all_sync(FULL, hi <= 0)) { run_window_steps<RULE, V, false, 2>(q, ksteps, r, 0, 0); return; }
+    }
+    run_window_steps<RULE, V, false>(q, ksteps, r, 0, 0);
 }
 
 __device__ __forceinline__ int64_t wrap_index(int64_t i, int64_t n, int bmode, int64_t halo)
@@ -348,6 +454,7 @@ __device__ __noinline__ void slow_window(const BlockedArgs& a, const DevRule& r,
     }
 }
 
+
 #ifndef FQNM_PREFETCH
 #define FQNM_PREFETCH 0        // K2: stage the next window in shared memory (cp.async) while stepping
                                // (measured 2.3% slower at V = 32: the staging registers spill)
@@ -439,7 +546,7 @@ __global__ void __launch_bounds__(256, MINB) k_blocked(BlockedArgs a, DevRule r)
                 }
             }
 #endif
-            run_window_steps<RULE, V, false>(q, a.ksteps, r, 0, 0);
+            run_window_steps_signed<RULE, V>(q, a.ksteps, r);
             // store the cells whose dependence cone stayed inside the window
 #pragma unroll
             for (int j = 0; j < V / 4; ++j) {
@@ -568,7 +675,7 @@ __global__ void __launch_bounds__(256, MINB) k_blocked_persist(PersistArgs a, De
                 const int4 v = __ldcg(s4 + j);
                 q[4 * j] = v.x; q[4 * j + 1] = v.y; q[4 * j + 2] = v.z; q[4 * j + 3] = v.w;
             }
-            run_window_steps<RULE, V, false>(q, ks, r, 0, 0);
+            run_window_steps_signed<RULE, V>(q, ks, r);
             int4* d4 = reinterpret_cast<int4*>(dst + ws) + lane * (V / 4);
 #pragma unroll
             for (int j = 0; j < V / 4; ++j) {
@@ -712,7 +819,7 @@ __global__ void __launch_bounds__(256, k6_minb<RULE>()) k_resident(ResidentArgs 
         if (wall)
             run_window_steps<RULE, V, true>(q, kb, r, ws + (int64_t)lane * V, a.n);
         else
-            run_window_steps<RULE, V, false>(q, kb, r, 0, 0);
+            run_window_steps_signed<RULE, V>(q, kb, r);
         done += kb;
         if (done >= a.nsteps) break;
         ++blk;
@@ -1082,6 +1189,11 @@ cudaError_t blocked_rule(int V, int minb, const BlockedArgs& a, const DevRule& r
                                 cudaStream_t st, int cap)
 {
     if (minb) {
+#ifdef FQNM_EXTRA_VARIANTS
+        if (V == 32 && minb == 3) return blocked_v<RULE, 32, 3>(a, r, st, cap);
+        if (V == 64 && minb == 2) return blocked_v<RULE, 64, 2>(a, r, st, cap);
+        if (V == 64 && minb == 1) return blocked_v<RULE, 64, 1>(a, r, st, cap);
+#endif
         if (V == 16 && minb == 3) return blocked_v<RULE, 16, 3>(a, r, st, cap);
         if (V == 16 && minb == 4) return blocked_v<RULE, 16, 4>(a, r, st, cap);
         if (V == 32 && minb == 2) return blocked_v<RULE, 32, 2>(a, r, st, cap);
@@ -1142,7 +1254,11 @@ extern template cudaError_t blocked_rule<R_GENERIC>(int, int, const BlockedArgs&
 extern template cudaError_t blocked_rule<R_LIN_FAST>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
 extern template cudaError_t blocked_rule<R_TP_FAST>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
 #endif
+#ifdef FQNM_EXTRA_VARIANTS
+bool blocked_has_V(int V) { return V == 8 || V == 16 || V == 32 || V == 64; }
+#else
 bool blocked_has_V(int V) { return V == 8 || V == 16 || V == 32; }
+#endif
 bool blocked_rule_has_V(int rule, int V) { return rule == R_TWOPOINT ? (V == 8 || V == 16) : blocked_has_V(V); }
 int blocked_max_V() { return 32; }
 

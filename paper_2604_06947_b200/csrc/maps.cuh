@@ -50,6 +50,14 @@ __device__ __forceinline__ int32_t generic_phi(int32_t q, int64_t c2, int64_t c1
     return (int32_t)round_div_i64(num, den, rounding);
 }
 
+__device__ __forceinline__ int32_t imad_hi(int32_t a, int32_t b, int32_t c)
+{
+    // ((int64) a * b >> 32) + c on the FMA pipe; with b = 1: c + (a >> 31)
+    int32_t d;
+    asm("mad.hi.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
 // EO Burgers magnitude g(q) = floor((2P q^2 + Q) / (2Q)) = RHA(kappa q^2),
 // for |q| < 2^22 and kappa q^2 <= 2^20 (proved at plan time):
 // 1. qf = float(q) exactly via the 1.5*2^23 magic (IADD + FADD);
@@ -137,6 +145,40 @@ __device__ __forceinline__ void eo_gm_p1(int32_t q, int32_t& g, int32_t& m, cons
 #endif
     m = gb & 0x3FFFFF & sg;                                              // [q<0] g
     g = BIASED ? gb : (gb & 0x3FFFFF);
+}
+
+// EO magnitude alone, for sign-uniform windows (DESIGN.md §K2 "sign-uniform windows"):
+// where every cell of a window has q >= 0, phi-(q) = 0 and phi+(q) = g(q) (the EO split's
+// supports, P:62-68 with f- = min(u,0)^2/2), so the step needs g only; q <= 0 likewise
+// needs g = phi- only.  Returns g with the constant bias of eo_gm_p1 for P = 1 (the
+// step uses differences of g only).  P = 1: I2FP (or IMAD + FADD, CONV = 1), FMUL,
+// FFMA, 2 IMAD, LEA.HI = 6 instructions, against eo_gm_p1's 8.
+#ifndef FQNM_EO_SIGN_LEA
+#define FQNM_EO_SIGN_LEA 0     // bits + (v >> 31): 0 LEA.HI (ALU pipe), 1 IMAD.HI (FMA pipe), 2 alternate
+#endif
+#ifndef FQNM_EO_SIGN_CONV
+#define FQNM_EO_SIGN_CONV 0    // 0: I2FP for every cell, 1: IMAD + FADD, 2: alternate by cell
+#endif
+template <int RULE, bool ALT>
+__device__ __forceinline__ int32_t eo_g_biased(int32_t q, const DevRule& r)
+{
+    if (RULE == R_EO_P1) {
+        constexpr bool fma_conv = FQNM_EO_SIGN_CONV == 1 || (FQNM_EO_SIGN_CONV == 2 && ALT);
+        float qf;
+        if (!fma_conv) qf = __int2float_rn(q);                               // exact, |q| < 2^24
+        else qf = __int_as_float(imad(q, r.one, 0x4B400000)) - 12582912.0f;  // exact, |q| < 2^22
+        const float s = __fmul_rn(qf, qf);
+        const float t = __fmaf_rn(s, r.eo_cf, 12582913.0f);                 // 0x4B400001 + est
+        const int32_t bits = __float_as_int(t);
+        const int32_t v = imad(q, q, imad(bits, r.eo_nQ, r.eo_c6));
+        constexpr bool hi_fma = FQNM_EO_SIGN_LEA == 1 || (FQNM_EO_SIGN_LEA == 2 && ALT);
+        if (hi_fma) return imad_hi(v, r.one, bits);                          // FMA pipe
+        return bits + (v >> 31);                                             // 0x4B400000 + g (LEA.HI)
+    } else {
+        int32_t g, m;
+        eo_gm(q, g, m, r);
+        return g;
+    }
 }
 
 // LINEAR |kappa| = P/Q <= 1: phi(q) = sign(kappa q) floor((2P|q| + Q)/(2Q)), for

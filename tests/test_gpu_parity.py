@@ -143,16 +143,84 @@ def test_cfg4_full_size_windows(F):
     plan = F.fqnm_plan(n, 1e-6, W.dt_dx_double(w, qmax), F.BURGERS_EO, F.PERIODIC)
     info = plan.info()
     assert (info["kappa_num"], info["kappa_den"]) == (1, 5 * qmax)
+    tv0 = tv_periodic(q)
     F.fqnm_step(plan, q, w.steps)
     torch.cuda.synchronize()
     assert int(q.sum(dtype=torch.int64)) == s0
     assert int(q.min()) >= mn and int(q.max()) <= mx
+    assert tv_periodic(q) <= tv0                                   # TVD (Lemma CFL)
+    changed = int((q != W.q0_cfg4(n=n, device=DEV)).sum())
+    assert changed > n // 4                                        # the run moved the state
     rule = oracle.Rule(W.BURGERS_EO, w.delta, W.dt_dx(w, qmax))
     rng = np.random.default_rng(41)
     _check_windows(q, lambda idx: W.q0_cfg4_at(idx, n=n, device=DEV), rule, n, w.steps,
                    True, True, _windows(n, rng)[:8])
     del q
     torch.cuda.empty_cache()
+
+
+def test_cfg4_full_state_blocked_vs_naive(F):
+    """The whole 2^31-cell state after BJ.cfg4's 1000 steps: K2 (temporally blocked, the
+    bench's launch configuration, sign-uniform windows) against K1 (one step per launch,
+    general map code, itself oracle-checked in test_all_families_match_oracle), element by
+    element."""
+    w = W.cfg("cfg4")
+    n = w.n
+    a = W.q0_cfg4(n=n, device=DEV)
+    qmax = int(a.abs().max())
+    lam = W.dt_dx_double(w, qmax)
+    pa = F.fqnm_plan(n, 1e-6, lam, F.BURGERS_EO, F.PERIODIC)
+    assert pa.info()["kernel"] == 2
+    pb = F.fqnm_plan(n, 1e-6, lam, F.BURGERS_EO, F.PERIODIC)
+    F.fqnm_debug_override(pb, 1, 0, 0)
+    b = a.clone()
+    F.fqnm_step(pa, a, w.steps)
+    del pa
+    F.fqnm_step(pb, b, w.steps)
+    del pb
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    del a, b
+    torch.cuda.empty_cache()
+
+
+def _sign_patch_data(rng, n, amp, patch):
+    """Patches of `patch` cells alternately >= 0, <= 0 and sign-changing, so the K2
+    windows (32 V cells) include all-positive, all-negative and mixed ones, and windows
+    whose only zero cells sit at their edges."""
+    q = np.abs(W.smooth_random(rng, n, amp, amp // 2))
+    for i, a in enumerate(range(0, n, patch)):
+        kind = i % 4
+        if kind == 1:
+            q[a:a + patch] = -q[a:a + patch]
+        elif kind == 2:
+            q[a:a + patch] -= int(np.median(q[a:a + patch]))
+        elif kind == 3:
+            q[a:a + patch:97] = 0
+    return q
+
+
+@pytest.mark.parametrize("kernel,V", [(2, 8), (2, 16), (2, 32), (6, 0), (12, 0)])
+@pytest.mark.parametrize("case", ["p1", "general_p"])
+@pytest.mark.parametrize("patch", [300, 1024, 5000])
+def test_eo_sign_uniform_windows(F, kernel, V, case, patch):
+    """The sign-uniform window paths (q >= 0: F = phi+(q_j); q <= 0: F = phi-(q_{j+1})) and
+    the general path side by side, against the oracle: K2 at every V, the resident stepper
+    K6 (the plan's default at this size) and the persistent K2P."""
+    delta, lam = ("1e-5", Fraction(4, 15)) if case == "p1" else ("1e-5", Fraction(3, 10))
+    n = 3 * 65536 + 11
+    rng = np.random.default_rng(V * 7 + kernel + patch)
+    q0 = _sign_patch_data(rng, n, 100000, patch)
+    plan = F.fqnm_plan_ex(n, float(Fraction(delta)), float(lam), F.BURGERS_EO)
+    assert plan.info()["rule"] == (5 if case == "p1" else 2)
+    if kernel == 6:
+        assert plan.info()["kernel"] == 6
+    else:
+        F.fqnm_debug_override(plan, kernel, 0, V)
+    q = to_dev(q0)
+    F.fqnm_step(plan, q, 150)
+    ref = oracle.Rule(W.BURGERS_EO, delta, lam).run(q0, 150)
+    assert np.array_equal(host(q), ref)
 
 
 def test_ens1_sampled(F):
