@@ -211,6 +211,8 @@ struct fqnm_plan {
     void* pipe_buf[3] = {nullptr, nullptr, nullptr};
     int32_t* pipe_head = nullptr;        // copy of q_host[0, H) taken before any D2H (the last
                                          // chunk's periodic right halo)
+    int* md_guard = nullptr;             // 2D/3D: state left [lo, hi] during a call (device)
+    int* md_guard_host = nullptr;
     int* pipe_guard = nullptr;           // one flag per chunk
     int* pipe_guard_host = nullptr;
     int64_t pipe_guard_n = 0;
@@ -732,6 +734,14 @@ extern "C" int fqnm_plan(fqnm_plan_t** out, int64_t N, double delta, double dt_d
     return fqnm_plan_ex(out, &d);
 }
 
+// multi-D admissible range: see the 2D/3D range guard below
+static void md_clamp_range(fqnm_plan_t* p, int dims)
+{
+    const int64_t lim = (int64_t)INT32_MAX / (1 + 4 * dims);
+    if (p->hi > lim) p->hi = lim;
+    if (p->lo < -lim) p->lo = -lim;
+}
+
 extern "C" int fqnm_plan_2d(fqnm_plan_t** out, int64_t nx, int64_t ny, double delta, double dt_dx,
                             double dt_dy, int flux_kind, int boundary, double param_x, double param_y)
 {
@@ -772,6 +782,7 @@ extern "C" int fqnm_plan_2d(fqnm_plan_t** out, int64_t nx, int64_t ny, double de
     if (p->rule != py->rule) p->rule = R_GENERIC;          // both directions on the int64 path
     p->lo = p->lo > py->lo ? p->lo : py->lo;
     p->hi = p->hi < py->hi ? p->hi : py->hi;
+    md_clamp_range(p, 2);
     p->dep_left = p->dep_left || py->dep_left;
     p->dep_right = p->dep_right || py->dep_right;
     delete py;
@@ -782,7 +793,9 @@ extern "C" int fqnm_plan_2d(fqnm_plan_t** out, int64_t nx, int64_t ny, double de
     cudaError_t e;
     if ((e = cudaMalloc(&p->scratch, p->scratch_bytes)) != cudaSuccess ||
         (e = cudaMalloc(&p->d_minmax, 2 * sizeof(long long))) != cudaSuccess ||
-        (e = cudaMallocHost(&p->h_minmax, 4 * sizeof(long long))) != cudaSuccess) {
+        (e = cudaMallocHost(&p->h_minmax, 4 * sizeof(long long))) != cudaSuccess ||
+        (e = cudaMalloc(&p->md_guard, sizeof(int))) != cudaSuccess ||
+        (e = cudaMallocHost(&p->md_guard_host, sizeof(int))) != cudaSuccess) {
         fqnm_destroy(p);
         return fail(FQNM_ERR_NOMEM, "allocating 2D plan buffers: %s", cudaGetErrorString(e));
     }
@@ -838,6 +851,7 @@ extern "C" int fqnm_plan_3d(fqnm_plan_t** out, int64_t nx, int64_t ny, int64_t n
         p->hi = p->hi < pd[m]->hi ? p->hi : pd[m]->hi;
         delete pd[m];
     }
+    md_clamp_range(p, 3);
     p->family = 8;
     p->V = 0;
     p->k = 1;
@@ -845,7 +859,9 @@ extern "C" int fqnm_plan_3d(fqnm_plan_t** out, int64_t nx, int64_t ny, int64_t n
     cudaError_t e;
     if ((e = cudaMalloc(&p->scratch, p->scratch_bytes)) != cudaSuccess ||
         (e = cudaMalloc(&p->d_minmax, 2 * sizeof(long long))) != cudaSuccess ||
-        (e = cudaMallocHost(&p->h_minmax, 4 * sizeof(long long))) != cudaSuccess) {
+        (e = cudaMallocHost(&p->h_minmax, 4 * sizeof(long long))) != cudaSuccess ||
+        (e = cudaMalloc(&p->md_guard, sizeof(int))) != cudaSuccess ||
+        (e = cudaMallocHost(&p->md_guard_host, sizeof(int))) != cudaSuccess) {
         fqnm_destroy(p);
         return fail(FQNM_ERR_NOMEM, "allocating 3D plan buffers: %s", cudaGetErrorString(e));
     }
@@ -863,6 +879,8 @@ static void pipe_release(fqnm_plan_t* p)
     }
     if (p->pipe_head) cudaFree(p->pipe_head);
     p->pipe_head = nullptr;
+    if (p->md_guard) cudaFree(p->md_guard);
+    if (p->md_guard_host) cudaFreeHost(p->md_guard_host);
     if (p->pipe_guard) cudaFree(p->pipe_guard);
     if (p->pipe_guard_host) cudaFreeHost(p->pipe_guard_host);
     p->pipe_guard = nullptr;
@@ -961,6 +979,41 @@ static int prof_end(fqnm_plan_t* p)
         if ((rc_ = prof_end(p)) != FQNM_OK) return rc_;    \
         p->launches++;                                     \
     } while (0)
+
+// ---- 2D/3D range guard: the unsplit directional composition (Thm P:364-401)
+// is not monotone in general once quantised (the per-direction increments of phi+ - phi-
+// can add up past 1), so the maximum principle that keeps a 1D state inside the plan's
+// admissible range [lo, hi] (where the fast closed-form maps are exact) is not available.
+// The 2D/3D kernels compare every cell they store with [lo, hi] and set a device flag;
+// the next launches return at once when it is set, and fqnm_step reports FQNM_ERR_RANGE
+// after the loop (q unspecified then).  The multi-D range is clamped at plan time to
+// |q| <= (2^31 - 1) / (1 + 4d), so the one step that leaves it cannot wrap int32.
+static void md_guard_args(fqnm_plan_t* p, int** guard, int32_t* glo, int32_t* ghi)
+{
+    const bool on = p->md_guard && p->d.check_range;
+    *guard = on ? p->md_guard : nullptr;
+    *glo = (int32_t)(p->lo < INT32_MIN ? INT32_MIN : p->lo);
+    *ghi = (int32_t)(p->hi > INT32_MAX ? INT32_MAX : p->hi);
+}
+
+static cudaError_t md_guard_reset(fqnm_plan_t* p)
+{
+    if (!p->md_guard || !p->d.check_range) return cudaSuccess;
+    return cudaMemsetAsync(p->md_guard, 0, sizeof(int), p->st);
+}
+
+
+static int md_guard_result(fqnm_plan_t* p)
+{
+    if (!p->md_guard || !p->d.check_range) return FQNM_OK;
+    CUDA_TRY(cudaMemcpyAsync(p->md_guard_host, p->md_guard, sizeof(int), cudaMemcpyDeviceToHost, p->st));
+    CUDA_TRY(cudaStreamSynchronize(p->st));
+    if (*p->md_guard_host)
+        return fail(FQNM_ERR_RANGE, "the 2D/3D state left the plan's admissible range [%lld, %lld] "
+                    "during the call (the unsplit composition is not monotone); q is unspecified",
+                    (long long)p->lo, (long long)p->hi);
+    return FQNM_OK;
+}
 
 static int bmode_of(const fqnm_plan_desc& d)
 {
@@ -1138,6 +1191,8 @@ extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
         a.ny = p->ny;
         a.ksteps = (int32_t)step2d_stream_rows(p->nx, p->ny);
         a.bmode = bm;
+        md_guard_args(p, &a.guard, &a.glo, &a.ghi);
+        CUDA_TRY(md_guard_reset(p));
         for (int64_t s = 0; s < nsteps;) {
             a.src = (const int32_t*)bufs[cur];
             a.dst = (int32_t*)bufs[cur ^ 1];
@@ -1152,12 +1207,13 @@ extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
             cur ^= 1;
         }
         if (cur != 0) CUDA_TRY(cudaMemcpyAsync(q, bufs[cur], bytes, cudaMemcpyDeviceToDevice, p->st));
-        return FQNM_OK;
+        return md_guard_result(p);
     }
     if (p->family == 7) {
         int64_t nb = (nsteps + p->k - 1) / p->k;
         if (nb % 2 == 1 && nsteps >= nb + 1) nb += 1;
         const int64_t base = nsteps / nb, rem = nsteps % nb;
+        CUDA_TRY(md_guard_reset(p));
         for (int64_t b = 0; b < nb; ++b) {
             Step2DArgs a;
             a.src = (const int32_t*)bufs[cur];
@@ -1166,11 +1222,12 @@ extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
             a.ny = p->ny;
             a.ksteps = (int)(base + (b < rem ? 1 : 0));
             a.bmode = bm;
+            md_guard_args(p, &a.guard, &a.glo, &a.ghi);
             PROF_LAUNCH(launch_step2d(p->rule, p->same_xy, a, p->dr, p->dry, p->st));
             cur ^= 1;
         }
         if (cur != 0) CUDA_TRY(cudaMemcpyAsync(q, bufs[cur], bytes, cudaMemcpyDeviceToDevice, p->st));
-        return FQNM_OK;
+        return md_guard_result(p);
     }
     if (p->family == 8) {
         Step3DArgs a;
@@ -1180,6 +1237,8 @@ extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
         a.nz = p->nz;
         a.zchunk = p->stream3d ? step3d_s_zchunk(p->nx, p->ny, p->nz) : step3d_zchunk(p->nx, p->ny, p->nz);
         a.bmode = bm;
+        md_guard_args(p, &a.guard, &a.glo, &a.ghi);
+        CUDA_TRY(md_guard_reset(p));
         for (int64_t s = 0; s < nsteps; ++s) {
             a.src = (const int32_t*)bufs[cur];
             a.dst = (int32_t*)bufs[cur ^ 1];
@@ -1190,7 +1249,7 @@ extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
             cur ^= 1;
         }
         if (cur != 0) CUDA_TRY(cudaMemcpyAsync(q, bufs[cur], bytes, cudaMemcpyDeviceToDevice, p->st));
-        return FQNM_OK;
+        return md_guard_result(p);
     }
     if (p->family == 1 || p->family == 5) {
         for (int64_t s = 0; s < nsteps; ++s) {

@@ -112,6 +112,10 @@ struct Step2DArgs {
     int64_t nx, ny;
     int32_t ksteps;
     int32_t bmode;
+    // optional range guard (2D/3D): *guard != 0 -> the launch does nothing;
+    // a stored cell outside [glo, ghi] sets *guard
+    int* guard;
+    int32_t glo, ghi;
 };
 cudaError_t launch_step2d(int rule, bool same, const Step2DArgs& a, const DevRule& rx,
                           const DevRule& ry, cudaStream_t st);
@@ -131,6 +135,8 @@ struct Step3DArgs {
     int64_t zchunk;     // z planes per CTA
     int32_t bmode;
     int32_t xt0;        // first x tile of the launch (set by launch_step3d)
+    int* guard;         // optional range guard, as Step2DArgs
+    int32_t glo, ghi;
 };
 cudaError_t launch_step3d(int rule, bool same, const Step3DArgs& a, const DevRule& rx,
                           const DevRule& ry, const DevRule& rz, cudaStream_t st);

@@ -99,19 +99,26 @@ struct K9Ring {
 // store the lane's cells of an output row: 8-byte pieces on the fast path (the halo
 // pairs at the strip ends are skipped), guarded scalar stores otherwise
 __device__ __forceinline__ void k9_store(int32_t* row, bool vec, int lane, int xl,
-                                         const int32_t (&out)[K9_V], const bool (&st)[K9_V])
+                                         const int32_t (&out)[K9_V], const bool (&st)[K9_V],
+                                         const Step2DArgs& a)
 {
     if (vec) {
 #pragma unroll
         for (int h = 0; h < K9_V / 2; ++h) {
             const int p = lane * K9_V + 2 * h;
-            if (p >= K9_H && p < K9_W - K9_H)
+            if (p >= K9_H && p < K9_W - K9_H) {
                 *reinterpret_cast<int2*>(row + xl + 2 * h) = make_int2(out[2 * h], out[2 * h + 1]);
+                md_note(a.guard, out[2 * h], a.glo, a.ghi);
+                md_note(a.guard, out[2 * h + 1], a.glo, a.ghi);
+            }
         }
     } else {
 #pragma unroll
         for (int j = 0; j < K9_V; ++j)
-            if (st[j]) row[xl + j] = out[j];
+            if (st[j]) {
+                row[xl + j] = out[j];
+                md_note(a.guard, out[j], a.glo, a.ghi);
+            }
     }
 }
 
@@ -199,6 +206,7 @@ __device__ __forceinline__ void update_row(const Row2<RULE, SAME>& B, const Row2
 template <int RULE, bool SAME>
 __global__ void K9_LB1 k_step2d_s(Step2DArgs a, DevRule rx, DevRule ry)
 {
+    if (a.guard && *a.guard) return;                    // state left the range earlier
     constexpr int V = K9_V;
     const int lane = threadIdx.x & 31;
     const int warp = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
@@ -257,7 +265,7 @@ __global__ void K9_LB1 k_step2d_s(Step2DArgs a, DevRule rx, DevRule ry)
         Nn.eval(rx, ry);
         int32_t out[V];
         update_row<RULE, SAME, false>(Bp, C, Nn, xl, nx, false, false, false, out);
-        k9_store(a.dst + r * nx, vec, lane, xl, out, st);
+        k9_store(a.dst + r * nx, vec, lane, xl, out, st, a);
         sz = sn;
     };
     int r = y0;
@@ -281,6 +289,7 @@ __global__ void K9_LB1 k_step2d_s(Step2DArgs a, DevRule rx, DevRule ry)
 template <int RULE, bool SAME>
 __global__ void K9_LB2 k_step2d_s2(Step2DArgs a, DevRule rx, DevRule ry)
 {
+    if (a.guard && *a.guard) return;                    // state left the range earlier
     constexpr int V = K9_V, L = K9_LOOK;
     const int lane = threadIdx.x & 31;
     const int warp = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
@@ -304,6 +313,12 @@ __global__ void K9_LB2 k_step2d_s2(Step2DArgs a, DevRule rx, DevRule ry)
     for (int j = 0; j < V; ++j) {
         const int p = lane * V + j, x = xl + j;
         stc[j] = p >= K9_H && p < K9_W - K9_H && x >= 0 && x < nx;
+    }
+    bool ck1[V];                                           // valid step-1 cells of the strip
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        const int p = lane * V + j, x = xl + j;
+        ck1[j] = p >= 1 && p < K9_W - 1 && x >= 0 && x < nx;
     }
     __shared__ int2 ring[L][256 / 32][K9_V / 2][32];
     K9Ring rg;
@@ -329,13 +344,18 @@ __global__ void K9_LB2 k_step2d_s2(Step2DArgs a, DevRule rx, DevRule ry)
             const int r = t - 1;
             if (wall) update_row<RULE, SAME, true>(A0, B0, C0, xl, nx, xwall, r == 0, r == ny - 1, C1.q);
             else update_row<RULE, SAME, false>(A0, B0, C0, xl, nx, false, false, false, C1.q);
+            if (a.guard && r >= 0 && r < ny) {             // range guard on the step-1 row
+#pragma unroll
+                for (int j = 0; j < V; ++j)
+                    if (ck1[j]) md_note(a.guard, C1.q[j], a.glo, a.ghi);
+            }
             C1.eval(rx, ry);
             if (t >= y0 + 2) {                             // step-2 row t - 2: store
                 const int r2 = t - 2;
                 int32_t out[V];
                 if (wall) update_row<RULE, SAME, true>(A1, B1, C1, xl, nx, xwall, r2 == 0, r2 == ny - 1, out);
                 else update_row<RULE, SAME, false>(A1, B1, C1, xl, nx, false, false, false, out);
-                k9_store(a.dst + r2 * nx, vec, lane, xl, out, stc);
+                k9_store(a.dst + r2 * nx, vec, lane, xl, out, stc, a);
             }
         }
     };

@@ -17,6 +17,7 @@
 // HBM traffic: the state is read and written once per step, 8 B per cell-update
 // (int32), plus the halo rows (L2 hits for interior tiles).
 // Indices are 32-bit (the planner guarantees nx * ny * nz < 2^31).
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -104,6 +105,7 @@ template <int RULE, bool SAME, bool VEC>
 __global__ void __launch_bounds__(32 * K8_WARPS, k8_minb<RULE>()) k_step3d(Step3DArgs a, DevRule rx, DevRule ry,
                                                         DevRule rz)
 {
+    if (a.guard && *a.guard) return;                    // state left the range earlier
     constexpr int V = K8_V;
     // y maps of the plane, per row; double-buffered by plane parity so one barrier per
     // plane suffices (a warp writing buffer b for plane z + 2 has passed the barrier of
@@ -242,10 +244,15 @@ __global__ void __launch_bounds__(32 * K8_WARPS, k8_minb<RULE>()) k_step3d(Step3
                 if (vec) {
                     *reinterpret_cast<int4*>(a.dst + base + xl) =
                         make_int4(out[0], out[1], out[2], out[3]);
+#pragma unroll
+                    for (int j = 0; j < V; ++j) md_note(a.guard, out[j], a.glo, a.ghi);
                 } else {
 #pragma unroll
                     for (int j = 0; j < V; ++j)
-                        if (xl + j < nx) a.dst[base + xl + j] = out[j];
+                        if (xl + j < nx) {
+                            a.dst[base + xl + j] = out[j];
+                            md_note(a.guard, out[j], a.glo, a.ghi);
+                        }
                 }
             }
         }
@@ -270,16 +277,18 @@ static cudaError_t step3d_rule(bool same, const Step3DArgs& a0, const DevRule& r
     Step3DArgs a = a0;
     dim3 block(32 * K8_WARPS);
     constexpr size_t dyn = (size_t)(K8_LOOK + 1) * K8_WARPS * 32 * sizeof(int4);
-    static unsigned long long attr_set = 0;                // once per instantiation and device
+    // once per instantiation and device (devices >= 64: every launch); atomic, so host
+    // threads launching concurrently do not race on the mask
+    static std::atomic<unsigned long long> attr_set{0};
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64 || !(attr_set >> dev & 1ull)) {
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64 || !(attr_set.load() >> dev & 1ull)) {
         for (auto f : {k_step3d<RULE, true, true>, k_step3d<RULE, false, true>,
                        k_step3d<RULE, true, false>, k_step3d<RULE, false, false>}) {
             cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)dyn);
             if (e != cudaSuccess) return e;
         }
-        if (dev < 64) attr_set |= 1ull << dev;
+        if (dev < 64) attr_set.fetch_or(1ull << dev);
     }
     const unsigned gy = (unsigned)((a.ny + K8_TY - 1) / K8_TY);
     const unsigned gz = (unsigned)((a.nz + a.zchunk - 1) / a.zchunk);

@@ -76,6 +76,7 @@ template <int RULE, bool SAME>
 __global__ void __launch_bounds__(32 * K10_WARPS) k_step3d_s(Step3DArgs a, DevRule rx, DevRule ry,
                                                            DevRule rz)
 {
+    if (a.guard && *a.guard) return;                    // state left the range earlier
     constexpr int V = K10_V, R = K10_R, L = K10_LOOK, S = K10_LOOK + 1;
     constexpr int NR = R + 2;                              // loaded rows per plane
     __shared__ int4 ring[S][K10_WARPS][NR][32];
@@ -211,10 +212,16 @@ __global__ void __launch_bounds__(32 * K10_WARPS) k_step3d_s(Step3DArgs a, DevRu
                     } else {
                         *reinterpret_cast<int2*>(row + xl) = make_int2(out[0], out[1]);
                     }
+#pragma unroll
+                    for (int j = 0; j < V; ++j)
+                        if ((lane > 0 || j >= 2) && (lane < 31 || j < 2)) md_note(a.guard, out[j], a.glo, a.ghi);
                 } else {
 #pragma unroll
                     for (int j = 0; j < V; ++j)
-                        if (stc[j]) row[xl + j] = out[j];
+                        if (stc[j]) {
+                            row[xl + j] = out[j];
+                            md_note(a.guard, out[j], a.glo, a.ghi);
+                        }
                 }
             }
         }

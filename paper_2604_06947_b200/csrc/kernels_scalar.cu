@@ -440,7 +440,10 @@ __device__ __noinline__ void slow_window(const BlockedArgs& a, const DevRule& r,
     const int64_t g0 = ws + lane * V;
     int32_t q[V];
 #pragma unroll
-    for (int j = 0; j < V; ++j) q[j] = src[wrap_index(g0 + j, n, a.bmode, a.halo)];
+    for (int j = 0; j < V; ++j) {
+        const int32_t* x = src + wrap_index(g0 + j, n, a.bmode, a.halo);
+        q[j] = a.p2p ? __ldcg(x) : *x;          // p2p: halos written by a peer in this launch
+    }
     if (a.bmode == BM_TRANSMISSIVE)
         run_window_steps<RULE, V, true>(q, a.ksteps, r, g0, n);
     else
@@ -525,10 +528,20 @@ __global__ void __launch_bounds__(256, MINB) k_blocked(BlockedArgs a, DevRule r)
 #endif
             {
                 const int4* s4 = reinterpret_cast<const int4*>(a.src + boff + ws) + lane * (V / 4);
+                if (a.p2p && ws < 0) {
+                    // the left halo was written by the peer GPU during this launch (released
+                    // by its flag): coherent L2 loads, not the read-only path
 #pragma unroll
-                for (int j = 0; j < V / 4; ++j) {
-                    int4 v = __ldg(s4 + j);
-                    q[4 * j] = v.x; q[4 * j + 1] = v.y; q[4 * j + 2] = v.z; q[4 * j + 3] = v.w;
+                    for (int j = 0; j < V / 4; ++j) {
+                        int4 v = __ldcg(s4 + j);
+                        q[4 * j] = v.x; q[4 * j + 1] = v.y; q[4 * j + 2] = v.z; q[4 * j + 3] = v.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < V / 4; ++j) {
+                        int4 v = __ldg(s4 + j);
+                        q[4 * j] = v.x; q[4 * j + 1] = v.y; q[4 * j + 2] = v.z; q[4 * j + 3] = v.w;
+                    }
                 }
             }
 #if FQNM_PREFETCH
@@ -882,6 +895,7 @@ __global__ void __launch_bounds__(256, k6_minb<RULE>()) k_resident(ResidentArgs 
 template <int RULE, bool SAME, bool WALL>
 __global__ void __launch_bounds__(512) k_step2d(Step2DArgs a, DevRule rx, DevRule ry)
 {
+    if (a.guard && *a.guard) return;                    // state left the range earlier
     extern __shared__ int32_t sm2[];
     constexpr int TX = STEP2D_TX, TY = STEP2D_TY;
     constexpr int NA = (TX + 2 * STEP2D_KMAX + 31) / 32;       // cell columns per thread
@@ -959,6 +973,13 @@ __global__ void __launch_bounds__(512) k_step2d(Step2DArgs a, DevRule rx, DevRul
                         if (gj == ny - 1) tyr = PY[i] + MY[i];
                     }
                     q[b][c] = q[b][c] + txl - txr + tyl - tyr;
+                    // range guard on the intermediate steps too (valid cells of the
+                    // shrinking trapezoid inside the domain; the last step at the store)
+                    if (a.guard && s + 1 < K && x > s && x < RX - 1 - s && y > s && y < RY - 1 - s) {
+                        const int64_t gi = ox + x, gj = oy + y;
+                        if (gi >= 0 && gi < nx && gj >= 0 && gj < ny)
+                            md_note(a.guard, q[b][c], a.glo, a.ghi);
+                    }
                 }
             }
         if (s + 1 < K) {
@@ -972,8 +993,10 @@ __global__ void __launch_bounds__(512) k_step2d(Step2DArgs a, DevRule rx, DevRul
         for (int c = 0; c < NA; ++c) {
             const int x = tx + 32 * c, y = ty + 16 * b;
             const int64_t gi = ox + x, gj = oy + y;
-            if (x >= K && x < K + TX && y >= K && y < K + TY && gi < nx && gj < ny)
+            if (x >= K && x < K + TX && y >= K && y < K + TY && gi < nx && gj < ny) {
                 a.dst[gj * nx + gi] = q[b][c];
+                md_note(a.guard, q[b][c], a.glo, a.ghi);
+            }
         }
 }
 

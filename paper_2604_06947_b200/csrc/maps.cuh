@@ -291,4 +291,11 @@ __device__ __forceinline__ int32_t transfer_lr(int32_t qL, int32_t qR, const Dev
     return pL + mR;
 }
 
+// 2D/3D range guard: a stored cell outside the plan's admissible range [lo, hi] (where
+// the fast closed-form maps are proven exact) flags the call (fqnm_api.cu md_guard_*)
+__device__ __forceinline__ void md_note(int* guard, int32_t v, int32_t lo, int32_t hi)
+{
+    if (guard && (v < lo || v > hi)) atomicOr(guard, 1);
+}
+
 }  // namespace fqnm
