@@ -298,7 +298,7 @@ def timed(do_step, args, world, local, plan, stepper_plans):
 
 
 def alu_roofline(kernel: str, ops_alg: int, updates_per_launch: float, per_launch_ms: float,
-                 hbm_bytes_per_launch: float, extra: dict):
+                 hbm_bytes_per_launch: float, extra: dict, mix_ceiling_key: str = ""):
     peaks, peak_src = _peaks()
     f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
     peak_ops = SM_COUNT * LANES_PER_SM_CLK * f_max                    # int lane-ops/s at max clock
@@ -326,6 +326,15 @@ def alu_roofline(kernel: str, ops_alg: int, updates_per_launch: float, per_launc
             roof["measured_issue_peak"] = mp / 1e12
             roof["frac_vs_measured_issue_peak"] = achieved_ops / mp
             roof["measured_peak_source"] = src
+        # and against the compute-only ceiling of the kernel's own instruction mix: the
+        # sign-uniform EO step on register data (no loads/stores), same occupancy
+        e = micro.get("eo_sign_step", {})
+        if mix_ceiling_key == "eo_sign_step" and e.get("lane_ops_per_clk_per_sm"):
+            ceil_ops = e["lane_ops_per_clk_per_sm"] * SM_COUNT * f_max
+            roof["mix_ceiling"] = {"what": "K2 sign-uniform step on register data, 7 instr/cell "
+                                           "(tools/micro.cu k_eo_sign_step)",
+                                   "achieved_frac": achieved_ops / ceil_ops,
+                                   "ceiling_ops": ceil_ops / 1e12}
     return roof
 
 
@@ -422,7 +431,8 @@ def run_cfg4(args):
         {"kernel_launches": kern_launches, "kernel_share_of_step": kern_ms / ms if ms > 0 else None,
          "k": info["k"], "V": info["cells_per_thread"], "ops_basis": ops_key,
          "windows_redundancy": 32.0 * info["cells_per_thread"] / (
-             32.0 * info["cells_per_thread"] - 2 * ((info["k"] + 3) // 4 * 4))})
+             32.0 * info["cells_per_thread"] - 2 * ((info["k"] + 3) // 4 * 4))},
+        mix_ceiling_key="eo_sign_step" if ops_key == "burgers_eo_sign_uniform" else "")
     tr, tr_src = ncu_traffic(n_local)
     if tr is not None:
         roofline["traffic"] = tr

@@ -91,6 +91,9 @@ __device__ __forceinline__ void eval_maps(const int32_t (&q)[V], int32_t (&g)[V]
 // >= 0 stays >= 0 inside its dependence cone for all k steps, so there phi- = 0 and the
 // interface transfer is F_{j+1/2} = phi+(q_j) = g_j; for q <= 0, F_{j+1/2} = phi-(q_{j+1})
 // = g_{j+1}.  Cells outside the cone are cut off by the caller either way.
+#ifndef FQNM_LIN_STREAM
+#define FQNM_LIN_STREAM 0      // LIN kappa = 1/2 step streamed cell by cell (variant)
+#endif
 #ifndef FQNM_SIGN_STREAM
 #define FQNM_SIGN_STREAM 1     // sign-uniform step: maps evaluated cell by cell (no map array)
 #endif
@@ -157,6 +160,21 @@ __device__ __forceinline__ void one_step(int32_t (&q)[V], const DevRule& r, int 
             for (int j = 0; j + 1 < V; ++j) q[j] = q[j] + g[j] - g[j + 1];
             q[V - 1] = q[V - 1] + g[V - 1] - gr;
         }
+    } else if (FQNM_LIN_STREAM && RULE == R_LIN_HALF && !WALL) {
+        // kappa = 1/2 streamed: phi+ of the lane's last cell first (for the shuffle),
+        // then cell by cell h_j = trunc(q_j/2), q'_j = phi+(q_{j-1}) + h_j (no arrays)
+        const int32_t hl = q[V - 1] / 2;
+        const int32_t plast = hl * r.mone + q[V - 1];
+        int32_t pp = NB == 0 ? __shfl_up_sync(FULL, plast, 1)
+                             : __shfl_sync(FULL, plast, (lane + 31) & 31);
+#pragma unroll
+        for (int j = 0; j + 1 < V; ++j) {
+            const int32_t h = q[j] / 2;
+            const int32_t p = h * r.mone + q[j];
+            q[j] = pp * r.one + h;
+            pp = p;
+        }
+        q[V - 1] = pp * r.one + hl;
     } else if (RULE == R_LIN_HALF && !WALL) {
         // kappa = 1/2: q'_j = trunc(q_j/2) + phi+(q_{j-1}), phi+ = q - trunc(q/2).
         // The runtime r.one turns the two adds into IMADs (FMA pipe) so the

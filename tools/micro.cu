@@ -1,0 +1,207 @@
+// Per-pipe issue-rate microbenchmarks on the B200 (SURVEY §2.5 K8,
+// §8(d)-D3 "confirm with microbenchmarks").  Each kernel runs long chains of ONE SASS
+// instruction class (checked with cuobjdump -sass, see tools/micro.py), 8 independent
+// chains per thread, 2 CTAs x 512 threads per SM (32 warps), every CTA co-resident, and
+// reports lane-operations per SM clock: total lane-ops / 148 / (max CTA clock64 span).
+// The "eo_sign_step" kernel is the K2 sign-uniform step itself (maps.cuh eo_g_biased +
+// the update, V = 32 cells per lane, one shuffle per step) on register data: the
+// compute-only ceiling of the headline kernel's instruction mix.
+//
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I csrc -I include
+//        tools/micro.cu -o tools/micro     (tools/micro.py does this)
+#include <cstdio>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "fqnm_internal.h"
+#include "maps.cuh"
+
+using namespace fqnm;
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
+    fprintf(stderr, "%s: %s\n", #x, cudaGetErrorString(e_)); return 1; } } while (0)
+
+constexpr int ITERS = 4096;
+constexpr int CH = 8;           // independent chains per thread
+
+struct Span { unsigned long long t0, t1; };
+
+__device__ __forceinline__ void span_begin(unsigned long long& t0) { t0 = clock64(); }
+__device__ __forceinline__ void span_end(Span* s, unsigned long long t0)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) { s[blockIdx.x].t0 = t0; s[blockIdx.x].t1 = clock64(); }
+}
+
+// ---- single-class kernels (8 ops per iteration per chain group) ----
+#define CHAIN_KERNEL(NAME, TYPE, INIT, OP)                                              \
+__global__ void __launch_bounds__(512, 2) NAME(TYPE* out, Span* sp, TYPE a, TYPE b)    \
+{                                                                                       \
+    unsigned long long t0; __syncthreads(); span_begin(t0);                             \
+    TYPE x[CH];                                                                          \
+    _Pragma("unroll") for (int c = 0; c < CH; ++c) x[c] = INIT;                         \
+    for (int i = 0; i < ITERS; ++i) {                                                   \
+        _Pragma("unroll") for (int c = 0; c < CH; ++c) { OP; }                          \
+    }                                                                                   \
+    TYPE s = x[0];                                                                       \
+    _Pragma("unroll") for (int c = 1; c < CH; ++c) s = s + x[c];                        \
+    if (s == a) out[threadIdx.x] = s;                                                   \
+    span_end(sp, t0);                                                                   \
+}
+
+CHAIN_KERNEL(k_iadd3, int32_t, (int32_t)(threadIdx.x + c),
+             asm volatile("add.s32 %0, %0, %1;\n\tadd.s32 %0, %0, %2;" : "+r"(x[c]) : "r"(a), "r"(b)))
+CHAIN_KERNEL(k_lop3, int32_t, (int32_t)(threadIdx.x + c),
+             asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[c]) : "r"(a), "r"(b)))
+CHAIN_KERNEL(k_imad, int32_t, (int32_t)(threadIdx.x + c),
+             asm volatile("mad.lo.s32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(a), "r"(b)))
+CHAIN_KERNEL(k_imad_hi, int32_t, (int32_t)(threadIdx.x + c),
+             asm volatile("mad.hi.s32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(a), "r"(b)))
+CHAIN_KERNEL(k_ffma, float, (float)(threadIdx.x + c),
+             asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(x[c]) : "f"(a), "f"(b)))
+CHAIN_KERNEL(k_dfma, double, (double)(threadIdx.x + c),
+             asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(x[c]) : "d"(a), "d"(b)))
+CHAIN_KERNEL(k_i2fp, int32_t, (int32_t)(threadIdx.x + c),
+             { float t; asm volatile("cvt.rn.f32.s32 %0, %1;" : "=f"(t) : "r"(x[c]));
+               x[c] = __float_as_int(t) >> 8; })
+CHAIN_KERNEL(k_lea_hi, int32_t, (int32_t)(threadIdx.x + c),
+             { int32_t t = x[c] >> 31; asm volatile("add.s32 %0, %0, %1;" : "+r"(x[c]) : "r"(t)); x[c] ^= a; })
+
+// ---- mixed streams: ALU + FMA-pipe interleaved 1:1 (independent chains) ----
+__global__ void __launch_bounds__(512, 2) k_mixed_alu_fma(int32_t* out, Span* sp, int32_t a, int32_t b)
+{
+    unsigned long long t0; __syncthreads(); span_begin(t0);
+    int32_t x[CH], y[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) { x[c] = threadIdx.x + c; y[c] = threadIdx.x - c; }
+    for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[c]) : "r"(a), "r"(b));
+            asm volatile("mad.lo.s32 %0, %0, %1, %2;" : "+r"(y[c]) : "r"(a), "r"(b));
+        }
+    }
+    int32_t s = 0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) s += x[c] ^ y[c];
+    if (s == 123456789) out[threadIdx.x] = s;
+    span_end(sp, t0);
+}
+
+__global__ void __launch_bounds__(512, 2) k_shfl(int32_t* out, Span* sp, int32_t a, int32_t b)
+{
+    unsigned long long t0; __syncthreads(); span_begin(t0);
+    int32_t x[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) x[c] = threadIdx.x + c;
+    for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) x[c] = __shfl_up_sync(0xffffffffu, x[c], 1);
+    }
+    int32_t s = 0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) s += x[c];
+    if (s == 123456789) out[threadIdx.x] = s;
+    span_end(sp, t0);
+}
+
+// ---- the K2 sign-uniform step on register data (V = 32, 256-thread CTAs, 2 per SM,
+// 128 registers: the headline kernel's configuration without its loads/stores) ----
+constexpr int SV = 32;
+constexpr int SSTEPS = 256;
+__global__ void __launch_bounds__(256, 2) k_eo_sign_step(int32_t* out, Span* sp, DevRule r, int32_t seed)
+{
+    unsigned long long t0; __syncthreads(); span_begin(t0);
+    const int lane = threadIdx.x & 31;
+    int32_t q[SV];
+#pragma unroll
+    for (int j = 0; j < SV; ++j) q[j] = 100000 + ((seed + 37 * j + 11 * (int)threadIdx.x) & 4095);
+    for (int s = 0; s < SSTEPS; ++s) {
+        const int32_t glast = eo_g_biased<R_EO_P1, true>(q[SV - 1], r);
+        int32_t gp = __shfl_up_sync(0xffffffffu, glast, 1);
+#pragma unroll
+        for (int j = 0; j + 1 < SV; j += 2) {
+            const int32_t g0 = eo_g_biased<R_EO_P1, false>(q[j], r);
+            q[j] = q[j] + gp - g0;
+            if (j + 2 < SV) {
+                const int32_t g1 = eo_g_biased<R_EO_P1, true>(q[j + 1], r);
+                q[j + 1] = q[j + 1] + g0 - g1;
+                gp = g1;
+            } else {
+                gp = g0;
+            }
+        }
+        q[SV - 1] = q[SV - 1] + gp - glast;
+        if (lane == 0) q[0] = 100000;        // keep the window's data positive and bounded
+    }
+    int32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < SV; ++j) acc ^= q[j];
+    if (acc == 123456789) out[threadIdx.x] = acc;
+    span_end(sp, t0);
+}
+
+int main(int argc, char** argv)
+{
+    const int sms = 148;
+    Span* sp;
+    void* out;
+    CK(cudaMalloc(&sp, sms * 4 * sizeof(Span)));
+    CK(cudaMalloc(&out, 4096 * 8));
+    std::vector<Span> h(sms * 4);
+    auto measure = [&](const char* name, const char* sass, int blocks_per_sm, int threads,
+                       double lane_ops_per_thread, auto launch) -> int {
+        const int blocks = sms * blocks_per_sm;
+        double best = 0, best_ns = 0;
+        for (int rep = 0; rep < 5; ++rep) {
+            cudaEvent_t e0, e1;
+            cudaEventCreate(&e0); cudaEventCreate(&e1);
+            cudaEventRecord(e0);
+            launch(blocks, threads);
+            cudaEventRecord(e1);
+            CK(cudaEventSynchronize(e1));
+            CK(cudaGetLastError());
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            CK(cudaMemcpy(h.data(), sp, blocks * sizeof(Span), cudaMemcpyDeviceToHost));
+            unsigned long long span = 0;
+            for (int b = 0; b < blocks; ++b) span = h[b].t1 - h[b].t0 > span ? h[b].t1 - h[b].t0 : span;
+            const double ops_sm = lane_ops_per_thread * threads * blocks_per_sm;
+            const double rate = ops_sm / (double)span;
+            if (rate > best) { best = rate; best_ns = ms * 1e6; }
+            cudaEventDestroy(e0); cudaEventDestroy(e1);
+        }
+        printf("{\"name\": \"%s\", \"sass\": \"%s\", \"lane_ops_per_clk_per_sm\": %.3f, "
+               "\"warp_instr_per_clk_per_smsp\": %.4f, \"kernel_ns\": %.0f, "
+               "\"lane_ops_per_s\": %.6e}\n",
+               name, sass, best, best / 128.0, best_ns,
+               lane_ops_per_thread * threads * blocks / (best_ns * 1e-9));
+        return 0;
+    };
+    const double n1 = (double)ITERS * CH;
+    int32_t a = 3, b = 5;
+#define L1(K, T, A, B) [&](int g, int t) { K<<<g, t>>>((T*)out, sp, (T)(A), (T)(B)); }
+    measure("iadd3", "IADD3", 2, 512, n1, L1(k_iadd3, int32_t, a, b));
+    measure("lop3", "LOP3", 2, 512, n1, L1(k_lop3, int32_t, a, b));
+    measure("imad", "IMAD", 2, 512, n1, L1(k_imad, int32_t, a, b));
+    measure("imad_hi", "IMAD.HI", 2, 512, n1, L1(k_imad_hi, int32_t, a, b));
+    measure("ffma", "FFMA", 2, 512, n1, L1(k_ffma, float, 1.0001f, 0.5f));
+    measure("dfma", "DFMA", 2, 512, n1, L1(k_dfma, double, 1.0000001, 0.5));
+    measure("i2fp_shf", "I2FP + SHF pairs (per op)", 2, 512, 2 * n1, L1(k_i2fp, int32_t, 0, 0));
+    measure("lea_hi", "LEA.HI + LOP3 pairs (per op)", 2, 512, 2 * n1, L1(k_lea_hi, int32_t, a, b));
+    measure("mixed_alu_fma_int", "LOP3 + IMAD interleaved", 2, 512, 2 * n1, L1(k_mixed_alu_fma, int32_t, a, b));
+    measure("shfl", "SHFL.UP", 2, 512, n1, L1(k_shfl, int32_t, a, b));
+    DevRule r;
+    std::memset(&r, 0, sizeof r);
+    const int64_t Q = 1724240;                              // cfg4's kappa = 1/Q
+    r.one = 1; r.mone = -1;
+    r.eo_cf = (float)(1.0 / (double)Q * (1.0 - 1.0 / 2097152.0));
+    r.eo_nQ = (int32_t)(-Q);
+    r.eo_c6 = (int32_t)(uint32_t)((uint64_t)Q * 0x4B400001ull - (uint64_t)((Q + 1) / 2));
+    // 7 instructions per cell-update (I2FP, FMUL, FFMA, 2 IMAD, LEA.HI, IADD3)
+    measure("eo_sign_step", "K2 sign-uniform step, 7 instr/cell", 2, 256, 7.0 * SSTEPS * SV,
+            [&](int g, int t) { k_eo_sign_step<<<g, t>>>((int32_t*)out, sp, r, 17); });
+    return 0;
+}
