@@ -192,9 +192,9 @@ struct fqnm_plan {
     bool stream2d = true;               // 2D: K9 streaming instead of K7
     int k2s = 2;                        // K9 steps per launch (1 or 2)
     bool stream3d = false;              // 3D: K10 warp streaming instead of K8 (measured slower)
-    // K2P persistent stepper (one launch for all blocks): -1 auto, 0 off, 1 forced.
-    // Off by default: measured slower than launch-per-block K2 (cfg3 53 vs 27 ms)
-    int persist = 0;
+    // K2P persistent stepper (one launch for all blocks): -1 auto (use_persist: few waves
+    // of windows per launch), 0 off (kernel override 2), 1 forced (kernel override 12)
+    int persist = -1;
     unsigned int* pflags = nullptr;
     unsigned long long* pcounter = nullptr;
     int64_t pflags_n = 0;
@@ -1056,7 +1056,10 @@ static bool use_persist(fqnm_plan_t* p, int64_t nb)
     if (p->persist == 1) return true;
     const int64_t S = 32 * p->V - (p->dep_left ? round4(p->k) : 0) - (p->dep_right ? round4(p->k) : 0);
     const int64_t nwin = (d.n_local + S - 1) / S;
-    return nwin < 64 * 148 * 16;                     // fewer than 64 waves of resident warps
+    // few waves of resident warps per launch: the last partial wave of every K2 launch is a
+    // visible share (cfg3: 7.4 waves, K2P 6.35 vs K2 6.22 TCUPS); from ~48 waves on K2 wins
+    // (EO 2^28: 3.89 vs 3.74; profiles/r02_tune_k2p.jsonl)
+    return nwin < 16 * 148 * 16;
 }
 
 static int step_persist(fqnm_plan_t* p, void* q, int64_t nb, int64_t base, int64_t rem)

@@ -143,6 +143,79 @@ __global__ void __launch_bounds__(256, 2) k_eo_sign_step(int32_t* out, Span* sp,
     span_end(sp, t0);
 }
 
+// ---- the K2 LIN kappa = 1/2 step on register data (cfg3's mix: LEA.HI + SHF + 2 IMAD) ----
+__global__ void __launch_bounds__(256, 2) k_lin_half_step(int32_t* out, Span* sp, DevRule r, int32_t seed)
+{
+    unsigned long long t0; __syncthreads(); span_begin(t0);
+    const int lane = threadIdx.x & 31;
+    int32_t q[SV];
+#pragma unroll
+    for (int j = 0; j < SV; ++j) q[j] = ((seed + 37 * j + 11 * (int)threadIdx.x) & 8191) - 4096;
+    for (int s = 0; s < SSTEPS; ++s) {
+        int32_t h[SV], p[SV];
+#pragma unroll
+        for (int j = 0; j < SV; ++j) {
+            h[j] = q[j] / 2;
+            p[j] = h[j] * r.mone + q[j];
+        }
+        const int32_t pl = __shfl_up_sync(0xffffffffu, p[SV - 1], 1);
+        q[0] = pl * r.one + h[0];
+#pragma unroll
+        for (int j = 1; j < SV; ++j) q[j] = p[j - 1] * r.one + h[j];
+        if (lane == 0) q[0] = 777;
+    }
+    int32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < SV; ++j) acc ^= q[j];
+    if (acc == seed + 123456789) out[threadIdx.x] = acc;
+    span_end(sp, t0);
+}
+
+// ---- EO sign-step variants (cells per clock; exploration of the instruction mix) ----
+// CONV: 0 I2FP, 1 IMAD + FADD, 2 alternate; ORD: 0 v = q*q + (bits*nQ + c6),
+// 1 v = bits*nQ + (q*q + c6) (the q*q IMAD off the float chain's critical path)
+template <int CONV, int ORD>
+__device__ __forceinline__ int32_t g_var(int32_t q, const DevRule& r, bool odd)
+{
+    float qf;
+    if (CONV == 0 || (CONV == 2 && !odd)) qf = __int2float_rn(q);
+    else qf = __int_as_float(imad(q, r.one, 0x4B400000)) - 12582912.0f;
+    const float sq = __fmul_rn(qf, qf);
+    const float t = __fmaf_rn(sq, r.eo_cf, 12582913.0f);
+    const int32_t bits = __float_as_int(t);
+    int32_t v;
+    if (ORD == 0) v = imad(q, q, imad(bits, r.eo_nQ, r.eo_c6));
+    else v = imad(bits, r.eo_nQ, imad(q, q, r.eo_c6));
+    return bits + (v >> 31);
+}
+
+template <int CONV, int ORD, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_eo_var(int32_t* out, Span* sp, DevRule r, int32_t seed)
+{
+    unsigned long long t0; __syncthreads(); span_begin(t0);
+    const int lane = threadIdx.x & 31;
+    int32_t q[SV];
+#pragma unroll
+    for (int j = 0; j < SV; ++j) q[j] = 100000 + ((seed + 37 * j + 11 * (int)threadIdx.x) & 4095);
+    for (int s = 0; s < SSTEPS; ++s) {
+        const int32_t glast = g_var<CONV, ORD>(q[SV - 1], r, true);
+        int32_t gp = __shfl_up_sync(0xffffffffu, glast, 1);
+#pragma unroll
+        for (int j = 0; j + 1 < SV; ++j) {
+            const int32_t gj = g_var<CONV, ORD>(q[j], r, (j & 1) != 0);
+            q[j] = q[j] + gp - gj;
+            gp = gj;
+        }
+        q[SV - 1] = q[SV - 1] + gp - glast;
+        if (lane == 0) q[0] = 100000;
+    }
+    int32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < SV; ++j) acc ^= q[j];
+    if (acc == seed + 123456789) out[threadIdx.x] = acc;
+    span_end(sp, t0);
+}
+
 int main(int argc, char** argv)
 {
     const int sms = 148;
@@ -203,5 +276,16 @@ int main(int argc, char** argv)
     // 7 instructions per cell-update (I2FP, FMUL, FFMA, 2 IMAD, LEA.HI, IADD3)
     measure("eo_sign_step", "K2 sign-uniform step, 7 instr/cell", 2, 256, 7.0 * SSTEPS * SV,
             [&](int g, int t) { k_eo_sign_step<<<g, t>>>((int32_t*)out, sp, r, 17); });
+    // EO variants: reported as lane-ops at 7 per cell, i.e. cells/clk x 7 (comparable)
+#define EOV(C, O, M, NAME) measure(NAME, "EO sign-step variant (7-op-equivalent cells)", M, 256, \
+        7.0 * SSTEPS * SV, [&](int g, int t) { k_eo_var<C, O, M><<<g, t>>>((int32_t*)out, sp, r, 17); })
+    EOV(0, 0, 2, "eo_var_conv0_ord0");
+    EOV(0, 1, 2, "eo_var_conv0_ord1");
+    EOV(1, 0, 2, "eo_var_conv1_ord0");
+    EOV(1, 1, 2, "eo_var_conv1_ord1");
+    EOV(2, 1, 2, "eo_var_conv2_ord1");
+    // 4 instructions per cell-update (LEA.HI, SHF, 2 IMAD)
+    measure("lin_half_step", "K2 LIN 1/2 step, 4 instr/cell", 2, 256, 4.0 * SSTEPS * SV,
+            [&](int g, int t) { k_lin_half_step<<<g, t>>>((int32_t*)out, sp, r, 17); });
     return 0;
 }
