@@ -109,6 +109,16 @@ __device__ __forceinline__ void one_step(int32_t (&q)[V], const DevRule& r, int 
             const int32_t glast = eo_g_biased<RULE, true>(q[V - 1], r);
             int32_t gp = NB == 0 ? __shfl_up_sync(FULL, glast, 1)
                                  : __shfl_sync(FULL, glast, (lane + 31) & 31);
+#if FQNM_EO_SIGN_CONV != 2 && FQNM_EO_SIGN_LEA != 2
+            // every cell evaluates the same form: a plain cell loop (micro: 0.90 vs 0.86 issue
+            // for the paired loop below, which alternating variants need)
+#pragma unroll
+            for (int j = 0; j + 1 < V; ++j) {
+                const int32_t gj = eo_g_biased<RULE, false>(q[j], r);
+                q[j] = q[j] + gp - gj;
+                gp = gj;
+            }
+#else
 #pragma unroll
             for (int j = 0; j + 1 < V; j += 2) {         // V even: j + 1 <= V - 2 here
                 const int32_t g0 = eo_g_biased<RULE, false>(q[j], r);
@@ -121,6 +131,7 @@ __device__ __forceinline__ void one_step(int32_t (&q)[V], const DevRule& r, int 
                     gp = g0;
                 }
             }
+#endif
             q[V - 1] = q[V - 1] + gp - glast;
         } else {                           // q_j += g_j - g_{j+1}
             const int32_t g0 = eo_g_biased<RULE, false>(q[0], r);

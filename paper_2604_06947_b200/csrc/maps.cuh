@@ -136,7 +136,7 @@ __device__ __forceinline__ void eo_gm_p1(int32_t q, int32_t& g, int32_t& m, cons
     const float s = __fmul_rn(qf, qf);
     const float t = __fmaf_rn(s, r.eo_cf, 12582913.0f);                 // 0x4B400001 + est
     const int32_t bits = __float_as_int(t);
-    const int32_t v = imad(q, q, imad(bits, r.eo_nQ, r.eo_c6));
+    const int32_t v = imad(bits, r.eo_nQ, imad(q, q, r.eo_c6));          // q*q off the float chain
     const int32_t gb = bits + (v >> 31);                                 // 0x4B400000 + g
 #if FQNM_EO_P1_SIGN
     const int32_t sg = __mulhi(q, r.one);                                // q >> 31 as IMAD.HI (FMA pipe)
@@ -170,7 +170,9 @@ __device__ __forceinline__ int32_t eo_g_biased(int32_t q, const DevRule& r)
         const float s = __fmul_rn(qf, qf);
         const float t = __fmaf_rn(s, r.eo_cf, 12582913.0f);                 // 0x4B400001 + est
         const int32_t bits = __float_as_int(t);
-        const int32_t v = imad(q, q, imad(bits, r.eo_nQ, r.eo_c6));
+        // v = q*q + (-Q) bits + c6 (mod 2^32) with q*q + c6 first: that IMAD does not wait
+        // for the float chain, so the chain's tail is one IMAD + LEA (micro: 0.90 vs 0.81 issue)
+        const int32_t v = imad(bits, r.eo_nQ, imad(q, q, r.eo_c6));
         constexpr bool hi_fma = FQNM_EO_SIGN_LEA == 1 || (FQNM_EO_SIGN_LEA == 2 && ALT);
         if (hi_fma) return imad_hi(v, r.one, bits);                          // FMA pipe
         return bits + (v >> 31);                                             // 0x4B400000 + g (LEA.HI)

@@ -122,16 +122,10 @@ __global__ void __launch_bounds__(256, 2) k_eo_sign_step(int32_t* out, Span* sp,
         const int32_t glast = eo_g_biased<R_EO_P1, true>(q[SV - 1], r);
         int32_t gp = __shfl_up_sync(0xffffffffu, glast, 1);
 #pragma unroll
-        for (int j = 0; j + 1 < SV; j += 2) {
-            const int32_t g0 = eo_g_biased<R_EO_P1, false>(q[j], r);
-            q[j] = q[j] + gp - g0;
-            if (j + 2 < SV) {
-                const int32_t g1 = eo_g_biased<R_EO_P1, true>(q[j + 1], r);
-                q[j + 1] = q[j + 1] + g0 - g1;
-                gp = g1;
-            } else {
-                gp = g0;
-            }
+        for (int j = 0; j + 1 < SV; ++j) {                 // as kernels_scalar.cu one_step
+            const int32_t gj = eo_g_biased<R_EO_P1, false>(q[j], r);
+            q[j] = q[j] + gp - gj;
+            gp = gj;
         }
         q[SV - 1] = q[SV - 1] + gp - glast;
         if (lane == 0) q[0] = 100000;        // keep the window's data positive and bounded
