@@ -593,7 +593,11 @@ static int resident_alloc(fqnm_plan_t* p)
     const int64_t n = p->d.n_local;
     int64_t Pmax = (n + 4 - 1) / 4;
     if (Pmax > RESIDENT_MAX_WARPS) Pmax = RESIDENT_MAX_WARPS;
-    if (!p->edges) CUDA_TRY(cudaMalloc(&p->edges, sizeof(int32_t) * 2 * Pmax * 2 * (size_t)Hmax));
+    if (!p->edges) {                         // 8-byte {value, tag} words (K6 exchange)
+        const size_t eb = sizeof(uint64_t) * 2 * Pmax * 2 * (size_t)Hmax;
+        CUDA_TRY(cudaMalloc(&p->edges, eb));
+        CUDA_TRY(cudaMemset(p->edges, 0, eb));                              // tag 0 never matches
+    }
     if (!p->flags) {
         CUDA_TRY(cudaMalloc(&p->flags, sizeof(unsigned int) * Pmax));
         CUDA_TRY(cudaMemset(p->flags, 0, sizeof(unsigned int) * Pmax));   // tags start at 1

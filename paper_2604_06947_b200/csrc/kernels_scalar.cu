@@ -34,6 +34,10 @@
 #define FQNM_STREAM_STEP 0     // K2/K3/K6 interior cells updated in map order (variant)
 #endif
 
+#ifndef FQNM_RES_LL
+#define FQNM_RES_LL 1          // K6 halo exchange in {value, tag} words (no fence / flag round trip)
+#endif
+
 #ifndef FQNM_RES_FENCE
 #define FQNM_RES_FENCE 0
 #endif
@@ -866,6 +870,57 @@ __global__ void __launch_bounds__(256, k6_minb<RULE>()) k_resident(ResidentArgs 
         if (done >= a.nsteps) break;
         ++blk;
         const uint32_t tag = a.tag_base + blk;
+#if FQNM_RES_LL
+        // edge exchange in 8-byte {value, tag} words (single-copy atomic): the writer needs
+        // no fence and no flag, the reader polls the words it needs until every tag is the
+        // block's.  Slot (blk & 1) is safe to overwrite two blocks later: by then the
+        // neighbour has read it (its block blk+1 needed these edges).
+        {
+            uint64_t* e = reinterpret_cast<uint64_t*>(a.edges) + ((size_t)(blk & 1) * a.P + w) * 2 * H;
+            const uint64_t hi = (uint64_t)tag << 32;
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                const int pos = lane * V + j;
+                if (pos >= H && pos < 2 * H)
+                    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" :: "l"(e + pos - H),
+                                 "l"(hi | (uint32_t)q[j]) : "memory");
+                if (pos >= Sw && pos < Sw + H)
+                    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" :: "l"(e + H + pos - Sw),
+                                 "l"(hi | (uint32_t)q[j]) : "memory");
+            }
+            const uint64_t* el = reinterpret_cast<const uint64_t*>(a.edges) +
+                                 ((size_t)(blk & 1) * a.P + wl) * 2 * H + H;   // left nbr's right edge
+            const uint64_t* er = reinterpret_cast<const uint64_t*>(a.edges) +
+                                 ((size_t)(blk & 1) * a.P + wr) * 2 * H;       // right nbr's left edge
+            bool need[V];
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                const int pos = lane * V + j;
+                need[j] = pos < H || (pos >= H + Sw && pos < H + Sw + H);
+            }
+            const long long t0 = clock64();
+            for (;;) {
+                bool ok = true;
+#pragma unroll
+                for (int j = 0; j < V; ++j) {
+                    if (!need[j]) continue;
+                    const int pos = lane * V + j;
+                    const uint64_t* src = pos < H ? el + pos : er + pos - H - Sw;
+                    uint64_t v;
+                    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(src) : "memory");
+                    if ((uint32_t)(v >> 32) == tag) {
+                        q[j] = (int32_t)(uint32_t)v;
+                        need[j] = false;
+                    } else {
+                        ok = false;
+                    }
+                }
+                if (__all_sync(FULL, ok)) break;
+                if (clock64() - t0 > SPIN_TRAP_CYCLES) __trap();
+            }
+        }
+        continue;
+#endif
         // publish the edges: left = positions [H, 2H), right = [Sw, Sw + H)
         int32_t* e = a.edges + ((size_t)(blk & 1) * a.P + w) * 2 * H;
 #pragma unroll
