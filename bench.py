@@ -425,13 +425,15 @@ def run_cfg4(args):
         "" if info["rule"] == 5 else "_general_p")
     ops_alg = OPS_ALG[ops_key]
     hbm_bytes_per_launch = 8.0 * n_local                               # read + write int32 once per block
+    # which K2 ran: the sign-specialised K2S (V = 48) when the range check proved the sign
+    k2s = plan.info()["k2s_launches"] > 0
+    Vk = 48 if k2s else info["cells_per_thread"]
+    kname = "k_blocked<%s,V=%d%s>" % (RULE_NAMES.get(info["rule"], "?"), Vk, ",sign" if k2s else "")
     roofline = alu_roofline(
-        "k_blocked<%s,V=%d>" % (RULE_NAMES.get(info["rule"], "?"), info["cells_per_thread"]),
-        ops_alg, updates_per_launch, per_launch_ms, hbm_bytes_per_launch,
+        kname, ops_alg, updates_per_launch, per_launch_ms, hbm_bytes_per_launch,
         {"kernel_launches": kern_launches, "kernel_share_of_step": kern_ms / ms if ms > 0 else None,
-         "k": info["k"], "V": info["cells_per_thread"], "ops_basis": ops_key,
-         "windows_redundancy": 32.0 * info["cells_per_thread"] / (
-             32.0 * info["cells_per_thread"] - 2 * ((info["k"] + 3) // 4 * 4))},
+         "k": info["k"], "V": Vk, "ops_basis": ops_key,
+         "windows_redundancy": 32.0 * Vk / (32.0 * Vk - 2 * ((info["k"] + 3) // 4 * 4))},
         mix_ceiling_key="eo_sign_step" if ops_key == "burgers_eo_sign_uniform" else "")
     tr, tr_src = ncu_traffic(n_local)
     if tr is not None:

@@ -34,7 +34,7 @@ LINEAR, BURGERS_EO, BURGERS_LF, EULER_ROE, EULER_ROE_DENSITY = 0, 1, 2, 3, 4
 BURGERS_GODUNOV, BURGERS_EO2, BURGERS_LF2 = 5, 6, 7      # two-point rules (Thm P:262-280)
 PERIODIC, TRANSMISSIVE, HALO = 0, 1, 2
 I32, I64 = 0, 1
-ABI_VERSION = 2                                           # include/fqnm.h FQNM_ABI_VERSION
+ABI_VERSION = 3                                           # include/fqnm.h FQNM_ABI_VERSION
 ROUND_HALF_AWAY, ROUND_FLOOR, ROUND_HALF_EVEN = 0, 1, 2
 STATUS = {0: "FQNM_OK", 1: "FQNM_ERR_ARG", 2: "FQNM_ERR_CFL", 3: "FQNM_ERR_RANGE",
           4: "FQNM_ERR_CUDA", 5: "FQNM_ERR_UNSUPPORTED", 6: "FQNM_ERR_NOMEM"}
@@ -74,7 +74,7 @@ class PlanInfo(ctypes.Structure):
         ("rule", ctypes.c_int32), ("k", ctypes.c_int32), ("cells_per_thread", ctypes.c_int32),
         ("kernel", ctypes.c_int32), ("scratch_bytes", ctypes.c_int64),
         ("s_euler", ctypes.c_double), ("g1_euler", ctypes.c_double),
-        ("d8_lim", ctypes.c_int64),
+        ("d8_lim", ctypes.c_int64), ("k2s_launches", ctypes.c_int64),
     ]
 
     def as_dict(self):

@@ -206,6 +206,14 @@ struct fqnm_plan {
     int64_t launches = 0;
     // pipelined end-to-end stepping (fqnm_step_host): chunk plan + 3 ext buffers + streams
     const int* guard = nullptr;          // K2 launches return at once when *guard != 0
+    // K2S (sign-specialised K2, EO rules): sign_hint = 1 / 2 when this fqnm_step call's
+    // range check proved every cell >= 0 / <= 0 (the maximum principle keeps it for the
+    // call); sign_dev = device sign bits of the input (pipelined chunks: dual launch)
+    int sign_hint = 0;
+    int64_t k2s_launches = 0;            // K2S launches since creation (fqnm_plan_info)
+    bool no_sign = false;                // kernel override 2 / 12 / 100m + 2: the general K2 only
+    const int* sign_dev = nullptr;
+    int* pipe_sign = nullptr;            // per chunk sign bits (pipelined fqnm_step_host)
     fqnm_plan_t* pipe_child = nullptr;
     int64_t pipe_H = 0, pipe_C = 0, pipe_m = 0;
     void* pipe_buf[3] = {nullptr, nullptr, nullptr};
@@ -885,6 +893,8 @@ static void pipe_release(fqnm_plan_t* p)
     p->pipe_head = nullptr;
     if (p->md_guard) cudaFree(p->md_guard);
     if (p->md_guard_host) cudaFreeHost(p->md_guard_host);
+    if (p->pipe_sign) cudaFree(p->pipe_sign);
+    p->pipe_sign = nullptr;
     if (p->pipe_guard) cudaFree(p->pipe_guard);
     if (p->pipe_guard_host) cudaFreeHost(p->pipe_guard_host);
     p->pipe_guard = nullptr;
@@ -1040,6 +1050,20 @@ static int launch_block(fqnm_plan_t* p, const int32_t* src, int32_t* dst, int ks
     a.KR = p->dep_right ? round4(ksteps) : 0;
     a.bmode = bmode_of(d);
     a.guard = p->guard;
+    // K2S geometry (V = 48): when the host proved the sign, or for the dual launch
+    const bool sign_ok = d.boundary != FQNM_HALO && blocked_sign_has_rule(p->rule) && !p->no_sign &&
+                         32 * BLOCKED_SIGN_V - a.KL - a.KR >= 4;
+    if (sign_ok && (p->sign_hint || p->sign_dev)) {
+        BlockedArgs b = a;
+        const int64_t S2 = 32 * BLOCKED_SIGN_V - a.KL - a.KR;
+        b.nwin = (d.n_local + S2 - 1) / S2;
+        b.sign_bits = p->sign_hint ? nullptr : p->sign_dev;
+        PROF_LAUNCH(launch_blocked_sign(p->rule, p->sign_hint ? p->sign_hint : 1, b, p->dr, p->st,
+                                        148 * 32));
+        p->k2s_launches++;
+        if (p->sign_hint) return FQNM_OK;
+        a.sign_bits = p->sign_dev;                 // dual launch: the general K2 covers the rest
+    }
     const int64_t S = 32 * p->V - a.KL - a.KR;
     if (S < 4) return fail(FQNM_ERR_ARG, "k = %d too large for V = %d", ksteps, p->V);
     a.nwin = (d.n_local + S - 1) / S;
@@ -1152,10 +1176,16 @@ extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
         return fail(FQNM_ERR_UNSUPPORTED, "split-domain plans step through fqnm_step_block");
     if (nsteps == 0) return FQNM_OK;
     int rc;
+    p->sign_hint = 0;
     if (d.check_range && d.nvar == 1) {
         bool gen = false;
         if ((rc = check_range(p, q, &gen)) != FQNM_OK) return rc;
         if (gen) return step_generic_child(p, q, nsteps);
+        // the range check's min/max: a state of one sign keeps it for the call (D8
+        // monotonicity, Lemma CFL), so K2 can run the sign-specialised K2S
+        const long long mn = p->h_minmax[2], mx = p->h_minmax[3];
+        if (p->family == 2 && blocked_sign_has_rule(p->rule))
+            p->sign_hint = mn >= 0 ? 1 : (mx <= 0 ? 2 : 0);
     }
     const int bm = bmode_of(d);
     const int64_t n = d.n_local;
@@ -1513,6 +1543,7 @@ static int pipe_setup(fqnm_plan_t* p, int64_t nsteps)
     for (int i = 0; i < 3 && e == cudaSuccess; ++i) e = cudaMalloc(&p->pipe_buf[i], (size_t)(C + 2 * H) * 4);
     if (e == cudaSuccess) e = cudaMalloc(&p->pipe_head, (size_t)H * 4);
     if (e == cudaSuccess) e = cudaMalloc(&p->pipe_guard, (size_t)m * sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&p->pipe_sign, (size_t)m * sizeof(int));
     if (e == cudaSuccess) e = cudaMallocHost(&p->pipe_guard_host, (size_t)m * sizeof(int));
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->pipe_h2d, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->pipe_d2h, cudaStreamNonBlocking);
@@ -1549,6 +1580,10 @@ static int step_host_pipelined(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
 //    pipe_head on the H2D stream before H2D(0) (so before D2H(0)) and taken from there;
 //  * chunk c's right halo and chunk 0's left halo are outputs of later D2Hs, which follow
 //    that chunk's H2D through the compute dependency.
+#ifndef FQNM_PIPE_DUAL
+#define FQNM_PIPE_DUAL 0       // pipelined chunks: K2S + K2 dual launch on the device sign bits
+                               // (measured slower on cfg4 e2e: 3535 vs 3602 GCUPS)
+#endif
 static int step_host_pipelined_impl(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
 {
     const int64_t n = p->d.n_local, C = p->pipe_C, H = p->pipe_H, m = p->pipe_m, E = C + 2 * H;
@@ -1559,6 +1594,7 @@ static int step_host_pipelined_impl(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
     cudaEvent_t* ev_out = p->pipe_ev + 6;
     const bool check = p->d.check_range != 0;
     CUDA_TRY(cudaMemsetAsync(p->pipe_guard, 0, (size_t)m * sizeof(int), p->st));
+    CUDA_TRY(cudaMemsetAsync(p->pipe_sign, 0, (size_t)m * sizeof(int), p->st));
     CUDA_TRY(cudaEventRecord(ev_comp[0], p->st));                 // guard reset before any use
     CUDA_TRY(cudaStreamWaitEvent(p->pipe_h2d, ev_comp[0], 0));
     CUDA_TRY(cudaMemcpyAsync(p->pipe_head, qh, (size_t)H * 4, cudaMemcpyHostToDevice, p->pipe_h2d));
@@ -1592,16 +1628,21 @@ static int step_host_pipelined_impl(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
         // range check + stepping on the compute stream
         CUDA_TRY(cudaStreamWaitEvent(p->st, ev_in[b], 0));
         if (check) {
-            CUDA_TRY(launch_range_guard(buf, E, p->lo, p->hi, p->pipe_guard + c, p->st));
+            // range guard of the extended chunk + its sign bits (K2S / K2 dual launch)
+            CUDA_TRY(launch_range_sign_guard(buf, E, p->lo, p->hi, p->pipe_guard + c,
+                                             p->pipe_sign + c, p->st));
             p->launches++;
             ch->guard = p->pipe_guard + c;
+            ch->sign_dev = FQNM_PIPE_DUAL ? p->pipe_sign + c : nullptr;
         } else {
             ch->guard = nullptr;
+            ch->sign_dev = nullptr;
         }
         const int64_t l0 = ch->launches;
         rc = fqnm_step(ch, buf, nsteps);
         p->launches += ch->launches - l0;
         ch->guard = nullptr;
+        ch->sign_dev = nullptr;
         if (rc != FQNM_OK) return rc;
         CUDA_TRY(cudaEventRecord(ev_comp[b], p->st));
         // D2H of the inner C cells, after the stepping and after H2D(c+1) read their tail
@@ -1927,6 +1968,7 @@ static void fill_info(const fqnm_plan_t* p, fqnm_plan_info* info)
     info->s_euler = p->s_e;
     info->g1_euler = p->g1_e;
     info->d8_lim = p->d8_lim;
+    info->k2s_launches = p->k2s_launches;
 }
 
 extern "C" int fqnm_plan_validate(const fqnm_plan_desc* d, fqnm_plan_info* info)
@@ -1993,6 +2035,11 @@ extern "C" int fqnm_debug_override(fqnm_plan_t* p, int32_t kernel, int32_t k, in
         }
         return FQNM_OK;
     }
+    bool allow_sign = false;
+    if (kernel == 22) {                 // K2, with K2S where the range check proves a sign
+        kernel = 2;
+        allow_sign = true;
+    }
     if (kernel >= 100) {               // K2 with a register-cap variant: 2 + 100 * minb
         p->minb = kernel / 100;
         kernel = kernel % 100;
@@ -2019,7 +2066,7 @@ extern "C" int fqnm_debug_override(fqnm_plan_t* p, int32_t kernel, int32_t k, in
         }
         return FQNM_OK;
     }
-    if (kernel == 2) p->persist = 0;
+    if (kernel == 2) { p->persist = 0; p->no_sign = !allow_sign; }
     if (kernel) {
         if (d.boundary == FQNM_HALO && kernel != 2) return fail(FQNM_ERR_UNSUPPORTED, "split domains use K2");
         if (kernel == 3) {

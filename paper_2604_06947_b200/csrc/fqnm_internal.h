@@ -76,6 +76,10 @@ struct BlockedArgs {
     unsigned int* peer_left_flags;
     unsigned int* peer_right_flags;
     const int* guard;              // optional: nonzero -> the launch does nothing (failed range check)
+    // dual launch (the sign of the state is only known on the device): bit 0 of *sign_bits
+    // set = some cell < 0.  The sign-specialised kernel (K2S) returns when it is set, the
+    // general K2 when it is clear.  nullptr: one kernel, chosen by the host.
+    const int* sign_bits;
 };
 
 struct EulerArgs {
@@ -164,6 +168,15 @@ cudaError_t launch_defect(const double* rowsum, const unsigned int* c0, const un
 // kernel launchers (kernels_scalar.cu / kernels_euler.cu); return cudaError_t
 cudaError_t launch_blocked(int rule, int V, int minb, const BlockedArgs& a, const DevRule& r,
                            cudaStream_t st, int grid_cap);
+// K2S: K2 for a state whose cells are all >= 0 (sign 1) or all <= 0 (sign 2), EO rules only,
+// V = BLOCKED_SIGN_V cells per lane (no vote, no general path: 128 registers hold V = 48)
+#define BLOCKED_SIGN_V 48
+bool blocked_sign_has_rule(int rule);
+cudaError_t launch_blocked_sign(int rule, int sign, const BlockedArgs& a, const DevRule& r,
+                                cudaStream_t st, int grid_cap);
+// flag |= 1 if any q[i] outside [lo, hi]; sign_bits |= 1 if any q[i] < 0, 2 if any > 0
+cudaError_t launch_range_sign_guard(const int32_t* q, int64_t n, long long lo, long long hi,
+                                    int* flag, int* sign_bits, cudaStream_t st);
 cudaError_t launch_resident(int rule, int V, const ResidentArgsHost& h, const DevRule& r,
                             cudaStream_t st);
 

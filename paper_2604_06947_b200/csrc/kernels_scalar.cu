@@ -502,11 +502,18 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa), "l"(gmem) : "memory");
 }
 
-template <int RULE, int V, int MINB>
+// FSIGN (K2S, EO rules): 0 = vote per window (general K2), 1 = every cell >= 0, 2 = every
+// cell <= 0 for the whole call (host-proved from the range check's min/max, or the dual
+// launch's sign_bits): the fast windows step with one_step SIGN directly
+template <int RULE, int V, int MINB, int FSIGN = 0>
 __global__ void __launch_bounds__(256, MINB) k_blocked(BlockedArgs a, DevRule r)
 {
     static_assert(V % 4 == 0, "V must be a multiple of 4 (int4 vectors)");
     if (a.guard && *a.guard) return;                            // input failed its range check
+    if (a.sign_bits) {                                          // dual launch: one of the two runs
+        const bool has_neg = (*a.sign_bits & 1) != 0;
+        if (FSIGN == 1 ? has_neg : !has_neg) return;
+    }
     constexpr int W = 32 * V;
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -592,7 +599,8 @@ __global__ void __launch_bounds__(256, MINB) k_blocked(BlockedArgs a, DevRule r)
                 }
             }
 #endif
-            run_window_steps_signed<RULE, V>(q, a.ksteps, r);
+            if (FSIGN != 0) run_window_steps<RULE, V, false, FSIGN>(q, a.ksteps, r, 0, 0);
+            else run_window_steps_signed<RULE, V>(q, a.ksteps, r);
             // store the cells whose dependence cone stayed inside the window
 #pragma unroll
             for (int j = 0; j < V / 4; ++j) {
@@ -1275,13 +1283,13 @@ static inline int grid_for(int64_t work, int threads, int cap)
     return (int)g;
 }
 
-template <int RULE, int V, int MINB>
+template <int RULE, int V, int MINB, int FSIGN = 0>
 cudaError_t blocked_v(const BlockedArgs& a, const DevRule& r, cudaStream_t st, int cap)
 {
     const int threads = 256;
     int64_t warps = a.nwin * a.batch;
     int g = grid_for(warps * 32, threads, cap);
-    k_blocked<RULE, V, MINB><<<g, threads, 0, st>>>(a, r);
+    k_blocked<RULE, V, MINB, FSIGN><<<g, threads, 0, st>>>(a, r);
     return cudaGetLastError();
 }
 
@@ -1300,6 +1308,8 @@ cudaError_t blocked_rule(int V, int minb, const BlockedArgs& a, const DevRule& r
         if (V == 32 && minb == 3) return blocked_v<RULE, 32, 3>(a, r, st, cap);
         if (V == 64 && minb == 2) return blocked_v<RULE, 64, 2>(a, r, st, cap);
         if (V == 64 && minb == 1) return blocked_v<RULE, 64, 1>(a, r, st, cap);
+        if (V == 48 && minb == 2) return blocked_v<RULE, 48, 2>(a, r, st, cap);
+        if (V == 40 && minb == 2) return blocked_v<RULE, 40, 2>(a, r, st, cap);
 #endif
         if (V == 16 && minb == 3) return blocked_v<RULE, 16, 3>(a, r, st, cap);
         if (V == 16 && minb == 4) return blocked_v<RULE, 16, 4>(a, r, st, cap);
@@ -1321,6 +1331,23 @@ template cudaError_t blocked_rule<R_LIN_HALF>(int, int, const BlockedArgs&, cons
 #if FQNM_PART(5)
 template cudaError_t blocked_rule<R_EO_FAST>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
 template cudaError_t blocked_rule<R_EO_P1>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
+#endif
+#if FQNM_PART(4)
+bool blocked_sign_has_rule(int rule) { return rule == R_EO_P1 || rule == R_EO_FAST; }
+
+// K2S: V = 48, two 256-thread CTAs per SM (128 registers; the sign step keeps no map array)
+cudaError_t launch_blocked_sign(int rule, int sign, const BlockedArgs& a, const DevRule& r,
+                                cudaStream_t st, int grid_cap)
+{
+    constexpr int V = BLOCKED_SIGN_V;
+    if (rule == R_EO_P1)
+        return sign == 1 ? blocked_v<R_EO_P1, V, 2, 1>(a, r, st, grid_cap)
+                         : blocked_v<R_EO_P1, V, 2, 2>(a, r, st, grid_cap);
+    if (rule == R_EO_FAST)
+        return sign == 1 ? blocked_v<R_EO_FAST, V, 2, 1>(a, r, st, grid_cap)
+                         : blocked_v<R_EO_FAST, V, 2, 2>(a, r, st, grid_cap);
+    return cudaErrorInvalidValue;
+}
 #endif
 #if FQNM_PART(8)
 template cudaError_t blocked_v<R_GENERIC, 32, FQNM_BLOCKED_MINB0>(const BlockedArgs&, const DevRule&, cudaStream_t, int);
@@ -1362,7 +1389,7 @@ extern template cudaError_t blocked_rule<R_LIN_FAST>(int, int, const BlockedArgs
 extern template cudaError_t blocked_rule<R_TP_FAST>(int, int, const BlockedArgs&, const DevRule&, cudaStream_t, int);
 #endif
 #ifdef FQNM_EXTRA_VARIANTS
-bool blocked_has_V(int V) { return V == 8 || V == 16 || V == 32 || V == 64; }
+bool blocked_has_V(int V) { return V == 8 || V == 16 || V == 32 || V == 64 || V == 48 || V == 40; }
 #else
 bool blocked_has_V(int V) { return V == 8 || V == 16 || V == 32; }
 #endif
@@ -1621,6 +1648,31 @@ __global__ void k_range_guard(const int32_t* __restrict__ q, int64_t n, long lon
         bad |= (v < lo) | (v > hi);
     }
     if (__any_sync(FULL, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+__global__ void k_range_sign_guard(const int32_t* __restrict__ q, int64_t n, long long lo,
+                                   long long hi, int* flag, int* sign_bits)
+{
+    bool bad = false, neg = false, pos = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const long long v = q[i];
+        bad |= (v < lo) | (v > hi);
+        neg |= v < 0;
+        pos |= v > 0;
+    }
+    const bool b = __any_sync(FULL, bad), ng = __any_sync(FULL, neg), ps = __any_sync(FULL, pos);
+    if ((threadIdx.x & 31) == 0) {
+        if (b) atomicOr(flag, 1);
+        if (ng || ps) atomicOr(sign_bits, (ng ? 1 : 0) | (ps ? 2 : 0));
+    }
+}
+
+cudaError_t launch_range_sign_guard(const int32_t* q, int64_t n, long long lo, long long hi,
+                                    int* flag, int* sign_bits, cudaStream_t st)
+{
+    k_range_sign_guard<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(q, n, lo, hi, flag, sign_bits);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_range_guard(const int32_t* q, int64_t n, long long lo, long long hi, int* flag,

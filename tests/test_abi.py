@@ -35,7 +35,7 @@ def test_exports_every_declared_symbol(F):
     lib = ctypes.CDLL(F.lib_path())
     for n in names:
         assert hasattr(lib, n), f"libfqnm.so does not export {n}"
-    assert F.abi_version() == F.ABI_VERSION == 2
+    assert F.abi_version() == F.ABI_VERSION == 3
 
 
 def test_library_is_sm100a_only(F):

@@ -119,3 +119,25 @@ def test_step_host_checks_buffer(F):
         F.fqnm_step_host(plan, np.zeros(4096, dtype=np.float32), 1)
     with pytest.raises(ValueError):
         F.fqnm_step_host(plan, np.zeros(8192, dtype=np.int32), 1)
+
+
+@pytest.mark.parametrize("sign", [1, -1, 0])
+def test_pipelined_step_host_sign_chunks(F, sign):
+    """The pipelined fqnm_step_host on all-positive, all-negative and partly negative data
+    (chunks of both kinds; the range-sign guard runs per chunk) equals fqnm_step, which
+    itself runs K2S on the one-signed states."""
+    n = 1 << 24
+    rng = np.random.default_rng(5 + sign)
+    q0 = np.abs(W.smooth_random(rng, n, 100000, 50000)).astype(np.int32)
+    if sign < 0:
+        q0 = -q0
+    elif sign == 0:
+        q0[: n // 3] = -q0[: n // 3]                      # some chunks mixed or negative
+    qmax = int(np.abs(q0).max())
+    lam = W.dt_dx_double(W.cfg("cfg2"), qmax)
+    plan = F.fqnm_plan(n, 1e-5, lam, F.BURGERS_EO, F.PERIODIC)
+    ref = torch.tensor(q0, device="cuda")
+    F.fqnm_step(plan, ref, 77)
+    qh = torch.tensor(q0).pin_memory()
+    F.fqnm_step_host(plan, qh, 77)
+    assert torch.equal(qh, ref.cpu())

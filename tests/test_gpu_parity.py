@@ -223,6 +223,34 @@ def test_eo_sign_uniform_windows(F, kernel, V, case, patch):
     assert np.array_equal(host(q), ref)
 
 
+@pytest.mark.parametrize("sign", [1, -1])
+@pytest.mark.parametrize("case", ["p1", "general_p"])
+@pytest.mark.parametrize("n", [1536 * 3 + 7, 200_003, 1 << 21])
+def test_k2s_sign_specialised_kernel(F, sign, case, n):
+    """K2S: a range-checked fqnm_step whose whole state is >= 0 (or <= 0) runs the
+    sign-specialised kernel (V = 48, no vote, no general path); a mixed state runs K2."""
+    delta, lam = ("1e-5", Fraction(4, 15)) if case == "p1" else ("1e-5", Fraction(3, 10))
+    rng = np.random.default_rng(n + (sign > 0))
+    q0 = sign * np.abs(W.smooth_random(rng, n, 100000, 50000))
+    q0[rng.integers(0, n, 50)] = 0                                   # zeros are allowed
+    plan = F.fqnm_plan_ex(n, 1e-5, float(lam), F.BURGERS_EO, check_range=True)
+    F.fqnm_debug_override(plan, 22, 0, 32)            # K2 (not K2P/K6/K4) + K2S
+    ref = oracle.Rule(W.BURGERS_EO, delta, lam).run(q0, 97)
+    q = to_dev(q0)
+    k0 = plan.info()["k2s_launches"]
+    F.fqnm_step(plan, q, 97)
+    assert np.array_equal(host(q), ref)
+    assert plan.info()["k2s_launches"] > k0
+    # a mixed-sign state takes the general kernel
+    q1 = q0.copy()
+    q1[n // 2] = -sign * 5
+    k1 = plan.info()["k2s_launches"]
+    q = to_dev(q1)
+    F.fqnm_step(plan, q, 33)
+    assert np.array_equal(host(q), oracle.Rule(W.BURGERS_EO, delta, lam).run(q1, 33))
+    assert plan.info()["k2s_launches"] == k1
+
+
 def test_ens1_sampled(F):
     w = W.cfg("ens1")
     B = w.batch
