@@ -214,6 +214,8 @@ struct fqnm_plan {
     bool no_sign = false;                // kernel override 2 / 12 / 100m + 2: the general K2 only
     const int* sign_dev = nullptr;
     int* pipe_sign = nullptr;            // per chunk sign bits (pipelined fqnm_step_host)
+    int* pipe_sign_host = nullptr;
+    int sign_preset = 0;                 // sign_hint a caller (the pipeline) proved for one call
     fqnm_plan_t* pipe_child = nullptr;
     int64_t pipe_H = 0, pipe_C = 0, pipe_m = 0;
     void* pipe_buf[3] = {nullptr, nullptr, nullptr};
@@ -895,6 +897,8 @@ static void pipe_release(fqnm_plan_t* p)
     if (p->md_guard_host) cudaFreeHost(p->md_guard_host);
     if (p->pipe_sign) cudaFree(p->pipe_sign);
     p->pipe_sign = nullptr;
+    if (p->pipe_sign_host) cudaFreeHost(p->pipe_sign_host);
+    p->pipe_sign_host = nullptr;
     if (p->pipe_guard) cudaFree(p->pipe_guard);
     if (p->pipe_guard_host) cudaFreeHost(p->pipe_guard_host);
     p->pipe_guard = nullptr;
@@ -1035,6 +1039,10 @@ static int bmode_of(const fqnm_plan_desc& d)
            : (d.boundary == FQNM_HALO ? BM_HALO : BM_PERIODIC);
 }
 
+#ifndef FQNM_K2S_GRID
+#define FQNM_K2S_GRID (148 * 32)   // K2S grid cap in CTAs (windows are grid-strided over the warps)
+#endif
+
 static int launch_block(fqnm_plan_t* p, const int32_t* src, int32_t* dst, int ksteps)
 {
     const fqnm_plan_desc& d = p->d;
@@ -1059,7 +1067,7 @@ static int launch_block(fqnm_plan_t* p, const int32_t* src, int32_t* dst, int ks
         b.nwin = (d.n_local + S2 - 1) / S2;
         b.sign_bits = p->sign_hint ? nullptr : p->sign_dev;
         PROF_LAUNCH(launch_blocked_sign(p->rule, p->sign_hint ? p->sign_hint : 1, b, p->dr, p->st,
-                                        148 * 32));
+                                        FQNM_K2S_GRID));
         p->k2s_launches++;
         if (p->sign_hint) return FQNM_OK;
         a.sign_bits = p->sign_dev;                 // dual launch: the general K2 covers the rest
@@ -1176,7 +1184,7 @@ extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
         return fail(FQNM_ERR_UNSUPPORTED, "split-domain plans step through fqnm_step_block");
     if (nsteps == 0) return FQNM_OK;
     int rc;
-    p->sign_hint = 0;
+    p->sign_hint = p->sign_preset;
     if (d.check_range && d.nvar == 1) {
         bool gen = false;
         if ((rc = check_range(p, q, &gen)) != FQNM_OK) return rc;
@@ -1544,6 +1552,7 @@ static int pipe_setup(fqnm_plan_t* p, int64_t nsteps)
     if (e == cudaSuccess) e = cudaMalloc(&p->pipe_head, (size_t)H * 4);
     if (e == cudaSuccess) e = cudaMalloc(&p->pipe_guard, (size_t)m * sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&p->pipe_sign, (size_t)m * sizeof(int));
+    if (e == cudaSuccess) e = cudaMallocHost(&p->pipe_sign_host, (size_t)m * sizeof(int));
     if (e == cudaSuccess) e = cudaMallocHost(&p->pipe_guard_host, (size_t)m * sizeof(int));
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->pipe_h2d, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->pipe_d2h, cudaStreamNonBlocking);
@@ -1583,6 +1592,15 @@ static int step_host_pipelined(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
 #ifndef FQNM_PIPE_DUAL
 #define FQNM_PIPE_DUAL 0       // pipelined chunks: K2S + K2 dual launch on the device sign bits
                                // (measured slower on cfg4 e2e: 3535 vs 3602 GCUPS)
+#endif
+#ifndef FQNM_PIPE_SIGN_USE
+#define FQNM_PIPE_SIGN_USE 1   // experiment switch: 0 = read the sign bits but keep K2
+#endif
+#ifndef FQNM_PIPE_SIGN
+#define FQNM_PIPE_SIGN 0       // pipelined chunks: the host reads each chunk's sign bits and
+                               // steps one-signed chunks with K2S (the per-chunk host wait
+                               // measured 2977 vs 3615 GCUPS e2e; K2S on chunk-sized problems
+                               // is not faster than the voting K2 either: dual 3539-3593)
 #endif
 static int step_host_pipelined_impl(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
 {
@@ -1634,6 +1652,16 @@ static int step_host_pipelined_impl(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
             p->launches++;
             ch->guard = p->pipe_guard + c;
             ch->sign_dev = FQNM_PIPE_DUAL ? p->pipe_sign + c : nullptr;
+            if (!FQNM_PIPE_DUAL && FQNM_PIPE_SIGN && blocked_sign_has_rule(ch->rule)) {
+                // read the chunk's sign bits on the host: the guard runs right after the
+                // previous chunk's stepping on this stream, so the wait overlaps that
+                // stepping and the stream idles only for the launch latency of the next
+                CUDA_TRY(cudaMemcpyAsync(p->pipe_sign_host + c, p->pipe_sign + c, sizeof(int),
+                                         cudaMemcpyDeviceToHost, p->st));
+                CUDA_TRY(cudaStreamSynchronize(p->st));
+                const int bits = p->pipe_sign_host[c];
+                ch->sign_preset = !FQNM_PIPE_SIGN_USE ? 0 : (bits & 1) == 0 ? 1 : ((bits & 2) == 0 ? 2 : 0);
+            }
         } else {
             ch->guard = nullptr;
             ch->sign_dev = nullptr;
@@ -1643,6 +1671,7 @@ static int step_host_pipelined_impl(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
         p->launches += ch->launches - l0;
         ch->guard = nullptr;
         ch->sign_dev = nullptr;
+        ch->sign_preset = 0;
         if (rc != FQNM_OK) return rc;
         CUDA_TRY(cudaEventRecord(ev_comp[b], p->st));
         // D2H of the inner C cells, after the stepping and after H2D(c+1) read their tail
