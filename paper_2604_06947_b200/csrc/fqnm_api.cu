@@ -216,8 +216,12 @@ struct fqnm_plan {
     int* pipe_sign = nullptr;            // per chunk sign bits (pipelined fqnm_step_host)
     int* pipe_sign_host = nullptr;
     int sign_preset = 0;                 // sign_hint a caller (the pipeline) proved for one call
-    fqnm_plan_t* pipe_child = nullptr;
+    fqnm_plan_t* pipe_child = nullptr;   // the child plan of the full chunk size C
     int64_t pipe_H = 0, pipe_C = 0, pipe_m = 0;
+    // chunk list (ramped: the first and last full chunks are cut into C/8, C/8, C/4, C/2 so the
+    // un-overlapped first H2D and last D2H are small); pipe_kids[i] steps chunks of size C >> i
+    std::vector<int64_t> pipe_start, pipe_size;
+    fqnm_plan_t* pipe_kids[4] = {nullptr, nullptr, nullptr, nullptr};
     void* pipe_buf[3] = {nullptr, nullptr, nullptr};
     int32_t* pipe_head = nullptr;        // copy of q_host[0, H) taken before any D2H (the last
                                          // chunk's periodic right halo)
@@ -885,16 +889,21 @@ extern "C" int fqnm_plan_3d(fqnm_plan_t** out, int64_t nx, int64_t ny, int64_t n
 
 static void pipe_release(fqnm_plan_t* p)
 {
+    for (int i = 1; i < 4; ++i) {
+        if (p->pipe_kids[i]) fqnm_destroy(p->pipe_kids[i]);
+        p->pipe_kids[i] = nullptr;
+    }
     if (p->pipe_child) fqnm_destroy(p->pipe_child);
     p->pipe_child = nullptr;
+    p->pipe_kids[0] = nullptr;
+    p->pipe_start.clear();
+    p->pipe_size.clear();
     for (int i = 0; i < 3; ++i) {
         if (p->pipe_buf[i]) cudaFree(p->pipe_buf[i]);
         p->pipe_buf[i] = nullptr;
     }
     if (p->pipe_head) cudaFree(p->pipe_head);
     p->pipe_head = nullptr;
-    if (p->md_guard) cudaFree(p->md_guard);
-    if (p->md_guard_host) cudaFreeHost(p->md_guard_host);
     if (p->pipe_sign) cudaFree(p->pipe_sign);
     p->pipe_sign = nullptr;
     if (p->pipe_sign_host) cudaFreeHost(p->pipe_sign_host);
@@ -927,6 +936,8 @@ extern "C" void fqnm_destroy(fqnm_plan_t* p)
     if (p->hflags) cudaFree(p->hflags);
     if (p->pflags) cudaFree(p->pflags);
     if (p->pcounter) cudaFree(p->pcounter);
+    if (p->md_guard) cudaFree(p->md_guard);
+    if (p->md_guard_host) cudaFreeHost(p->md_guard_host);
     for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
     pipe_release(p);
     delete p;
@@ -1513,6 +1524,22 @@ extern "C" int fqnm_observe(const fqnm_plan_t* p, const void* q, double* u)
 // the H2D copy of chunk c+1 and the D2H copy of chunk c-1 overlap the stepping of
 // chunk c (three streams, events).  The input range check of each extended region
 // runs on the device and, if it fails, turns that chunk's launches into no-ops.
+#ifndef FQNM_PIPE_RAMP
+#define FQNM_PIPE_RAMP 1       // pipelined fqnm_step_host: ramped first/last chunks (C/8 .. C/2)
+#endif
+#ifndef FQNM_PIPE_DUAL
+#define FQNM_PIPE_DUAL 0       // pipelined chunks: K2S + K2 dual launch on the device sign bits
+                               // (measured slower on cfg4 e2e: 3535 vs 3602 GCUPS)
+#endif
+#ifndef FQNM_PIPE_SIGN_USE
+#define FQNM_PIPE_SIGN_USE 1   // experiment switch: 0 = read the sign bits but keep K2
+#endif
+#ifndef FQNM_PIPE_SIGN
+#define FQNM_PIPE_SIGN 0       // pipelined chunks: the host reads each chunk's sign bits and
+                               // steps one-signed chunks with K2S (the per-chunk host wait
+                               // measured 2977 vs 3615 GCUPS e2e; K2S on chunk-sized problems
+                               // is not faster than the voting K2 either: dual 3539-3593)
+#endif
 static int pipe_setup(fqnm_plan_t* p, int64_t nsteps)
 {
     const int64_t n = p->d.n_local;
@@ -1527,23 +1554,43 @@ static int pipe_setup(fqnm_plan_t* p, int64_t nsteps)
     if (!m) return FQNM_ERR_UNSUPPORTED;
     if (p->pipe_child && p->pipe_H == H && p->pipe_C == C) return FQNM_OK;
     pipe_release(p);
-    fqnm_plan_desc d = p->d;
-    d.n_local = d.n_global = C + 2 * H;
-    d.offset = 0;
-    d.boundary = FQNM_TRANSMISSIVE;
-    d.kappa_num = p->kap_num;
-    d.kappa_den = p->kap_den;
-    d.q_lo = p->lo;
-    d.q_hi = p->hi;
-    d.check_range = 0;
-    d.k = p->k;
-    d.stream = (void*)p->st;
-    fqnm_plan_t* c = nullptr;
-    int rc = plan_build(&c, &d, true);
-    if (rc != FQNM_OK) return rc;
-    if (c->family != 2 || c->rule != p->rule) { fqnm_destroy(c); return FQNM_ERR_UNSUPPORTED; }
-    c->st = p->st;
-    p->pipe_child = c;
+    // chunk list: m chunks of C, the first and last ramped when C/8 keeps the constraints
+    const bool ramp = FQNM_PIPE_RAMP && m >= 3 && (C / 8) % 32 == 0 && H * 16 <= C / 8;
+    {
+        std::vector<int64_t> sz;
+        if (ramp) { sz = {C / 8, C / 8, C / 4, C / 2}; }
+        for (int64_t i = ramp ? 1 : 0; i < (ramp ? m - 1 : m); ++i) sz.push_back(C);
+        if (ramp) { sz.push_back(C / 2); sz.push_back(C / 4); sz.push_back(C / 8); sz.push_back(C / 8); }
+        int64_t st0 = 0;
+        for (int64_t x : sz) { p->pipe_start.push_back(st0); p->pipe_size.push_back(x); st0 += x; }
+        if (st0 != n) { pipe_release(p); return FQNM_ERR_UNSUPPORTED; }
+    }
+    for (int i = 0; i < (ramp ? 4 : 1); ++i) {
+        fqnm_plan_desc d = p->d;
+        d.n_local = d.n_global = (C >> i) + 2 * H;
+        d.offset = 0;
+        d.boundary = FQNM_TRANSMISSIVE;
+        d.kappa_num = p->kap_num;
+        d.kappa_den = p->kap_den;
+        d.q_lo = p->lo;
+        d.q_hi = p->hi;
+        d.check_range = 0;
+        d.k = p->k;
+        d.stream = (void*)p->st;
+        fqnm_plan_t* c = nullptr;
+        int rc = plan_build(&c, &d, true);
+        if (rc != FQNM_OK) { pipe_release(p); return rc; }
+        if (c->family != 2 || c->rule != p->rule) {
+            fqnm_destroy(c);
+            pipe_release(p);
+            return FQNM_ERR_UNSUPPORTED;
+        }
+        c->st = p->st;
+        c->persist = 0;                  // chunk steps keep the launch-per-block K2
+        p->pipe_kids[i] = c;
+        if (i == 0) p->pipe_child = c;
+    }
+    m = (int64_t)p->pipe_size.size();
     p->pipe_H = H;
     p->pipe_C = C;
     p->pipe_m = m;
@@ -1589,24 +1636,15 @@ static int step_host_pipelined(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
 //    pipe_head on the H2D stream before H2D(0) (so before D2H(0)) and taken from there;
 //  * chunk c's right halo and chunk 0's left halo are outputs of later D2Hs, which follow
 //    that chunk's H2D through the compute dependency.
-#ifndef FQNM_PIPE_DUAL
-#define FQNM_PIPE_DUAL 0       // pipelined chunks: K2S + K2 dual launch on the device sign bits
-                               // (measured slower on cfg4 e2e: 3535 vs 3602 GCUPS)
-#endif
-#ifndef FQNM_PIPE_SIGN_USE
-#define FQNM_PIPE_SIGN_USE 1   // experiment switch: 0 = read the sign bits but keep K2
-#endif
-#ifndef FQNM_PIPE_SIGN
-#define FQNM_PIPE_SIGN 0       // pipelined chunks: the host reads each chunk's sign bits and
-                               // steps one-signed chunks with K2S (the per-chunk host wait
-                               // measured 2977 vs 3615 GCUPS e2e; K2S on chunk-sized problems
-                               // is not faster than the voting K2 either: dual 3539-3593)
-#endif
 static int step_host_pipelined_impl(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
 {
-    const int64_t n = p->d.n_local, C = p->pipe_C, H = p->pipe_H, m = p->pipe_m, E = C + 2 * H;
-    fqnm_plan_t* ch = p->pipe_child;
-    ch->st = p->st;                                                // the caller's current stream
+    const int64_t n = p->d.n_local, C = p->pipe_C, H = p->pipe_H, m = p->pipe_m;
+    auto kid_of = [&](int64_t c) -> fqnm_plan_t* {
+        const int64_t sz = p->pipe_size[c];
+        for (int i = 0; i < 4; ++i)
+            if (p->pipe_kids[i] && (C >> i) == sz) return p->pipe_kids[i];
+        return nullptr;
+    };
     cudaEvent_t* ev_in = p->pipe_ev;
     cudaEvent_t* ev_comp = p->pipe_ev + 3;
     cudaEvent_t* ev_out = p->pipe_ev + 6;
@@ -1619,8 +1657,9 @@ static int step_host_pipelined_impl(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
     auto h2d = [&](int64_t c) -> int {
         const int b = (int)(c % 3);
         int32_t* buf = (int32_t*)p->pipe_buf[b];
+        const int64_t E = p->pipe_size[c] + 2 * H;
         if (c >= 3) CUDA_TRY(cudaStreamWaitEvent(p->pipe_h2d, ev_out[b], 0));   // buffer free
-        int64_t s0 = c * C - H;
+        int64_t s0 = p->pipe_start[c] - H;
         if (s0 < 0) s0 += n;
         const int64_t first = (s0 + E <= n) ? E : n - s0;
         CUDA_TRY(cudaMemcpyAsync(buf, qh + s0, (size_t)first * 4, cudaMemcpyHostToDevice, p->pipe_h2d));
@@ -1642,6 +1681,10 @@ static int step_host_pipelined_impl(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
     for (int64_t c = 0; c < m; ++c) {
         const int b = (int)(c % 3);
         int32_t* buf = (int32_t*)p->pipe_buf[b];
+        const int64_t Cc = p->pipe_size[c], E = Cc + 2 * H;
+        fqnm_plan_t* ch = kid_of(c);
+        if (!ch) return fail(FQNM_ERR_ARG, "e2e pipeline: no child plan for chunk %lld", (long long)c);
+        ch->st = p->st;                                            // the caller's current stream
         if (c + 1 < m && (rc = h2d(c + 1)) != FQNM_OK) return rc;  // reads chunk c's cells: first
         // range check + stepping on the compute stream
         CUDA_TRY(cudaStreamWaitEvent(p->st, ev_in[b], 0));
@@ -1653,9 +1696,7 @@ static int step_host_pipelined_impl(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
             ch->guard = p->pipe_guard + c;
             ch->sign_dev = FQNM_PIPE_DUAL ? p->pipe_sign + c : nullptr;
             if (!FQNM_PIPE_DUAL && FQNM_PIPE_SIGN && blocked_sign_has_rule(ch->rule)) {
-                // read the chunk's sign bits on the host: the guard runs right after the
-                // previous chunk's stepping on this stream, so the wait overlaps that
-                // stepping and the stream idles only for the launch latency of the next
+                // read the chunk's sign bits on the host (measured slower, off by default)
                 CUDA_TRY(cudaMemcpyAsync(p->pipe_sign_host + c, p->pipe_sign + c, sizeof(int),
                                          cudaMemcpyDeviceToHost, p->st));
                 CUDA_TRY(cudaStreamSynchronize(p->st));
@@ -1674,10 +1715,11 @@ static int step_host_pipelined_impl(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
         ch->sign_preset = 0;
         if (rc != FQNM_OK) return rc;
         CUDA_TRY(cudaEventRecord(ev_comp[b], p->st));
-        // D2H of the inner C cells, after the stepping and after H2D(c+1) read their tail
+        // D2H of the inner cells, after the stepping and after H2D(c+1) read their tail
         CUDA_TRY(cudaStreamWaitEvent(p->pipe_d2h, ev_comp[b], 0));
         if (c + 1 < m) CUDA_TRY(cudaStreamWaitEvent(p->pipe_d2h, ev_in[(c + 1) % 3], 0));
-        CUDA_TRY(cudaMemcpyAsync(qh + c * C, buf + H, (size_t)C * 4, cudaMemcpyDeviceToHost, p->pipe_d2h));
+        CUDA_TRY(cudaMemcpyAsync(qh + p->pipe_start[c], buf + H, (size_t)Cc * 4, cudaMemcpyDeviceToHost,
+                                 p->pipe_d2h));
         CUDA_TRY(cudaEventRecord(ev_out[b], p->pipe_d2h));
     }
     if (check)

@@ -1,6 +1,3 @@
 mkdir -p gpurun_out
-B=$PWD/paper_2604_06947_b200/build
-for v in default cap2 cap2dual cap4dual dual; do
-  if [ $v = default ]; then L=$PWD/paper_2604_06947_b200/libfqnm.so; else L=$B/libfqnm_$v.so; fi
-  FQNM_LIBPATH=$L timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu --no-parity > gpurun_out/bench_$v.log 2>&1
-done
+timeout 900 python -m pytest tests/test_gpu_e2e.py -q -x > gpurun_out/t.log 2>&1; echo EXIT $? >> gpurun_out/t.log
+for r in 1 2; do timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/bench_ramp$r.log 2>&1; done
