@@ -20,7 +20,7 @@ from typing import Optional
 __all__ = [
     "FqnmError", "Plan", "fqnm_plan", "fqnm_plan_ex", "fqnm_step", "fqnm_step_block",
     "fqnm_observe", "fqnm_step_host", "fqnm_get_info", "fqnm_transfer", "fqnm_transfer_device",
-    "fqnm_roe_transfer_device", "fqnm_debug_override", "fqnm_launch_count", "fqnm_destroy",
+    "fqnm_roe_transfer_device", "fqnm_debug_override", "fqnm_debug_rcp_sqrt", "fqnm_launch_count", "fqnm_destroy",
     "fqnm_plan_validate", "fqnm_profile_enable", "fqnm_profile_read", "fqnm_halo_buffers",
     "fqnm_halo_connect", "fqnm_halo_owned", "fqnm_step_group", "fqnm_ipc_export",
     "fqnm_ipc_open", "fqnm_ipc_close", "owned_tensor", "fqnm_plan_2d", "fqnm_transfer2",
@@ -145,6 +145,7 @@ def _load():
     L.fqnm_transfer2_device.argtypes = [vp, vp, vp, vp, i64]
     L.fqnm_equivalence.argtypes = [vp, vp, vp, i64, i64, ctypes.POINTER(EquivalenceStats)]
     L.fqnm_debug_override.argtypes = [vp, i32, i32, i32]
+    L.fqnm_debug_rcp_sqrt.argtypes = [i64, ctypes.c_uint64, i32, i32, ctypes.POINTER(ctypes.c_int64)]
     L.fqnm_plan_validate.argtypes = [ctypes.POINTER(PlanDesc), ctypes.POINTER(PlanInfo)]
     L.fqnm_profile_enable.argtypes = [vp, ctypes.c_int]
     L.fqnm_profile_read.argtypes = [vp, ctypes.POINTER(dbl), ctypes.POINTER(i64)]
@@ -537,6 +538,14 @@ def fqnm_roe_transfer_device(plan: Plan, qL, qR):
 
 def fqnm_debug_override(plan: Plan, kernel: int = 0, k: int = 0, cells_per_thread: int = 0):
     _check(_load().fqnm_debug_override(plan.handle, int(kernel), int(k), int(cells_per_thread)))
+
+
+def fqnm_debug_rcp_sqrt(n: int, seed: int = 0, e_lo: int = -60, e_hi: int = 60):
+    """(rcp mismatches, sqrt mismatches, range flags) of the Euler kernel's own 1/x and
+    sqrt sequences against the CUDA library's correctly rounded ones on n random doubles."""
+    out = (ctypes.c_int64 * 3)()
+    _check(_load().fqnm_debug_rcp_sqrt(int(n), int(seed), int(e_lo), int(e_hi), out))
+    return int(out[0]), int(out[1]), int(out[2])
 
 
 # ---- fused peer-memory halo exchange --------------------------------------

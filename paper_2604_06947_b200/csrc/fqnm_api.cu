@@ -238,6 +238,24 @@ struct fqnm_plan {
     size_t ev_used = 0;
 };
 
+extern "C" int fqnm_debug_rcp_sqrt(int64_t n, uint64_t seed, int32_t e_lo, int32_t e_hi,
+                                   int64_t* mismatches)
+{
+    if (!mismatches) return fail(FQNM_ERR_ARG, "null argument");
+    if (n < 0 || e_lo < -1022 || e_hi > 1023 || e_lo > e_hi)
+        return fail(FQNM_ERR_ARG, "exponent range must satisfy -1022 <= e_lo <= e_hi <= 1023");
+    unsigned long long* d = nullptr;
+    unsigned long long h[3] = {0, 0, 0};
+    CUDA_TRY(cudaMalloc(&d, sizeof h));
+    cudaError_t e = cudaMemset(d, 0, sizeof h);
+    if (e == cudaSuccess && n > 0) e = launch_rcp_sqrt_check(n, seed, e_lo, e_hi, d, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return fail(FQNM_ERR_CUDA, "rcp/sqrt check: %s", cudaGetErrorString(e));
+    for (int i = 0; i < 3; ++i) mismatches[i] = (int64_t)h[i];
+    return FQNM_OK;
+}
+
 static void fill_info(const fqnm_plan_t* p, fqnm_plan_info* info);
 static int plan_build(fqnm_plan_t** out, const fqnm_plan_desc* din, bool allocate,
                       bool trusted_range = false);

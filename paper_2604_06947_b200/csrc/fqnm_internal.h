@@ -225,6 +225,9 @@ cudaError_t launch_euler(int V, const EulerArgs& a, cudaStream_t st);
 cudaError_t launch_roe_transfer(const int64_t* qL, const int64_t* qR, int64_t* T, int64_t n,
                                 double delta, double s, double g1, cudaStream_t st);
 
+cudaError_t launch_rcp_sqrt_check(int64_t n, uint64_t seed, int e_lo, int e_hi,
+                                  unsigned long long* counts, cudaStream_t st);
+
 int blocked_max_V();
 bool blocked_has_V(int V);
 bool blocked_rule_has_V(int rule, int V);

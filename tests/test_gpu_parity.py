@@ -699,3 +699,54 @@ def test_eo_beyond_fast_domain_falls_back_to_int64(F, n):
     with pytest.raises(F.FqnmError) as e:
         F.fqnm_step(plan, to_dev(q2), 1)
     assert e.value.status == 3
+
+
+def test_euler_branch_free_rcp_sqrt_match_library(F):
+    """The Euler kernel's own 1/x and sqrt sequences (branch-free interior windows) are the
+    correctly rounded results: bit-identical to __drcp_rn / __dsqrt_rn on 2^26 random
+    doubles over the physical exponent range and over the whole range their flag admits;
+    outside it the flag is raised (the kernel then redoes the window with the library)."""
+    assert F.fqnm_debug_rcp_sqrt(1 << 26, 1, -40, 40) == (0, 0, 0)
+    assert F.fqnm_debug_rcp_sqrt(1 << 26, 2, -767, 256) == (0, 0, 0)
+    r, s, flagged = F.fqnm_debug_rcp_sqrt(1 << 20, 3, 300, 400)
+    assert flagged == 1 << 20
+    r, s, flagged = F.fqnm_debug_rcp_sqrt(1 << 20, 4, -1022, -800)
+    assert flagged == 1 << 20
+
+
+@pytest.mark.parametrize("kind", [3, 4])
+def test_euler_random_field_steps(F, kind):
+    """Euler/Roe on a rough random field (every interface a different Riemann problem,
+    subsonic, transonic and supersonic: the Harten branch, both signs of every transfer),
+    many windows and a ragged tail, 4 steps, all three V; plus one cell with a count above
+    2^50 so that window leaves the branch-free path."""
+    rng = np.random.default_rng(77)
+    n = 40 * 1024 + 19
+    x = np.arange(n) / n
+    rho = 1.0 + 0.5 * np.sin(2 * np.pi * 3 * x) + rng.uniform(-0.05, 0.05, n)
+    p = 1.0 + 0.4 * np.cos(2 * np.pi * 5 * x) + rng.uniform(-0.05, 0.05, n)
+    mach = 1.5 * np.sin(2 * np.pi * 2 * x) + rng.uniform(-0.1, 0.1, n)
+    u = mach * np.sqrt(1.4 * p / rho)
+    E = p / 0.4 + 0.5 * rho * u * u
+    delta = 1e-7
+    lam = 0.05
+    if kind == 3:
+        q0 = np.stack([np.rint(rho / delta), np.rint(rho * u / delta), np.rint(E / delta)]).astype(np.int64)
+        run = lambda q, s: oracle.euler_run(q, s, delta, lam)
+    else:
+        q0 = oracle.pack_mixed(np.rint(rho / delta).astype(np.int64), rho * u, E)
+        run = lambda q, s: oracle.euler_density_run(q, s, delta, lam)
+    ref = run(q0, 4)
+    for V in (1, 2, 4):
+        plan = F.fqnm_plan(n, delta, lam, kind, F.TRANSMISSIVE)
+        F.fqnm_debug_override(plan, 0, 0, V)
+        q = to_dev(q0, torch.int64)
+        F.fqnm_step(plan, q, 4)
+        assert np.array_equal(q.cpu().numpy(), ref), V
+    if kind == 3:
+        q1 = q0.copy()
+        q1[:, 20000] = [(1 << 50) + 12345, 0, (1 << 51) + 999]      # huge but finite state
+        plan = F.fqnm_plan(n, delta, lam, kind, F.TRANSMISSIVE)
+        q = to_dev(q1, torch.int64)
+        F.fqnm_step(plan, q, 1)
+        assert np.array_equal(q.cpu().numpy(), run(q1, 1))
