@@ -553,7 +553,10 @@ static int choose_kernel(fqnm_plan_t* p)
     const fqnm_plan_desc& d = p->d;
     if (d.nvar == 3) {
         p->family = 5;
-        p->V = 1;                       // 100 registers, 20 warps/SM: 53.3 vs 51.5 (V = 2) GCUPS
+        // V = 2 (64-cell windows, 151 registers, 12 warps/SM) since the branch-free interior
+        // path: cfg5 80.8 vs 70.4 (V = 1) vs 71.7 (V = 4) GCUPS; small problems keep V = 1
+        // (twice the warps)
+        p->V = (d.n_local * (d.batch > 0 ? d.batch : 1) >= (1 << 17)) ? 2 : 1;
         p->k = 1;
         return FQNM_OK;
     }
