@@ -541,11 +541,12 @@ def fqnm_debug_override(plan: Plan, kernel: int = 0, k: int = 0, cells_per_threa
 
 
 def fqnm_debug_rcp_sqrt(n: int, seed: int = 0, e_lo: int = -60, e_hi: int = 60):
-    """(rcp mismatches, sqrt mismatches, range flags) of the Euler kernel's own 1/x and
-    sqrt sequences against the CUDA library's correctly rounded ones on n random doubles."""
-    out = (ctypes.c_int64 * 3)()
+    """(rcp mismatches, sqrt mismatches, range flags, div mismatches) of the Euler kernel's
+    own 1/x, sqrt and x/y sequences against the CUDA library's correctly rounded ones on n
+    random doubles."""
+    out = (ctypes.c_int64 * 4)()
     _check(_load().fqnm_debug_rcp_sqrt(int(n), int(seed), int(e_lo), int(e_hi), out))
-    return int(out[0]), int(out[1]), int(out[2])
+    return int(out[0]), int(out[1]), int(out[2]), int(out[3])
 
 
 # ---- fused peer-memory halo exchange --------------------------------------

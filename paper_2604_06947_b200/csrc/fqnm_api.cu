@@ -245,14 +245,14 @@ extern "C" int fqnm_debug_rcp_sqrt(int64_t n, uint64_t seed, int32_t e_lo, int32
     if (n < 0 || e_lo < -1022 || e_hi > 1023 || e_lo > e_hi)
         return fail(FQNM_ERR_ARG, "exponent range must satisfy -1022 <= e_lo <= e_hi <= 1023");
     unsigned long long* d = nullptr;
-    unsigned long long h[3] = {0, 0, 0};
+    unsigned long long h[4] = {0, 0, 0, 0};
     CUDA_TRY(cudaMalloc(&d, sizeof h));
     cudaError_t e = cudaMemset(d, 0, sizeof h);
     if (e == cudaSuccess && n > 0) e = launch_rcp_sqrt_check(n, seed, e_lo, e_hi, d, 0);
     if (e == cudaSuccess) e = cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
     cudaFree(d);
     if (e != cudaSuccess) return fail(FQNM_ERR_CUDA, "rcp/sqrt check: %s", cudaGetErrorString(e));
-    for (int i = 0; i < 3; ++i) mismatches[i] = (int64_t)h[i];
+    for (int i = 0; i < 4; ++i) mismatches[i] = (int64_t)h[i];
     return FQNM_OK;
 }
 

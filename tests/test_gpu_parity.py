@@ -706,11 +706,12 @@ def test_euler_branch_free_rcp_sqrt_match_library(F):
     correctly rounded results: bit-identical to __drcp_rn / __dsqrt_rn on 2^26 random
     doubles over the physical exponent range and over the whole range their flag admits;
     outside it the flag is raised (the kernel then redoes the window with the library)."""
-    assert F.fqnm_debug_rcp_sqrt(1 << 26, 1, -40, 40) == (0, 0, 0)
-    assert F.fqnm_debug_rcp_sqrt(1 << 26, 2, -767, 256) == (0, 0, 0)
-    r, s, flagged = F.fqnm_debug_rcp_sqrt(1 << 20, 3, 300, 400)
+    assert F.fqnm_debug_rcp_sqrt(1 << 26, 1, -40, 40) == (0, 0, 0, 0)
+    assert F.fqnm_debug_rcp_sqrt(1 << 26, 2, -767, 256) == (0, 0, 0, 0)
+    assert F.fqnm_debug_rcp_sqrt(1 << 26, 5, -120, 120) == (0, 0, 0, 0)
+    r, s, flagged, _ = F.fqnm_debug_rcp_sqrt(1 << 20, 3, 300, 400)
     assert flagged == 1 << 20
-    r, s, flagged = F.fqnm_debug_rcp_sqrt(1 << 20, 4, -1022, -800)
+    r, s, flagged, _ = F.fqnm_debug_rcp_sqrt(1 << 20, 4, -1022, -800)
     assert flagged == 1 << 20
 
 
