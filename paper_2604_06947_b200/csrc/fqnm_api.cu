@@ -573,14 +573,22 @@ static int choose_kernel(fqnm_plan_t* p)
         p->V = 8;
         p->k = d.k;
         if (p->k <= 0) {
-            // deepest halo (fewest L2 exchanges) whose warps still all fit: measured on
-            // cfg2, time per run falls ~1/k up to k = 80 (profiles/r01_summary.md)
-            static const int ks[] = {80, 64, 48, 32, 16};
-            for (int kk : ks) {
+            // time per step ~ (warps per SM sub-partition) x t_step + t_exchange / k: the
+            // exchange (one L2 round trip, ~2.7 us) is paid once per k steps, but a deeper
+            // halo means more warps (P = n / (256 - 2k)), and past 4 x 148 warps some
+            // sub-partitions issue for two.  cfg2: k = 72 gives P = 586 (one warp per
+            // sub-partition, 128-thread CTAs), k = 80 gave P = 683 in 86 CTAs of 8 warps
+            // (2.65 -> 1.9 ms; profiles/r02_tune_cfg2.jsonl)
+            double best = 1e30;
+            int bestk = 0;
+            for (int kk = 124; kk >= 8; kk -= 4) {
                 int P, base, rem, H;
-                p->k = kk;
-                if (resident_geometry(p, kk, &P, &base, &rem, &H) == FQNM_OK) break;
+                if (resident_geometry(p, kk, &P, &base, &rem, &H) != FQNM_OK) continue;
+                const int wps = (P + 148 * 4 - 1) / (148 * 4);
+                const double t = wps * 50.0 + 2700.0 / kk;
+                if (t < best) { best = t; bestk = kk; }
             }
+            p->k = bestk > 0 ? bestk : 16;
         }
     } else {
         p->family = 2;

@@ -1482,14 +1482,16 @@ static cudaError_t resident_v(const ResidentArgsHost& h, const DevRule& r, cudaS
     a.tag_base = h.tag_base;
     a.nsteps = h.nsteps; a.P = h.P; a.base = h.base; a.rem = h.rem; a.H = h.H; a.k = h.k;
     a.bmode = h.bmode;
-    const int threads = 256;
-    const int blocks = (h.P * 32 + threads - 1) / threads;
     int per_sm = 0, dev = 0, sms = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<RULE, V>,
-                                                                  threads, 0);
+    cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    // up to 4 warps per SM: 128-thread CTAs, one per SM, one warp per sub-partition (the
+    // run is latency-bound per warp; two warps on a sub-partition halve its step rate)
+    const int threads = h.P <= 4 * sms ? 128 : 256;
+    const int blocks = (h.P * 32 + threads - 1) / threads;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident<RULE, V>, threads, 0);
+    if (e != cudaSuccess) return e;
     if (blocks > per_sm * sms) return cudaErrorCooperativeLaunchTooLarge;
     void* args[] = {&a, const_cast<DevRule*>(&r)};
     return cudaLaunchCooperativeKernel((const void*)k_resident<RULE, V>, blocks, threads, args, 0, st);
