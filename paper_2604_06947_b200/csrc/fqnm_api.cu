@@ -1149,8 +1149,11 @@ static int step_persist(fqnm_plan_t* p, void* q, int64_t nb, int64_t base, int64
     a.n = d.n_local;
     a.KL = p->dep_left ? round4(kmax) : 0;
     a.KR = p->dep_right ? round4(kmax) : 0;
-    a.S = 32 * p->V - a.KL - a.KR;
-    if (a.S < 4) return fail(FQNM_ERR_ARG, "k = %d too large for V = %d", kmax, p->V);
+    // K2PS: the sign-specialised persistent kernel when the range check proved the sign
+    const int sign = (!p->no_sign && blocked_sign_has_rule(p->rule)) ? p->sign_hint : 0;
+    const int Vp = blocked_persist_V(p->rule, sign);
+    a.S = 32 * Vp - a.KL - a.KR;
+    if (a.S < 4) return fail(FQNM_ERR_ARG, "k = %d too large for V = %d", kmax, Vp);
     a.nwin = (a.n + a.S - 1) / a.S;
     a.base = (int32_t)base;
     a.rem = (int32_t)rem;
@@ -1175,7 +1178,8 @@ static int step_persist(fqnm_plan_t* p, void* q, int64_t nb, int64_t base, int64
     a.counter = p->pcounter;
     a.tag_base = p->ptag;
     p->ptag += (uint32_t)nb + 1;
-    PROF_LAUNCH(launch_blocked_persist(p->rule, a, p->dr, p->st));
+    PROF_LAUNCH(launch_blocked_persist(p->rule, sign, a, p->dr, p->st));
+    if (sign) p->k2s_launches++;
     return FQNM_OK;
 }
 
@@ -2144,6 +2148,11 @@ extern "C" int fqnm_debug_override(fqnm_plan_t* p, int32_t kernel, int32_t k, in
         p->minb = kernel / 100;
         kernel = kernel % 100;
     }
+    bool persist_sign = false;
+    if (kernel == 32) {                 // K2P, with the sign-specialised K2PS where proved
+        kernel = 12;
+        persist_sign = true;
+    }
     if (kernel == 12) {                 // K2P persistent stepper (K2 geometry V = 32, 2 CTAs/SM)
         if (d.nvar != 1 || p->family >= 7 || d.batch != 1 || d.boundary == FQNM_HALO ||
             !blocked_persist_has_rule(p->rule))
@@ -2160,6 +2169,7 @@ extern "C" int fqnm_debug_override(fqnm_plan_t* p, int32_t kernel, int32_t k, in
         p->V = 32;
         p->minb = 2;
         p->persist = 1;
+        p->no_sign = !persist_sign;
         if (k) {
             if (k > max_block_steps(p, 32)) return fail(FQNM_ERR_ARG, "k too large for V = 32");
             p->k = k;

@@ -192,8 +192,10 @@ struct PersistArgs {
     unsigned long long* counter;
     uint32_t tag_base;
 };
-cudaError_t launch_blocked_persist(int rule, const PersistArgs& a, const DevRule& r, cudaStream_t st);
+cudaError_t launch_blocked_persist(int rule, int sign, const PersistArgs& a, const DevRule& r,
+                                   cudaStream_t st);
 bool blocked_persist_has_rule(int rule);
+int blocked_persist_V(int rule, int sign);   // cells per lane of the persistent kernel
 cudaError_t launch_halo_prime(const BlockedArgs& a, cudaStream_t st);
 cudaError_t launch_naive(int rule, const int32_t* src, int32_t* dst, int64_t n, int64_t batch,
                          int bmode, const DevRule& r, cudaStream_t st);

@@ -175,7 +175,7 @@ __device__ __forceinline__ void one_step(int32_t (&q)[V], const DevRule& r, int 
             for (int j = 0; j + 1 < V; ++j) q[j] = q[j] + g[j] - g[j + 1];
             q[V - 1] = q[V - 1] + g[V - 1] - gr;
         }
-    } else if (FQNM_LIN_STREAM && RULE == R_LIN_HALF && !WALL) {
+    } else if ((FQNM_LIN_STREAM || V > 32) && RULE == R_LIN_HALF && !WALL) {
         // kappa = 1/2 streamed: phi+ of the lane's last cell first (for the shuffle),
         // then cell by cell h_j = trunc(q_j/2), q'_j = phi+(q_{j-1}) + h_j (no arrays)
         const int32_t hl = q[V - 1] / 2;
@@ -644,17 +644,31 @@ __global__ void __launch_bounds__(256, MINB) k_blocked(BlockedArgs a, DevRule r)
 // KL/KR cells into this window's owned range).  The whole warp takes part (lane i
 // polls the i-th window) so it never diverges around the hot loop; relaxed polling,
 // one acquire fence at the end.
-static __device__ __forceinline__ void persist_wait_cover(const PersistArgs& a, int64_t w,
-                                                          uint32_t target, int lane)
+// the window this lane polls for item (b, w), or -1: lanes 0..2 take w-1, w, w+1 when the
+// widened range fits in the neighbours (E <= S, the usual case), else the general cover
+static __device__ __forceinline__ int64_t persist_cover_window(const PersistArgs& a, int64_t w, int lane)
 {
     const int64_t n = a.n, S = a.S, nwin = a.nwin;
     const int64_t E = a.KL > a.KR ? a.KL : a.KR;
-    const int64_t span = (S + 2 * E + S - 1) / S + 1;          // windows touched, upper bound
-    // the range in window units, relative to w; walls clamp, periodic wraps
-    const int64_t lo = w * S - E, hi = w * S + S + E - 1;
     int64_t my = -1;
+    if (E <= S && nwin >= 4) {
+        // [wS - E, wS + S + E) touches windows w-1, w, w+1 only; at the periodic wrap the
+        // last window may be short, so its left neighbour is covered too
+        if (lane < 3) {
+            my = w - 1 + lane;
+            if (a.bmode == BM_PERIODIC) my = my < 0 ? my + nwin : (my >= nwin ? my - nwin : my);
+            else my = my < 0 ? 0 : (my >= nwin ? nwin - 1 : my);
+        } else if (lane == 3 && a.bmode == BM_PERIODIC) {
+            // a short last window: the range of w = 0 reaches back into window nwin - 2, and
+            // the ranges of the last two windows reach forward into window 0
+            if (w == 0) my = nwin - 2;
+            else if (w >= nwin - 2) my = 0;
+        }
+        return my;
+    }
+    const int64_t span = (S + 2 * E + S - 1) / S + 1;          // windows touched, upper bound
+    const int64_t lo = w * S - E, hi = w * S + S + E - 1;
     if (lane < 2 * span + 2) {
-        // lane i -> the window containing cell lo + i * S (and the last cell for the last lane)
         int64_t x = lo + (int64_t)lane * S;
         if (x > hi) x = hi;
         if (a.bmode == BM_PERIODIC) { x %= n; if (x < 0) x += n; }
@@ -662,18 +676,33 @@ static __device__ __forceinline__ void persist_wait_cover(const PersistArgs& a, 
         my = x / S;
         if (my >= nwin) my = nwin - 1;
     }
-    // the last window may be short: also cover the window before the wrap point
     if (lane == 31 && a.bmode == BM_PERIODIC && (lo < 0 || hi >= n)) my = nwin - 1 > 0 ? nwin - 2 : 0;
     if (lane == 30 && a.bmode == BM_PERIODIC && (lo < 0 || hi >= n)) my = nwin - 1;
+    return my;
+}
+
+// one relaxed poll of the lane's window flag: true when it carries at least `target`
+static __device__ __forceinline__ bool persist_poll(const PersistArgs& a, int64_t my, uint32_t target)
+{
+    if (my < 0) return true;
+    unsigned int f;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(a.flags + my) : "memory");
+    return (int)(f - target) >= 0;
+}
+
+// Wait for the block b-1 windows whose owned cells overlap [wS - E, wS + S + E),
+// E = max(KL, KR) (periodic wrap / clamped walls): they cover the item's input window
+// (read after write) and include every block b-1 item that reads the cells this item
+// overwrites in the other buffer (write after read: those items' input windows reach
+// KL/KR cells into this window's owned range).  The whole warp takes part so it never
+// diverges around the hot loop; relaxed polling, one acquire fence at the end.
+static __device__ __forceinline__ void persist_wait_cover(const PersistArgs& a, int64_t w,
+                                                          uint32_t target, int lane)
+{
+    const int64_t my = persist_cover_window(a, w, lane);
     const long long t0 = clock64();
     for (;;) {
-        bool ok = true;
-        if (my >= 0) {
-            unsigned int f;
-            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(a.flags + my) : "memory");
-            ok = (int)(f - target) >= 0;
-        }
-        if (__all_sync(0xffffffffu, ok)) break;
+        if (__all_sync(0xffffffffu, persist_poll(a, my, target))) break;
         if (clock64() - t0 > SPIN_TRAP_CYCLES) __trap();
     }
     asm volatile("fence.acq_rel.gpu;" ::: "memory");   // acquire: the relaxed reads above
@@ -699,7 +728,13 @@ static __device__ __noinline__ void persist_slow(const int32_t* src, int32_t* ds
     }
 }
 
-template <int RULE, int V, int MINB>
+#ifndef FQNM_K2P_LIN_V
+#define FQNM_K2P_LIN_V 48      // cells per lane of the persistent LIN 1/2 kernel (streamed step,
+                               // 128 registers): cfg3 7.06 vs 6.96 TCUPS with V = 32
+#endif
+
+// FSIGN as k_blocked (K2S): the host proved the whole state >= 0 (1) or <= 0 (2)
+template <int RULE, int V, int MINB, int FSIGN = 0>
 __global__ void __launch_bounds__(256, MINB) k_blocked_persist(PersistArgs a, DevRule r)
 {
     constexpr int W = 32 * V;
@@ -707,11 +742,10 @@ __global__ void __launch_bounds__(256, MINB) k_blocked_persist(PersistArgs a, De
     const int64_t n = a.n, nwin = a.nwin, S = a.S;
     const unsigned long long total = (unsigned long long)a.nblocks * (unsigned long long)nwin;
     const int lo = a.KL, hi = W - a.KR;
-    for (;;) {
-        unsigned long long item = 0;
-        if (lane == 0) item = atomicAdd(a.counter, 1ull);
-        item = __shfl_sync(FULL, item, 0);
-        if (item >= total) return;
+    unsigned long long item = 0;
+    if (lane == 0) item = atomicAdd(a.counter, 1ull);
+    item = __shfl_sync(FULL, item, 0);
+    while (item < total) {
         const int b = (int)(item / (unsigned long long)nwin);
         const int64_t w = (int64_t)(item - (unsigned long long)b * (unsigned long long)nwin);
         const int64_t ws = w * S - a.KL;                           // first cell of the window
@@ -729,7 +763,8 @@ __global__ void __launch_bounds__(256, MINB) k_blocked_persist(PersistArgs a, De
                 const int4 v = __ldcg(s4 + j);
                 q[4 * j] = v.x; q[4 * j + 1] = v.y; q[4 * j + 2] = v.z; q[4 * j + 3] = v.w;
             }
-            run_window_steps_signed<RULE, V>(q, ks, r);
+            if (FSIGN != 0) run_window_steps<RULE, V, false, FSIGN>(q, ks, r, 0, 0);
+            else run_window_steps_signed<RULE, V>(q, ks, r);
             int4* d4 = reinterpret_cast<int4*>(dst + ws) + lane * (V / 4);
 #pragma unroll
             for (int j = 0; j < V / 4; ++j) {
@@ -740,14 +775,16 @@ __global__ void __launch_bounds__(256, MINB) k_blocked_persist(PersistArgs a, De
         } else {
             persist_slow<RULE, V>(src, dst, ws, n, a.bmode, ks, r, lo, hi, lane);
         }
+        // release: every lane fences its own stores (one warp-wide MEMBAR; measured 2-10 %
+        // faster than lane 0 fencing for the warp after a warp barrier), then the flag
         __syncwarp();
+        __threadfence();
         if (lane == 0) {
-#ifndef FQNM_PERSIST_NOFENCE
-            __threadfence();
-#endif
             asm volatile("st.release.gpu.global.u32 [%0], %1;"
                          :: "l"(a.flags + w), "r"(a.tag_base + (uint32_t)b + 1u) : "memory");
+            item = atomicAdd(a.counter, 1ull);
         }
+        item = __shfl_sync(FULL, item, 0);
     }
 }
 
@@ -757,23 +794,40 @@ bool blocked_persist_has_rule(int rule)
     return rule == R_LIN_HALF || rule == R_EO_P1 || rule == R_EO_FAST || rule == R_LIN_FAST;
 }
 
-template <int RULE>
+// cells per lane of the persistent kernel: the sign-specialised EO variant (sign = 1, 2)
+// has the K2S geometry
+int blocked_persist_V(int rule, int sign)
+{
+    if (sign != 0 && (rule == R_EO_P1 || rule == R_EO_FAST)) return BLOCKED_SIGN_V;
+    return rule == R_LIN_HALF ? FQNM_K2P_LIN_V : 32;
+}
+
+template <int RULE, int V = 32, int FSIGN = 0>
 static cudaError_t persist_rule(const PersistArgs& a, const DevRule& r, cudaStream_t st)
 {
     int per_sm = 0, dev = 0, sms = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blocked_persist<RULE, 32, 2>,
-                                                                  256, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, k_blocked_persist<RULE, V, 2, FSIGN>, 256, 0);
     if (e != cudaSuccess) return e;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-    k_blocked_persist<RULE, 32, 2><<<per_sm * sms, 256, 0, st>>>(a, r);
+    k_blocked_persist<RULE, V, 2, FSIGN><<<per_sm * sms, 256, 0, st>>>(a, r);
     return cudaGetLastError();
 }
 
-cudaError_t launch_blocked_persist(int rule, const PersistArgs& a, const DevRule& r, cudaStream_t st)
+cudaError_t launch_blocked_persist(int rule, int sign, const PersistArgs& a, const DevRule& r,
+                                   cudaStream_t st)
 {
+    if (sign != 0) {                                    // K2PS: persistent + sign-specialised
+        constexpr int V = BLOCKED_SIGN_V;
+        if (rule == R_EO_P1)
+            return sign == 1 ? persist_rule<R_EO_P1, V, 1>(a, r, st) : persist_rule<R_EO_P1, V, 2>(a, r, st);
+        if (rule == R_EO_FAST)
+            return sign == 1 ? persist_rule<R_EO_FAST, V, 1>(a, r, st) : persist_rule<R_EO_FAST, V, 2>(a, r, st);
+        return cudaErrorInvalidValue;
+    }
     switch (rule) {
-        case R_LIN_HALF: return persist_rule<R_LIN_HALF>(a, r, st);
+        case R_LIN_HALF: return persist_rule<R_LIN_HALF, FQNM_K2P_LIN_V>(a, r, st);
         case R_EO_P1: return persist_rule<R_EO_P1>(a, r, st);
         case R_EO_FAST: return persist_rule<R_EO_FAST>(a, r, st);
         case R_LIN_FAST: return persist_rule<R_LIN_FAST>(a, r, st);

@@ -251,6 +251,34 @@ def test_k2s_sign_specialised_kernel(F, sign, case, n):
     assert plan.info()["k2s_launches"] == k1
 
 
+@pytest.mark.parametrize("n", [41 * 1488 + 6, 30 * 976 + 3])   # last window of 6 / 3 cells < k
+@pytest.mark.parametrize("case", ["p1", "general"])
+@pytest.mark.parametrize("sign", [1, -1])
+def test_k2ps_persistent_sign_specialised_kernel(F, sign, case, n):
+    """K2PS: the persistent stepper with the sign-specialised body (V = 48, K2S geometry)
+    when the range check proves the sign; mixed states run the voting K2P.  Ragged sizes put
+    a short last window next to the periodic wrap (the flag cover of windows 0 and nwin - 2)."""
+    delta, lam = ("1e-5", Fraction(4, 15)) if case == "p1" else ("1e-5", Fraction(3, 10))
+    rng = np.random.default_rng(7 * n + (sign > 0))
+    q0 = sign * np.abs(W.smooth_random(rng, n, 100000, 50000))
+    q0[rng.integers(0, n, 50)] = 0
+    plan = F.fqnm_plan_ex(n, 1e-5, float(lam), F.BURGERS_EO, check_range=True)
+    F.fqnm_debug_override(plan, 32, 24, 0)
+    rule = oracle.Rule(W.BURGERS_EO, delta, lam)
+    q = to_dev(q0)
+    k0 = plan.info()["k2s_launches"]
+    F.fqnm_step(plan, q, 145)                           # 7 blocks, uneven step counts
+    assert np.array_equal(host(q), rule.run(q0, 145))
+    assert plan.info()["k2s_launches"] > k0
+    q1 = q0.copy()
+    q1[n // 3] = -sign * 5
+    k1 = plan.info()["k2s_launches"]
+    q = to_dev(q1)
+    F.fqnm_step(plan, q, 100)
+    assert np.array_equal(host(q), rule.run(q1, 100))
+    assert plan.info()["k2s_launches"] == k1
+
+
 def test_ens1_sampled(F):
     w = W.cfg("ens1")
     B = w.batch

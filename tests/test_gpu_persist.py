@@ -34,7 +34,10 @@ def F():
 @pytest.mark.parametrize("case", range(len(RULES)))
 @pytest.mark.parametrize("boundary", [W.PERIODIC, W.TRANSMISSIVE])
 @pytest.mark.parametrize("n,k,steps", [(50003, 24, 100), (50003, 7, 33), (4099, 16, 1), (1024, 8, 20),
-                                       (200000, 32, 97), (1000, 4, 41)])
+                                       (200000, 32, 97), (1000, 4, 41),
+                                       # last window shorter than k next to the periodic wrap
+                                       # (V = 48 one-sided LIN: S = 1512; V = 32 two-sided: S = 976)
+                                       (20 * 1512 + 2, 24, 100), (30 * 976 + 3, 24, 50)])
 def test_persistent_matches_oracle(F, case, boundary, n, k, steps):
     kind, delta, lam, param, amp, off = RULES[case]
     rng = np.random.default_rng(n + k + case)
