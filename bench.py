@@ -56,6 +56,10 @@ RULE_NAMES = {1: "LIN_HALF", 2: "EO_FAST", 3: "GENERIC", 4: "LIN_FAST", 5: "EO_P
 SM_COUNT = 148
 LANES_PER_SM_CLK = 128                          # 4 SMSPs x 32 lanes, 1 warp-instr/clk each
 WINDOW = 2048                                   # cells per parity window
+# float64-pipe instructions (DMUL + DADD + DFMA + DSETP) the Euler kernel executes per
+# cell-update, counted by ncu on the V = 2 branch-free path (profiles/r02_summary.md;
+# 305 thread instructions in all): the basis of cfg5's FP64-issue roofline
+FP64_PER_CELL_EULER = 122
 
 
 def _peaks():
@@ -433,7 +437,8 @@ def run_cfg4(args):
         kname, ops_alg, updates_per_launch, per_launch_ms, hbm_bytes_per_launch,
         {"kernel_launches": kern_launches, "kernel_share_of_step": kern_ms / ms if ms > 0 else None,
          "k": info["k"], "V": Vk, "ops_basis": ops_key,
-         "windows_redundancy": 32.0 * Vk / (32.0 * Vk - 2 * ((info["k"] + 3) // 4 * 4))},
+         # K2S windows carry a halo on one side only (a one-signed state moves one way)
+         "windows_redundancy": 32.0 * Vk / (32.0 * Vk - (1 if k2s else 2) * ((info["k"] + 3) // 4 * 4))},
         mix_ceiling_key="eo_sign_step" if ops_key == "burgers_eo_sign_uniform" else "")
     tr, tr_src = ncu_traffic(n_local)
     if tr is not None:
@@ -484,6 +489,13 @@ def run_cfg4(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_cfg4(qmax)
 
+    # ---- the other BASELINE configurations, timed + parity-checked (rank 0, N = 1 only) ----
+    others = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        del q, plan
+        torch.cuda.empty_cache()
+        others = run_other_configs(dev, args.seed)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -497,7 +509,7 @@ def run_cfg4(args):
                        "parallelism": ("domain split x%d, %s halo" % (world, halo_mode))
                        if world > 1 else "single domain"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
-            "gpu_launches": launches, "parity": parity,
+            "gpu_launches": launches, "parity": parity, "other_configs": others,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -554,6 +566,120 @@ def verify_cfg4(args, q, off, n_local, N, offsets, total, qmax, inv0, dev, world
         out = {"ok": None, "error": repr(ex)[:300]}
     if world > 1:
         dist.barrier()
+    return out
+
+
+# ---------------------------------------------------------------------------
+def run_other_configs(dev, seed: int):
+    """The other BASELINE.json configurations, timed and parity-checked beside the headline
+    (N = 1 only; outside the timed region of the bench line): cfg1, cfg2 (full runs vs the
+    oracle), cfg3 and a cfg5 window (light-cone windows vs the oracle), ENS-1 (sampled
+    problems).  Each entry: best of 3 repetitions by CUDA events on the launching stream,
+    after one warm-up run; roofline fraction on SURVEY 8(d)-D3's basis where one applies."""
+    import torch
+    import oracle
+    import paper_2604_06947_b200 as F
+    import workloads as W
+    out = []
+    rng = np.random.default_rng(seed)
+
+    def best_ms(plan, q0, steps, reps=3):
+        q = q0.clone()
+        F.fqnm_step(plan, q, steps)
+        torch.cuda.synchronize()
+        best = 1e30
+        for _ in range(reps):
+            q.copy_(q0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            F.fqnm_step(plan, q, steps)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return best, q
+
+    def entry(name, plan, cells, steps, ms, ok, what, bound=None):
+        info = plan.info()
+        e = {"config": name, "cells": cells, "time_steps": steps, "ms": ms,
+             "GCUPS": cells * steps / ms / 1e6, "kernel": info["kernel"], "V": info["cells_per_thread"],
+             "k": info["k"], "parity": {"ok": bool(ok), "what": what}}
+        if bound:
+            e["roofline"] = dict(bound, frac=e["GCUPS"] / bound["peak_gcups"])
+        out.append(e)
+
+    def windows_ok(run, q0h, qh, n, steps, periodic, width=1024, count=2, axis=-1):
+        ok = True
+        for a in [0] + [int(x) for x in rng.integers(0, n - width, count)]:
+            if periodic:
+                idx = np.arange(a - steps, a + width + steps) % n
+                ref = run(np.ascontiguousarray(np.take(q0h, idx, axis=axis)))
+                ref = np.take(ref, np.arange(steps, steps + width), axis=axis)
+            else:
+                lo, hi = max(0, a - steps), min(n, a + width + steps)
+                ref = run(np.ascontiguousarray(np.take(q0h, np.arange(lo, hi), axis=axis)))
+                ref = np.take(ref, np.arange(a - lo, a - lo + width), axis=axis)
+            ok = ok and np.array_equal(ref, np.take(qh, np.arange(a, a + width), axis=axis))
+        return ok
+
+    sm_ghz = _peaks()[0].get("sm_max_mhz", 1965.0) / 1e3
+    issue4 = {"bound": "alu", "ops_alg_per_cell_update": 4, "peak_gcups": 148 * 128 * sm_ghz / 4}
+    try:
+        # cfg1: linear advection, N = 1024, 2000 steps (one warp, K3)
+        w = W.cfg("cfg1")
+        q0h = W.q0_cfg1()
+        plan = F.fqnm_plan(w.n, float(w.delta), W.dt_dx_double(w), F.LINEAR, F.PERIODIC)
+        ms, q = best_ms(plan, torch.tensor(q0h, dtype=torch.int32, device=dev), w.steps)
+        ref = oracle.Rule(oracle.LINEAR, w.delta, W.dt_dx(w)).run(q0h, w.steps)
+        entry("cfg1", plan, w.n, w.steps, ms, np.array_equal(q.cpu().numpy(), ref), "full state vs oracle")
+        # cfg2: Burgers EO, N = 65536, 20000 steps (resident stepper, K6)
+        w = W.cfg("cfg2")
+        q0h = W.q0_cfg2()
+        qmax = int(np.abs(q0h).max())
+        plan = F.fqnm_plan(w.n, float(w.delta), W.dt_dx_double(w, qmax), F.BURGERS_EO, F.PERIODIC)
+        ms, q = best_ms(plan, torch.tensor(q0h, dtype=torch.int32, device=dev), w.steps)
+        ref = oracle.Rule(oracle.BURGERS_EO, w.delta, W.dt_dx(w, qmax)).run(q0h, w.steps)
+        entry("cfg2", plan, w.n, w.steps, ms, np.array_equal(q.cpu().numpy(), ref), "full state vs oracle")
+        # cfg3: linear kappa = 1/2, N = 2^24, 10^4 steps (K2P)
+        w = W.cfg("cfg3")
+        q0h = W.q0_cfg3()
+        plan = F.fqnm_plan(w.n, float(w.delta), W.dt_dx_double(w), F.LINEAR, F.PERIODIC)
+        ms, q = best_ms(plan, torch.tensor(q0h, dtype=torch.int32, device=dev), w.steps)
+        rule = oracle.Rule(oracle.LINEAR, w.delta, W.dt_dx(w))
+        qh = q.cpu().numpy()
+        ok = windows_ok(lambda x: rule.run(x, w.steps), q0h, qh, w.n, w.steps, True)
+        ok = ok and int(qh.astype(np.int64).sum()) == int(q0h.astype(np.int64).sum())
+        entry("cfg3", plan, w.n, w.steps, ms, ok, "3 light-cone windows of 1024 cells + exact sum", issue4)
+        del q, qh, q0h
+        # ENS-1: 2^16 independent cfg1-like problems (K3)
+        w = W.cfg("ens1")
+        q0h = W.q0_ensemble(w.batch)
+        plan = F.fqnm_plan_ex(w.n, float(w.delta), W.dt_dx_double(w), F.LINEAR, batch=w.batch)
+        ms, q = best_ms(plan, torch.tensor(q0h, dtype=torch.int32, device=dev), w.steps)
+        pick = np.unique(np.concatenate([[0, w.batch - 1], rng.integers(0, w.batch, 14)]))
+        ref = oracle.Rule(oracle.LINEAR, w.delta, W.dt_dx(w)).run(q0h[pick], w.steps)
+        entry("ens1", plan, w.n * w.batch, w.steps, ms, np.array_equal(q[pick].cpu().numpy(), ref),
+              "%d sampled problems vs oracle" % len(pick), issue4)
+        del q, q0h
+        # cfg5: Sod, 3 x int64, N = 2^26, a 300-step window at the configuration's dt/dx
+        w = W.cfg("cfg5")
+        S5 = 300
+        _, lam = W.sod_steps_and_dt_dx(w.n)
+        q0h = W.sod_q0(w.n)
+        plan = F.fqnm_plan(w.n, 1e-7, lam, F.EULER_ROE, F.TRANSMISSIVE)
+        ms, q = best_ms(plan, torch.tensor(q0h, dtype=torch.int64, device=dev), S5)
+        qh = q.cpu().numpy()
+        ok = True
+        for a in (0, w.n - 1024, w.n // 2 - 512, int(rng.integers(0, w.n - 1024))):
+            lo, hi = max(0, a - S5), min(w.n, a + 1024 + S5)
+            ref = oracle.euler_run(np.ascontiguousarray(q0h[:, lo:hi]), S5, 1e-7, lam)
+            ok = ok and np.array_equal(ref[:, a - lo:a - lo + 1024], qh[:, a:a + 1024])
+        micro = _micro_peaks()[0] or {}
+        dfma = micro.get("dfma", {}).get("lane_ops_per_clk_per_sm", 64.0)   # measured DFMA rate
+        entry("cfg5", plan, w.n, S5, ms, ok, "4 light-cone windows (walls, diaphragm, random)",
+              {"bound": "fp64", "fp64_instr_per_cell_update": FP64_PER_CELL_EULER,
+               "peak_gcups": 148 * dfma * sm_ghz / FP64_PER_CELL_EULER})
+    except Exception as ex:                 # never let the side measurements kill the bench line
+        out.append({"error": repr(ex)[:300]})
     return out
 
 
@@ -675,6 +801,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the side measurements of cfg1/2/3/5 and ENS-1 (N = 1)")
     ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"],
                     help="cfg4, N > 1: fused peer-memory halo exchange inside the kernel (p2p) "
                          "or torch.distributed NCCL send/recv between launches")

@@ -1103,7 +1103,12 @@ static int launch_block(fqnm_plan_t* p, const int32_t* src, int32_t* dst, int ks
                          32 * BLOCKED_SIGN_V - a.KL - a.KR >= 4;
     if (sign_ok && (p->sign_hint || p->sign_dev)) {
         BlockedArgs b = a;
-        const int64_t S2 = 32 * BLOCKED_SIGN_V - a.KL - a.KR;
+        // a one-signed state moves one way only: with every q >= 0 the transfer is
+        // F_{j+1/2} = phi+(q_j) and a cell depends on its left neighbour alone (q <= 0: on
+        // its right neighbour), so the window needs no halo on the other side
+        const int sgn = p->sign_hint ? p->sign_hint : 1;
+        if (sgn == 1) b.KR = 0; else b.KL = 0;
+        const int64_t S2 = 32 * BLOCKED_SIGN_V - b.KL - b.KR;
         b.nwin = (d.n_local + S2 - 1) / S2;
         b.sign_bits = p->sign_hint ? nullptr : p->sign_dev;
         PROF_LAUNCH(launch_blocked_sign(p->rule, p->sign_hint ? p->sign_hint : 1, b, p->dr, p->st,
@@ -1152,6 +1157,8 @@ static int step_persist(fqnm_plan_t* p, void* q, int64_t nb, int64_t base, int64
     // K2PS: the sign-specialised persistent kernel when the range check proved the sign
     const int sign = (!p->no_sign && blocked_sign_has_rule(p->rule)) ? p->sign_hint : 0;
     const int Vp = blocked_persist_V(p->rule, sign);
+    if (sign == 1) a.KR = 0;            // one-signed state: one-sided dependence (see launch_block)
+    else if (sign == 2) a.KL = 0;
     a.S = 32 * Vp - a.KL - a.KR;
     if (a.S < 4) return fail(FQNM_ERR_ARG, "k = %d too large for V = %d", kmax, Vp);
     a.nwin = (a.n + a.S - 1) / a.S;
