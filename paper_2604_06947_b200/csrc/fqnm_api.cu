@@ -1132,7 +1132,7 @@ static bool use_persist(fqnm_plan_t* p, int64_t nb)
     const fqnm_plan_desc& d = p->d;
     if (p->persist == 0 || nb < 2) return false;
     if (p->family != 2 || d.batch != 1 || d.boundary == FQNM_HALO || p->V != 32 || p->minb != 2 ||
-        !blocked_persist_has_rule(p->rule) || p->guard)
+        !blocked_persist_has_rule(p->rule))
         return false;
     if (p->persist == 1) return true;
     const int64_t S = 32 * p->V - (p->dep_left ? round4(p->k) : 0) - (p->dep_right ? round4(p->k) : 0);
@@ -1143,7 +1143,10 @@ static bool use_persist(fqnm_plan_t* p, int64_t nb)
     return nwin < 16 * 148 * 16;
 }
 
-static int step_persist(fqnm_plan_t* p, void* q, int64_t nb, int64_t base, int64_t rem)
+// sign: 0 voting kernel, 1 / 2 sign-specialised (K2PS); sign_bits: device sign bits of the
+// input for the dual launch of the pipelined chunks (null: unconditional launch)
+static int step_persist(fqnm_plan_t* p, void* q, int64_t nb, int64_t base, int64_t rem, int sign,
+                        const int* sign_bits)
 {
     const fqnm_plan_desc& d = p->d;
     const int kmax = (int)(base + (rem > 0 ? 1 : 0));
@@ -1154,8 +1157,6 @@ static int step_persist(fqnm_plan_t* p, void* q, int64_t nb, int64_t base, int64
     a.n = d.n_local;
     a.KL = p->dep_left ? round4(kmax) : 0;
     a.KR = p->dep_right ? round4(kmax) : 0;
-    // K2PS: the sign-specialised persistent kernel when the range check proved the sign
-    const int sign = (!p->no_sign && blocked_sign_has_rule(p->rule)) ? p->sign_hint : 0;
     const int Vp = blocked_persist_V(p->rule, sign);
     if (sign == 1) a.KR = 0;            // one-signed state: one-sided dependence (see launch_block)
     else if (sign == 2) a.KL = 0;
@@ -1183,6 +1184,8 @@ static int step_persist(fqnm_plan_t* p, void* q, int64_t nb, int64_t base, int64
     }
     a.flags = p->pflags;
     a.counter = p->pcounter;
+    a.guard = p->guard;
+    a.sign_bits = sign_bits;
     a.tag_base = p->ptag;
     p->ptag += (uint32_t)nb + 1;
     PROF_LAUNCH(launch_blocked_persist(p->rule, sign, a, p->dr, p->st));
@@ -1375,7 +1378,17 @@ extern "C" int fqnm_step(fqnm_plan_t* p, void* q, int64_t nsteps)
         if (nb % 2 == 1 && nsteps >= nb + 1) nb += 1;
         const int64_t base = nsteps / nb, rem = nsteps % nb;
         if (use_persist(p, nb)) {
-            if ((rc = step_persist(p, q, nb, base, rem)) != FQNM_OK) return rc;
+            // K2PS when the range check proved the sign; for a pipelined chunk the sign is
+            // known on the device only: K2PS (q >= 0) and the voting K2P are both launched and
+            // the one the sign bits do not select returns at once
+            const bool sign_rule = !p->no_sign && blocked_sign_has_rule(p->rule);
+            const int sign = sign_rule ? p->sign_hint : 0;
+            if (!sign && sign_rule && p->sign_dev) {
+                if ((rc = step_persist(p, q, nb, base, rem, 1, p->sign_dev)) != FQNM_OK) return rc;
+                if ((rc = step_persist(p, q, nb, base, rem, 0, p->sign_dev)) != FQNM_OK) return rc;
+            } else if ((rc = step_persist(p, q, nb, base, rem, sign, nullptr)) != FQNM_OK) {
+                return rc;
+            }
             cur = (int)(nb & 1);
             if (cur != 0) CUDA_TRY(cudaMemcpyAsync(q, bufs[cur], bytes, cudaMemcpyDeviceToDevice, p->st));
             return FQNM_OK;
@@ -1567,6 +1580,9 @@ extern "C" int fqnm_observe(const fqnm_plan_t* p, const void* q, double* u)
 #ifndef FQNM_PIPE_RAMP
 #define FQNM_PIPE_RAMP 1       // pipelined fqnm_step_host: ramped first/last chunks (C/8 .. C/2)
 #endif
+#ifndef FQNM_PIPE_PERSIST
+#define FQNM_PIPE_PERSIST 1    // pipelined chunks step with K2P / K2PS
+#endif
 #ifndef FQNM_PIPE_DUAL
 #define FQNM_PIPE_DUAL 0       // pipelined chunks: K2S + K2 dual launch on the device sign bits
                                // (measured slower on cfg4 e2e: 3535 vs 3602 GCUPS)
@@ -1626,7 +1642,10 @@ static int pipe_setup(fqnm_plan_t* p, int64_t nsteps)
             return FQNM_ERR_UNSUPPORTED;
         }
         c->st = p->st;
-        c->persist = 0;                  // chunk steps keep the launch-per-block K2
+        // chunks step with the persistent kernels (one launch for all blocks, no launch tails;
+        // K2PS + voting K2P dual launch on the chunk's device sign bits): e2e 3.65 -> see
+        // profiles/r02_tune_k2p.jsonl
+        c->persist = FQNM_PIPE_PERSIST && blocked_persist_has_rule(c->rule) ? 1 : 0;
         p->pipe_kids[i] = c;
         if (i == 0) p->pipe_child = c;
     }
@@ -1734,7 +1753,7 @@ static int step_host_pipelined_impl(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
                                              p->pipe_sign + c, p->st));
             p->launches++;
             ch->guard = p->pipe_guard + c;
-            ch->sign_dev = FQNM_PIPE_DUAL ? p->pipe_sign + c : nullptr;
+            ch->sign_dev = (FQNM_PIPE_DUAL || ch->persist == 1) ? p->pipe_sign + c : nullptr;
             if (!FQNM_PIPE_DUAL && FQNM_PIPE_SIGN && blocked_sign_has_rule(ch->rule)) {
                 // read the chunk's sign bits on the host (measured slower, off by default)
                 CUDA_TRY(cudaMemcpyAsync(p->pipe_sign_host + c, p->pipe_sign + c, sizeof(int),

@@ -191,6 +191,10 @@ struct PersistArgs {
     unsigned int* flags;        // [nwin]: tag_base + (blocks completed) for the window
     unsigned long long* counter;
     uint32_t tag_base;
+    const int* guard;           // the launch returns at once when *guard != 0 (input out of range)
+    const int* sign_bits;       // dual launch (pipelined chunks): bit 0 = the input has a negative
+                                // cell; the sign-specialised kernel runs when clear, the voting
+                                // kernel when set
 };
 cudaError_t launch_blocked_persist(int rule, int sign, const PersistArgs& a, const DevRule& r,
                                    cudaStream_t st);

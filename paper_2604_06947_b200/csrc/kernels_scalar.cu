@@ -737,6 +737,11 @@ static __device__ __noinline__ void persist_slow(const int32_t* src, int32_t* ds
 template <int RULE, int V, int MINB, int FSIGN = 0>
 __global__ void __launch_bounds__(256, MINB) k_blocked_persist(PersistArgs a, DevRule r)
 {
+    if (a.guard && *a.guard) return;                            // input failed its range check
+    if (a.sign_bits) {                                          // dual launch: one of the two runs
+        const bool has_neg = (*a.sign_bits & 1) != 0;
+        if (FSIGN == 1 ? has_neg : !has_neg) return;
+    }
     constexpr int W = 32 * V;
     const int lane = threadIdx.x & 31;
     const int64_t n = a.n, nwin = a.nwin, S = a.S;
