@@ -79,8 +79,17 @@ def test_rule_and_kernel_selection(F):
     assert info["kernel"] == 4
     info = F.fqnm_plan_validate(65536, 1e-5, 4 / 15, F.BURGERS_EO)      # cfg2: resident stepper
     assert info["kernel"] == 6
+    # K6 geometry from the time model: the deepest halo whose warps still fit one per SM
+    # sub-partition (4 x 148): n / (256 - 2k) <= 592 -> k = 72, P = 586
+    assert info["k"] == 72 and info["cells_per_thread"] == 8
+    assert -(-65536 // (256 - 2 * info["k"])) <= 4 * 148
+    info = F.fqnm_plan_validate(150000, 1e-5, 4 / 15, F.BURGERS_EO)     # needs > 592 warps at any k
+    assert info["kernel"] == 6 and 8 <= info["k"] <= 124 and info["k"] % 4 == 0
+    assert -(-150000 // (256 - 2 * info["k"])) <= 8 * 148
     info = F.fqnm_plan_validate(1 << 26, 1e-7, 0.3, F.EULER_ROE, F.TRANSMISSIVE)
     assert info["kernel"] == 5 and info["s_euler"] == 0.3 / 1e-7 and info["g1_euler"] == 1.4 - 1.0
+    assert info["cells_per_thread"] == 2                               # large problems: V = 2
+    assert F.fqnm_plan_validate(4096, 1e-7, 0.3, F.EULER_ROE, F.TRANSMISSIVE)["cells_per_thread"] == 1
 
 
 def test_d8_admissible_range_matches_oracle(F):
