@@ -379,6 +379,29 @@ __device__ __forceinline__ void run_window_steps_signed(int32_t (&q)[V], int kst
         return;
     }
 #endif
+    if (FQNM_SIGN_WINDOWS && RULE == R_TP_FAST) {
+        // Godunov for Burgers, Phi(qL, qR) = g(max(max(qL, 0), -min(qR, 0))) with the EO
+        // magnitude map g (even in q): on a window whose cells are all >= 0 it is g(qL), on
+        // one whose cells are all <= 0 it is g(qR) -- exactly the split EO rule's transfer
+        // there (the collapse of Thm transfer-operator equivalence), so such
+        // windows take the EO sign-uniform step (7 instructions per cell-update instead of
+        // the two-point evaluation).  Godunov is monotone on the D8 range (DESIGN A18), so
+        // the sign holds for the k steps on the dependence cone, as for EO.
+        int32_t lo = q[0], hi = q[0];
+#pragma unroll
+        for (int j = 1; j < V; ++j) { lo = min(lo, q[j]); hi = max(hi, q[j]); }
+        const bool pos = __all_sync(FULL, lo >= 0);
+        if (pos || __all_sync(FULL, hi <= 0)) {
+            if (r.tp_fast == 1) {
+                if (pos) run_window_steps<R_EO_P1, V, false, 1>(q, ksteps, r, 0, 0);
+                else run_window_steps<R_EO_P1, V, false, 2>(q, ksteps, r, 0, 0);
+            } else {
+                if (pos) run_window_steps<R_EO_FAST, V, false, 1>(q, ksteps, r, 0, 0);
+                else run_window_steps<R_EO_FAST, V, false, 2>(q, ksteps, r, 0, 0);
+            }
+            return;
+        }
+    }
     if (FQNM_SIGN_WINDOWS && (RULE == R_EO_P1 || RULE == R_EO_FAST)) {
         int32_t lo = q[0], hi = q[0];
 #pragma unroll

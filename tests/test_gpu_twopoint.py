@@ -158,3 +158,29 @@ def test_equivalence_argument_checks(F):
     pc = _plan(F, oracle.BURGERS_EO, "1e-4", Fraction(1, 3), 1, 100, W.TRANSMISSIVE)
     with pytest.raises(F.FqnmError):
         F.fqnm_equivalence(pa, pc, q, 3)
+
+
+@pytest.mark.parametrize("lam", [Fraction(4, 15), Fraction(3, 10)])          # P = 1 and general P
+@pytest.mark.parametrize("sign", [1, -1, 0])
+@pytest.mark.parametrize("fam,n", [(2, 300_007), (6, 65_536 + 77)])
+def test_godunov_sign_uniform_windows_take_the_eo_step(F, lam, sign, fam, n):
+    """Godunov fast rule (R_TP_FAST) in K2 (V = 32) and K6: windows whose cells are all >= 0
+    or all <= 0 (zeros included) step with the EO sign-uniform form, the rest with the
+    two-point evaluation; bit-exact against the oracle's Godunov rule on positive, negative
+    and patchwise mixed data, both boundaries."""
+    rng = np.random.default_rng(1000 * fam + n + sign)
+    q0 = np.abs(W.smooth_random(rng, n, 100000, 30000)) + 1
+    q0[rng.integers(0, n, 200)] = 0
+    if sign < 0:
+        q0 = -q0
+    elif sign == 0:
+        q0[n // 4: n // 2] *= -1                       # patches of each sign, two sign changes
+        q0[7 * n // 8:] *= -1
+    rule = oracle.TransferRule(oracle.BURGERS_GODUNOV, "1e-5", lam)
+    for boundary in (W.PERIODIC, W.TRANSMISSIVE):
+        plan = _plan(F, oracle.BURGERS_GODUNOV, "1e-5", lam, 1, n, boundary)
+        assert plan.info()["rule"] == 7                 # R_TP_FAST
+        F.fqnm_debug_override(plan, fam)
+        q = torch.tensor(q0, dtype=torch.int32, device=DEV)
+        F.fqnm_step(plan, q, 61)
+        assert np.array_equal(q.cpu().numpy().astype(np.int64), rule.run(q0, 61, boundary)), boundary
