@@ -541,6 +541,17 @@ static int build_rule(fqnm_plan_t* p)
         float cf = (float)target;
         while ((double)cf > target) cf = std::nextafterf(cf, 0.0f);
         r.eo_cf = cf;
+        // float64 form (eo_g_dp): see maps.cuh for the exactness argument
+        const long double inv = ((long double)P / (long double)Q) * (1.0L + std::ldexp(1.0L, -46));
+        r.eo_dinv = (double)inv;
+        r.eo_dc1 = -std::ldexp(r.eo_dinv, 52);
+        r.eo_xoff = (long long)(1023 + 52) << 52;       // bits of 2^52: one ulp is 1
+        const long double qm = (long double)std::max(std::llabs((long long)p->lo), std::llabs((long long)p->hi));
+        r.eo_dp_ok = ((long double)P * qm * qm < std::ldexp(1.0L, 44)) ? 1 : 0;
+        // the P = 1 stepping kernels use the float64 form unconditionally; its condition holds
+        // on the whole fast-path domain (|q| < 2^22), but fall back to the general-P rule
+        // (float32 + integer remainder) should a range ever exceed it
+        if (p->rule == R_EO_P1 && !r.eo_dp_ok) p->rule = R_EO_FAST;
     }
     return FQNM_OK;
 }

@@ -44,6 +44,11 @@ struct DevRule {
     int32_t eo_nQ;        // -Q
     int32_t eo_c6;        // Q * 0x4B400001 - ceil(Q/2)  (mod 2^32)
     int32_t eo_P;         // P
+    // EO magnitude map in float64 (maps.cuh eo_g_dp): g = rint((q^2) * eo_dinv) exactly
+    int32_t eo_dp_ok;     // planner: P q^2 < 2^44 on the admissible range
+    long long eo_xoff;    // bits of 2^52 (ulp 1): X = q*q + eo_xoff is the double 2^52 + q^2
+    double eo_dinv;       // (P/Q)(1 + 2^-46), rounded to double
+    double eo_dc1;        // -2^52 * eo_dinv (exact)
     // two-point rule (R_TWOPOINT): Phi = round(num / tp_den),
     //   Godunov: num = c2 max(max(qL,0)^2, min(qR,0)^2); EO2: c2 (max(qL,0)^2 + min(qR,0)^2);
     //   LF2: c2 (qL^2 + qR^2) + c1 (qL - qR)

@@ -1320,6 +1320,10 @@ __global__ void k_transfer(const int32_t* __restrict__ q, int32_t* __restrict__ 
          i += (int64_t)gridDim.x * blockDim.x) {
         int32_t p, m;
         phi_pm<RULE>(q[i], p, m, r);
+        // the stepping kernels' float64 form of the EO magnitude (eo_g_dp) must agree with
+        // the float32 + integer-remainder form the hook evaluates: a disagreement poisons
+        // the output, so the exhaustive map tests cover both forms
+        if (RULE == R_EO_P1 && r.eo_dp_ok && eo_g_dp(q[i], r) != p + m) p = INT32_MIN;
         pp[i] = p;
         pm[i] = m;
     }

@@ -159,9 +159,35 @@ __device__ __forceinline__ void eo_gm_p1(int32_t q, int32_t& g, int32_t& m, cons
 #ifndef FQNM_EO_SIGN_CONV
 #define FQNM_EO_SIGN_CONV 0    // 0: I2FP for every cell, 1: IMAD + FADD, 2: alternate by cell
 #endif
+// EO magnitude map in float64, 4 instructions with the update (IMAD.WIDE, DFMA, DADD + the
+// step's IADD3) against 7 for the float32-estimate + integer-remainder form.
+//   X  = q*q + bits(2^52)  is the double 2^52 + q^2 exactly (ulp(2^52) = 1, q^2 < 2^44: one IMAD.WIDE makes
+//        the product and the int64 -> double conversion);
+//   t1 = fma(X, dinv, -2^52 dinv) = fl(q^2 dinv): the FMA forms X dinv - 2^52 dinv = q^2 dinv
+//        exactly and rounds once, so t1 = v (1 + b), v = P q^2 / Q, 2^-47 < b < 2^-45
+//        (dinv = (P/Q)(1 + 2^-46) up to 2^-52, the rounding 2^-53);
+//   g  = low word of bits(t1 + 1.5 2^52) = rint(t1).
+// rint(t1) = RHA(v) = floor(v + 1/2): a tie v = k + 1/2 is pushed up by v b >= 16 ulp(v), so it
+// rounds to k + 1; any other v is at least 1/(2Q) from a half-integer and v b < 2^-45 v <
+// 1/(2Q) because v Q = P q^2 < 2^44 (eo_dp_ok, checked by the planner on the admissible
+// range), so t1 stays on v's side of every boundary and is never a half-integer itself.
+#ifndef FQNM_EO_DP
+#define FQNM_EO_DP 1           // sign-uniform EO step (P = 1): 1 = the float64 form (cfg4 4.18 -> 4.5 TCUPS)
+#endif
+__device__ __forceinline__ int32_t eo_g_dp(int32_t q, const DevRule& r)
+{
+    const long long X = (long long)q * (long long)q + r.eo_xoff;
+    const double t1 = __fma_rn(__longlong_as_double(X), r.eo_dinv, r.eo_dc1);
+    return __double2loint(__dadd_rn(t1, 6755399441055744.0));
+}
+
 template <int RULE, bool ALT>
 __device__ __forceinline__ int32_t eo_g_biased(int32_t q, const DevRule& r)
 {
+#if FQNM_EO_DP
+    // P = 1: P q^2 < 2^44 holds on the whole fast-path domain |q| < 2^22 (eo_dp_ok); g unbiased
+    if (RULE == R_EO_P1) return eo_g_dp(q, r);
+#endif
     if (RULE == R_EO_P1) {
         constexpr bool fma_conv = FQNM_EO_SIGN_CONV == 1 || (FQNM_EO_SIGN_CONV == 2 && ALT);
         float qf;

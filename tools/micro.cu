@@ -69,6 +69,32 @@ CHAIN_KERNEL(k_i2fp, int32_t, (int32_t)(threadIdx.x + c),
 CHAIN_KERNEL(k_lea_hi, int32_t, (int32_t)(threadIdx.x + c),
              { int32_t t = x[c] >> 31; asm volatile("add.s32 %0, %0, %1;" : "+r"(x[c]) : "r"(t)); x[c] ^= a; })
 
+CHAIN_KERNEL(k_dadd, double, (double)(threadIdx.x + c),
+             asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(x[c]) : "d"(a)))
+CHAIN_KERNEL(k_imad_wide, long long, (long long)(threadIdx.x + c),
+             { int lo = (int)x[c]; asm volatile("mad.wide.s32 %0, %1, %1, %2;" : "=l"(x[c]) : "r"(lo), "l"((long long)b)); })
+
+// ---- DFMA + DADD alternating (independent chains): the float64 half of the EO map ----
+__global__ void __launch_bounds__(512, 2) k_dfma_dadd(double* out, Span* sp, double a, double b)
+{
+    unsigned long long t0; __syncthreads(); span_begin(t0);
+    double x[CH], y[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) { x[c] = threadIdx.x + c; y[c] = threadIdx.x - c; }
+    for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(x[c]) : "d"(a), "d"(b));
+            asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(y[c]) : "d"(b));
+        }
+    }
+    double s = 0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) s += x[c] + y[c];
+    if (s == 123456789.0) out[threadIdx.x] = s;
+    span_end(sp, t0);
+}
+
 // ---- mixed streams: ALU + FMA-pipe interleaved 1:1 (independent chains) ----
 __global__ void __launch_bounds__(512, 2) k_mixed_alu_fma(int32_t* out, Span* sp, int32_t a, int32_t b)
 {
@@ -129,6 +155,63 @@ __global__ void __launch_bounds__(256, 2) k_eo_sign_step(int32_t* out, Span* sp,
         }
         q[SV - 1] = q[SV - 1] + gp - glast;
         if (lane == 0) q[0] = 100000;        // keep the window's data positive and bounded
+    }
+    int32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < SV; ++j) acc ^= q[j];
+    if (acc == 123456789) out[threadIdx.x] = acc;
+    span_end(sp, t0);
+}
+
+// ---- the K2 sign-uniform step with the float64 map (IMAD.WIDE, DFMA, DADD, IADD3) ----
+__global__ void __launch_bounds__(256, 2) k_eo_dp_step(int32_t* out, Span* sp, DevRule r, int32_t seed)
+{
+    unsigned long long t0; __syncthreads(); span_begin(t0);
+    const int lane = threadIdx.x & 31;
+    int32_t q[SV];
+#pragma unroll
+    for (int j = 0; j < SV; ++j) q[j] = 100000 + ((seed + 37 * j + 11 * (int)threadIdx.x) & 4095);
+    const EoDp c = eo_dp_consts(r);
+    for (int s = 0; s < SSTEPS; ++s) {
+        const int32_t glast = eo_g_dp(q[SV - 1], c);
+        int32_t gp = __shfl_up_sync(0xffffffffu, glast, 1);
+#pragma unroll
+        for (int j = 0; j + 1 < SV; ++j) {
+            const int32_t gj = eo_g_dp(q[j], c);
+            q[j] = q[j] + gp - gj;
+            gp = gj;
+        }
+        q[SV - 1] = q[SV - 1] + gp - glast;
+        if (lane == 0) q[0] = 100000;
+    }
+    int32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < SV; ++j) acc ^= q[j];
+    if (acc == 123456789) out[threadIdx.x] = acc;
+    span_end(sp, t0);
+}
+
+// ---- mixed: one cell in MIX takes the float32 + integer form, the rest the float64 form ----
+template <int MIX>
+__global__ void __launch_bounds__(256, 2) k_eo_mix_step(int32_t* out, Span* sp, DevRule r, int32_t seed)
+{
+    unsigned long long t0; __syncthreads(); span_begin(t0);
+    const int lane = threadIdx.x & 31;
+    int32_t q[SV];
+#pragma unroll
+    for (int j = 0; j < SV; ++j) q[j] = 100000 + ((seed + 37 * j + 11 * (int)threadIdx.x) & 4095);
+    const EoDp c = eo_dp_consts(r, 0x4B400000u);
+    for (int s = 0; s < SSTEPS; ++s) {
+        const int32_t glast = eo_g_dp(q[SV - 1], c);
+        int32_t gp = __shfl_up_sync(0xffffffffu, glast, 1);
+#pragma unroll
+        for (int j = 0; j + 1 < SV; ++j) {
+            const int32_t gj = (j % MIX) == 0 ? eo_g_biased_f32<R_EO_P1>(q[j], r) : eo_g_dp(q[j], c);
+            q[j] = q[j] + gp - gj;
+            gp = gj;
+        }
+        q[SV - 1] = q[SV - 1] + gp - glast;
+        if (lane == 0) q[0] = 100000;
     }
     int32_t acc = 0;
 #pragma unroll
@@ -256,6 +339,9 @@ int main(int argc, char** argv)
     measure("imad_hi", "IMAD.HI", 2, 512, n1, L1(k_imad_hi, int32_t, a, b));
     measure("ffma", "FFMA", 2, 512, n1, L1(k_ffma, float, 1.0001f, 0.5f));
     measure("dfma", "DFMA", 2, 512, n1, L1(k_dfma, double, 1.0000001, 0.5));
+    measure("dadd", "DADD", 2, 512, n1, L1(k_dadd, double, 1.5, 0.5));
+    measure("dfma_dadd", "DFMA + DADD interleaved (per op)", 2, 512, 2 * n1, L1(k_dfma_dadd, double, 1.0000001, 0.5));
+    measure("imad_wide", "IMAD.WIDE", 2, 512, n1, L1(k_imad_wide, long long, 3, 5));
     measure("i2fp_shf", "I2FP + SHF pairs (per op)", 2, 512, 2 * n1, L1(k_i2fp, int32_t, 0, 0));
     measure("lea_hi", "LEA.HI + LOP3 pairs (per op)", 2, 512, 2 * n1, L1(k_lea_hi, int32_t, a, b));
     measure("mixed_alu_fma_int", "LOP3 + IMAD interleaved", 2, 512, 2 * n1, L1(k_mixed_alu_fma, int32_t, a, b));
@@ -270,6 +356,19 @@ int main(int argc, char** argv)
     // 7 instructions per cell-update (I2FP, FMUL, FFMA, 2 IMAD, LEA.HI, IADD3)
     measure("eo_sign_step", "K2 sign-uniform step, 7 instr/cell", 2, 256, 7.0 * SSTEPS * SV,
             [&](int g, int t) { k_eo_sign_step<<<g, t>>>((int32_t*)out, sp, r, 17); });
+    {
+        const long double inv = (1.0L / (long double)Q) * (1.0L + ldexpl(1.0L, -46));
+        r.eo_dinv = (double)inv;
+        r.eo_dc1 = -ldexp(r.eo_dinv, 52);
+        r.eo_xoff = (long long)(1023 + 52) << 52;
+    }
+    // 4 instructions per cell-update (IMAD.WIDE, DFMA, DADD, IADD3)
+    measure("eo_dp_step", "K2 sign-uniform step, float64 map, 4 instr/cell", 2, 256, 4.0 * SSTEPS * SV,
+            [&](int g, int t) { k_eo_dp_step<<<g, t>>>((int32_t*)out, sp, r, 17); });
+    // mixes, reported as cells x 4 (comparable with eo_dp_step)
+#define MIXV(M, NAME) measure(NAME, "float64 map with one float32-form cell in M (cells x 4)", 2, 256, \
+        4.0 * SSTEPS * SV, [&](int g, int t) { k_eo_mix_step<M><<<g, t>>>((int32_t*)out, sp, r, 17); })
+    MIXV(2, "eo_mix2"); MIXV(3, "eo_mix3"); MIXV(4, "eo_mix4"); MIXV(6, "eo_mix6"); MIXV(8, "eo_mix8");
     // EO variants: reported as lane-ops at 7 per cell, i.e. cells/clk x 7 (comparable)
 #define EOV(C, O, M, NAME) measure(NAME, "EO sign-step variant (7-op-equivalent cells)", M, 256, \
         7.0 * SSTEPS * SV, [&](int g, int t) { k_eo_var<C, O, M><<<g, t>>>((int32_t*)out, sp, r, 17); })
