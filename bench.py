@@ -52,6 +52,15 @@ UNIT = "GCUPS"
 # Linear kappa = 1/2: 4.  SURVEY §8(d)-D3's a-priori 16 over-counts these closed forms.
 OPS_ALG = {"burgers_eo": 10, "burgers_eo_general_p": 11, "burgers_eo_sign_uniform": 7,
            "burgers_eo_sign_uniform_general_p": 8, "linear": 4}
+# The sign-uniform P = 1 step in float64 (maps.cuh eo_g_dp; K2S / K2PS and the sign-uniform
+# windows of K2 / K2P): IMAD.WIDE, DFMA, DADD + the IADD3 update = 4 instructions per
+# cell-update, of which the first three issue on the FP64 pipe (64 lanes/clk/SM: micro dadd,
+# dfma_dadd, imad_wide; the step's own ceiling is that pipe).  The binding resource is that
+# pipe -- 128/4 = 32 cell-updates/clk/SM of issue against 64/3 = 21.3 of the pipe -- so the
+# roofline counts the 3 pipe operations against 148 x 64 lanes x f.
+EO_DP_PIPE_OPS = 3
+EO_DP_INSTR = 4
+FP64_PIPE_LANES = 64
 RULE_NAMES = {1: "LIN_HALF", 2: "EO_FAST", 3: "GENERIC", 4: "LIN_FAST", 5: "EO_P1"}
 SM_COUNT = 148
 LANES_PER_SM_CLK = 128                          # 4 SMSPs x 32 lanes, 1 warp-instr/clk each
@@ -302,17 +311,22 @@ def timed(do_step, args, world, local, plan, stepper_plans):
 
 
 def alu_roofline(kernel: str, ops_alg: int, updates_per_launch: float, per_launch_ms: float,
-                 hbm_bytes_per_launch: float, extra: dict, mix_ceiling_key: str = ""):
+                 hbm_bytes_per_launch: float, extra: dict, mix_ceiling_key: str = "",
+                 pipe_lanes: int = 0, pipe_name: str = ""):
+    """ops_alg operations per cell-update against 148 SMs x lanes/clk x f: the whole SM's
+    instruction issue (128 lanes) by default, or the one pipe that binds (pipe_lanes)."""
     peaks, peak_src = _peaks()
     f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
-    peak_ops = SM_COUNT * LANES_PER_SM_CLK * f_max                    # int lane-ops/s at max clock
+    lanes = pipe_lanes if pipe_lanes else LANES_PER_SM_CLK
+    peak_ops = SM_COUNT * lanes * f_max                               # lane-ops/s at max clock
     achieved_ops = ops_alg * updates_per_launch / (per_launch_ms / 1e3)
     roof = {
         "bound": "alu", "kernel": kernel,
         "achieved": achieved_ops / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s",
         "frac": achieved_ops / peak_ops,
         "ops_alg_per_cell_update": ops_alg,
-        "peak_basis": "148 SMs x 128 int lanes/clk x sm_max_mhz (%s)" % peak_src,
+        "peak_basis": ("148 SMs x %d lanes/clk (%s) x sm_max_mhz (%s)" % (
+            lanes, pipe_name if pipe_lanes else "instruction issue: 4 schedulers x 32", peak_src)),
         "traffic": None, "traffic_source": None,
         "algorithmic_bytes_per_launch": hbm_bytes_per_launch,
         "kernel_ms_per_launch": per_launch_ms,
@@ -324,7 +338,7 @@ def alu_roofline(kernel: str, ops_alg: int, updates_per_launch: float, per_launc
     if micro:
         # the same achieved rate against the issue rate measured on a B200 by
         # microbenchmarks (the mixed ALU + FMA integer stream, scaled to sm_max_mhz)
-        m = micro.get("mixed_alu_fma_int", {})
+        m = micro.get("dfma_dadd" if pipe_lanes else "mixed_alu_fma_int", {})
         if m.get("lane_ops_per_clk_per_sm"):
             mp = m["lane_ops_per_clk_per_sm"] * SM_COUNT * f_max
             roof["measured_issue_peak"] = mp / 1e12
@@ -332,13 +346,16 @@ def alu_roofline(kernel: str, ops_alg: int, updates_per_launch: float, per_launc
             roof["measured_peak_source"] = src
         # and against the compute-only ceiling of the kernel's own instruction mix: the
         # sign-uniform EO step on register data (no loads/stores), same occupancy
-        e = micro.get("eo_sign_step", {})
-        if mix_ceiling_key == "eo_sign_step" and e.get("lane_ops_per_clk_per_sm"):
-            ceil_ops = e["lane_ops_per_clk_per_sm"] * SM_COUNT * f_max
-            roof["mix_ceiling"] = {"what": "K2 sign-uniform step on register data, 7 instr/cell "
-                                           "(tools/micro.cu k_eo_sign_step)",
-                                   "achieved_frac": achieved_ops / ceil_ops,
-                                   "ceiling_ops": ceil_ops / 1e12}
+        e = micro.get(mix_ceiling_key, {}) if mix_ceiling_key else {}
+        if e.get("lane_ops_per_clk_per_sm"):
+            # micro reports instructions; convert to cell-updates with its instructions per cell
+            per_cell = {"eo_sign_step": 7.0, "eo_dp_step": 4.0}[mix_ceiling_key]
+            ceil_cups = e["lane_ops_per_clk_per_sm"] / per_cell * SM_COUNT * f_max
+            cups = updates_per_launch / (per_launch_ms / 1e3)
+            roof["mix_ceiling"] = {"what": "the kernel's own step on register data, no loads/stores "
+                                           "(tools/micro.cu k_%s, %g instr/cell)" % (mix_ceiling_key, per_cell),
+                                   "achieved_frac": cups / ceil_cups,
+                                   "ceiling_tcups": ceil_cups / 1e12}
     return roof
 
 
@@ -433,13 +450,25 @@ def run_cfg4(args):
     k2s = plan.info()["k2s_launches"] > 0
     Vk = 48 if k2s else info["cells_per_thread"]
     kname = "k_blocked<%s,V=%d%s>" % (RULE_NAMES.get(info["rule"], "?"), Vk, ",sign" if k2s else "")
+    # P = 1 sign-uniform state: the float64 step, bound by the FP64 pipe
+    dp = uniform and info["rule"] == 5
+    if dp:
+        ops_key = "burgers_eo_sign_uniform_f64"
     roofline = alu_roofline(
-        kname, ops_alg, updates_per_launch, per_launch_ms, hbm_bytes_per_launch,
+        kname, EO_DP_PIPE_OPS if dp else ops_alg, updates_per_launch, per_launch_ms, hbm_bytes_per_launch,
         {"kernel_launches": kern_launches, "kernel_share_of_step": kern_ms / ms if ms > 0 else None,
          "k": info["k"], "V": Vk, "ops_basis": ops_key,
+         "instructions_per_cell_update": EO_DP_INSTR if dp else ops_alg,
          # K2S windows carry a halo on one side only (a one-signed state moves one way)
          "windows_redundancy": 32.0 * Vk / (32.0 * Vk - (1 if k2s else 2) * ((info["k"] + 3) // 4 * 4))},
-        mix_ceiling_key="eo_sign_step" if ops_key == "burgers_eo_sign_uniform" else "")
+        mix_ceiling_key="eo_dp_step" if dp else ("eo_sign_step" if ops_key == "burgers_eo_sign_uniform" else ""),
+        pipe_lanes=FP64_PIPE_LANES if dp else 0,
+        pipe_name="FP64 pipe: IMAD.WIDE, DFMA, DADD" if dp else "")
+    if dp:
+        # the same rate against whole-SM instruction issue (4 instructions, 128 lanes/clk)
+        cups = updates_per_launch / (per_launch_ms / 1e3)
+        roofline["frac_of_issue_bound"] = cups * EO_DP_INSTR / (
+            SM_COUNT * LANES_PER_SM_CLK * float(_peaks()[0].get("sm_max_mhz", 1965.0)) * 1e6)
     tr, tr_src = ncu_traffic(n_local)
     if tr is not None:
         roofline["traffic"] = tr

@@ -101,16 +101,21 @@ __device__ __forceinline__ void eval_maps(const int32_t (&q)[V], int32_t (&g)[V]
 #ifndef FQNM_SIGN_STREAM
 #define FQNM_SIGN_STREAM 1     // sign-uniform step: maps evaluated cell by cell (no map array)
 #endif
-template <int RULE, int V, bool WALL, int NB, int SIGN = 0>
+// SIGN_ = SIGN + 2 (3, 4): the same sign-uniform steps with the float32 form of the EO
+// magnitude (K6: a lone warp per sub-partition is latency-bound, and the float64 form's
+// longer latency costs it 5 %)
+template <int RULE, int V, bool WALL, int NB, int SIGN_ = 0>
 __device__ __forceinline__ void one_step(int32_t (&q)[V], const DevRule& r, int lane, int64_t g0,
                                          int64_t n)
 {
+    constexpr int SIGN = SIGN_ > 2 ? SIGN_ - 2 : SIGN_;
+    constexpr bool F32 = SIGN_ > 2;
     if (FQNM_SIGN_STREAM && SIGN != 0 && !WALL && (RULE == R_EO_P1 || RULE == R_EO_FAST)) {
         // streamed: the lane-edge map first (for the shuffle), then each cell's map right
         // before its update, so the ALU-pipe updates interleave with the map evaluation
         // and no array of maps is live
         if (SIGN == 1) {                   // q_j += g_{j-1} - g_j
-            const int32_t glast = eo_g_biased<RULE, true>(q[V - 1], r);
+            const int32_t glast = eo_g_sel<RULE, true, F32>(q[V - 1], r);
             int32_t gp = NB == 0 ? __shfl_up_sync(FULL, glast, 1)
                                  : __shfl_sync(FULL, glast, (lane + 31) & 31);
 #if FQNM_EO_SIGN_CONV != 2 && FQNM_EO_SIGN_LEA != 2
@@ -118,17 +123,17 @@ __device__ __forceinline__ void one_step(int32_t (&q)[V], const DevRule& r, int 
             // for the paired loop below, which alternating variants need)
 #pragma unroll
             for (int j = 0; j + 1 < V; ++j) {
-                const int32_t gj = eo_g_biased<RULE, false>(q[j], r);
+                const int32_t gj = eo_g_sel<RULE, false, F32>(q[j], r);
                 q[j] = q[j] + gp - gj;
                 gp = gj;
             }
 #else
 #pragma unroll
             for (int j = 0; j + 1 < V; j += 2) {         // V even: j + 1 <= V - 2 here
-                const int32_t g0 = eo_g_biased<RULE, false>(q[j], r);
+                const int32_t g0 = eo_g_sel<RULE, false, F32>(q[j], r);
                 q[j] = q[j] + gp - g0;
                 if (j + 2 < V) {
-                    const int32_t g1 = eo_g_biased<RULE, true>(q[j + 1], r);
+                    const int32_t g1 = eo_g_sel<RULE, true, F32>(q[j + 1], r);
                     q[j + 1] = q[j + 1] + g0 - g1;
                     gp = g1;
                 } else {
@@ -138,17 +143,17 @@ __device__ __forceinline__ void one_step(int32_t (&q)[V], const DevRule& r, int 
 #endif
             q[V - 1] = q[V - 1] + gp - glast;
         } else {                           // q_j += g_j - g_{j+1}
-            const int32_t g0 = eo_g_biased<RULE, false>(q[0], r);
+            const int32_t g0 = eo_g_sel<RULE, false, F32>(q[0], r);
             const int32_t gr = NB == 0 ? __shfl_down_sync(FULL, g0, 1)
                                        : __shfl_sync(FULL, g0, (lane + 1) & 31);
             int32_t gc = g0;
 #pragma unroll
             for (int j = 0; j + 1 < V; j += 2) {
-                const int32_t g1 = eo_g_biased<RULE, true>(q[j + 1], r);
+                const int32_t g1 = eo_g_sel<RULE, true, F32>(q[j + 1], r);
                 q[j] = q[j] + gc - g1;
                 gc = g1;
                 if (j + 2 < V) {
-                    const int32_t g2 = eo_g_biased<RULE, false>(q[j + 2], r);
+                    const int32_t g2 = eo_g_sel<RULE, false, F32>(q[j + 2], r);
                     q[j + 1] = q[j + 1] + gc - g2;
                     gc = g2;
                 }
@@ -159,8 +164,8 @@ __device__ __forceinline__ void one_step(int32_t (&q)[V], const DevRule& r, int 
         int32_t g[V];
 #pragma unroll
         for (int j = 0; j < V; j += 2) {
-            g[j] = eo_g_biased<RULE, false>(q[j], r);
-            if (j + 1 < V) g[j + 1] = eo_g_biased<RULE, true>(q[j + 1], r);
+            g[j] = eo_g_sel<RULE, false, F32>(q[j], r);
+            if (j + 1 < V) g[j + 1] = eo_g_sel<RULE, true, F32>(q[j + 1], r);
         }
         if (SIGN == 1) {                   // q_j += g_{j-1} - g_j
             const int32_t gl = NB == 0 ? __shfl_up_sync(FULL, g[V - 1], 1)
@@ -368,7 +373,7 @@ __device__ __forceinline__ void run_window_steps(int32_t (&q)[V], int ksteps, co
 // k steps of a window without walls (neighbours by shfl, edges cut off by the caller).
 // EO rules: one warp vote per window on the sign of its cells picks the sign-uniform
 // step (one_step SIGN) where it applies
-template <int RULE, int V>
+template <int RULE, int V, bool F32 = false>
 __device__ __forceinline__ void run_window_steps_signed(int32_t (&q)[V], int ksteps,
                                                         const DevRule& r)
 {
@@ -406,8 +411,8 @@ __device__ __forceinline__ void run_window_steps_signed(int32_t (&q)[V], int kst
         int32_t lo = q[0], hi = q[0];
 #pragma unroll
         for (int j = 1; j < V; ++j) { lo = min(lo, q[j]); hi = max(hi, q[j]); }
-        if (__all_sync(FULL, lo >= 0)) { run_window_steps<RULE, V, false, 1>(q, ksteps, r, 0, 0); return; }
-        if (__all_sync(FULL, hi <= 0)) { run_window_steps<RULE, V, false, 2>(q, ksteps, r, 0, 0); return; }
+        if (__all_sync(FULL, lo >= 0)) { run_window_steps<RULE, V, false, F32 ? 3 : 1>(q, ksteps, r, 0, 0); return; }
+        if (__all_sync(FULL, hi <= 0)) { run_window_steps<RULE, V, false, F32 ? 4 : 2>(q, ksteps, r, 0, 0); return; }
     }
     run_window_steps<RULE, V, false>(q, ksteps, r, 0, 0);
 }
@@ -955,7 +960,7 @@ __global__ void __launch_bounds__(256, k6_minb<RULE>()) k_resident(ResidentArgs 
         if (wall)
             run_window_steps<RULE, V, true>(q, kb, r, ws + (int64_t)lane * V, a.n);
         else
-            run_window_steps_signed<RULE, V>(q, kb, r);
+            run_window_steps_signed<RULE, V, true>(q, kb, r);
         done += kb;
         if (done >= a.nsteps) break;
         ++blk;

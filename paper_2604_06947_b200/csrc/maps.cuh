@@ -182,12 +182,20 @@ __device__ __forceinline__ int32_t eo_g_dp(int32_t q, const DevRule& r)
 }
 
 template <int RULE, bool ALT>
+__device__ __forceinline__ int32_t eo_g_biased(int32_t q, const DevRule& r);
+// the EO magnitude of the sign-uniform steps: the float64 form for P = 1 (P q^2 < 2^44 holds
+// on the whole fast-path domain |q| < 2^22, eo_dp_ok; g unbiased) unless F32 asks for the
+// float32 + integer-remainder form (g biased for P = 1; a step uses one form throughout)
+template <int RULE, bool ALT, bool F32>
+__device__ __forceinline__ int32_t eo_g_sel(int32_t q, const DevRule& r)
+{
+    if (FQNM_EO_DP && !F32 && RULE == R_EO_P1) return eo_g_dp(q, r);
+    return eo_g_biased<RULE, ALT>(q, r);
+}
+
+template <int RULE, bool ALT>
 __device__ __forceinline__ int32_t eo_g_biased(int32_t q, const DevRule& r)
 {
-#if FQNM_EO_DP
-    // P = 1: P q^2 < 2^44 holds on the whole fast-path domain |q| < 2^22 (eo_dp_ok); g unbiased
-    if (RULE == R_EO_P1) return eo_g_dp(q, r);
-#endif
     if (RULE == R_EO_P1) {
         constexpr bool fma_conv = FQNM_EO_SIGN_CONV == 1 || (FQNM_EO_SIGN_CONV == 2 && ALT);
         float qf;
