@@ -54,13 +54,14 @@ OPS_ALG = {"burgers_eo": 10, "burgers_eo_general_p": 11, "burgers_eo_sign_unifor
            "burgers_eo_sign_uniform_general_p": 8, "linear": 4}
 # The sign-uniform P = 1 step in float64 (maps.cuh eo_g_dp; K2S / K2PS and the sign-uniform
 # windows of K2 / K2P): IMAD.WIDE, DFMA, DADD + the IADD3 update = 4 instructions per
-# cell-update, of which the first three issue on the FP64 pipe (64 lanes/clk/SM: micro dadd,
-# dfma_dadd, imad_wide; the step's own ceiling is that pipe).  The binding resource is that
-# pipe -- 128/4 = 32 cell-updates/clk/SM of issue against 64/3 = 21.3 of the pipe -- so the
-# roofline counts the 3 pipe operations against 148 x 64 lanes x f.
-EO_DP_PIPE_OPS = 3
+# cell-update.  Two bounds coincide: instruction issue (128 lanes / 4) and the FP64 pipe
+# (64 lanes / 2 for DFMA + DADD) both allow 32 cell-updates/clk/SM = 9.3 TCUPS at 1.965 GHz.
+# The microbenchmarks (profiles/r02_micro.json) show the four instruction classes as
+# independent streams reach 0.94 of issue (grp_dfma_dadd_imadwide_iadd), but the step's own
+# dataflow (IMAD.WIDE -> DFMA -> DADD -> IADD3) tops out at 19.0 cell-updates/clk/SM
+# (eo_dp_step: 0.59 of issue; ncu: dispatch stalls on the FP64 instructions), which is what
+# `mix_ceiling` reports.
 EO_DP_INSTR = 4
-FP64_PIPE_LANES = 64
 RULE_NAMES = {1: "LIN_HALF", 2: "EO_FAST", 3: "GENERIC", 4: "LIN_FAST", 5: "EO_P1"}
 SM_COUNT = 148
 LANES_PER_SM_CLK = 128                          # 4 SMSPs x 32 lanes, 1 warp-instr/clk each
@@ -455,20 +456,19 @@ def run_cfg4(args):
     if dp:
         ops_key = "burgers_eo_sign_uniform_f64"
     roofline = alu_roofline(
-        kname, EO_DP_PIPE_OPS if dp else ops_alg, updates_per_launch, per_launch_ms, hbm_bytes_per_launch,
+        kname, EO_DP_INSTR if dp else ops_alg, updates_per_launch, per_launch_ms, hbm_bytes_per_launch,
         {"kernel_launches": kern_launches, "kernel_share_of_step": kern_ms / ms if ms > 0 else None,
          "k": info["k"], "V": Vk, "ops_basis": ops_key,
          "instructions_per_cell_update": EO_DP_INSTR if dp else ops_alg,
          # K2S windows carry a halo on one side only (a one-signed state moves one way)
          "windows_redundancy": 32.0 * Vk / (32.0 * Vk - (1 if k2s else 2) * ((info["k"] + 3) // 4 * 4))},
-        mix_ceiling_key="eo_dp_step" if dp else ("eo_sign_step" if ops_key == "burgers_eo_sign_uniform" else ""),
-        pipe_lanes=FP64_PIPE_LANES if dp else 0,
-        pipe_name="FP64 pipe: IMAD.WIDE, DFMA, DADD" if dp else "")
-    if dp:
-        # the same rate against whole-SM instruction issue (4 instructions, 128 lanes/clk)
-        cups = updates_per_launch / (per_launch_ms / 1e3)
-        roofline["frac_of_issue_bound"] = cups * EO_DP_INSTR / (
-            SM_COUNT * LANES_PER_SM_CLK * float(_peaks()[0].get("sm_max_mhz", 1965.0)) * 1e6)
+        mix_ceiling_key="eo_dp_step" if dp else ("eo_sign_step" if ops_key == "burgers_eo_sign_uniform" else ""))
+    # the same rate on the bases used before: the float32 form's 7 operations (the kernel of
+    # the earlier bench lines) and SURVEY 8(d)-D3's a-priori 16 operations per EO cell-update
+    cups = updates_per_launch / (per_launch_ms / 1e3)
+    issue = SM_COUNT * LANES_PER_SM_CLK * float(_peaks()[0].get("sm_max_mhz", 1965.0)) * 1e6
+    roofline["frac_on_7op_float32_form_basis"] = cups * 7 / issue
+    roofline["frac_on_survey_16op_basis"] = cups * 16 / issue
     tr, tr_src = ncu_traffic(n_local)
     if tr is not None:
         roofline["traffic"] = tr

@@ -95,6 +95,104 @@ __global__ void __launch_bounds__(512, 2) k_dfma_dadd(double* out, Span* sp, dou
     span_end(sp, t0);
 }
 
+// ---- IMAD.WIDE + DFMA alternating (independent chains): do they share a pipe? ----
+__global__ void __launch_bounds__(512, 2) k_imadwide_dfma(double* out, Span* sp, double a, double b)
+{
+    unsigned long long t0; __syncthreads(); span_begin(t0);
+    double x[CH]; long long y[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) { x[c] = threadIdx.x + c; y[c] = threadIdx.x - c; }
+    for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(x[c]) : "d"(a), "d"(b));
+            { int lo = (int)y[c]; asm volatile("mad.wide.s32 %0, %1, %1, %2;" : "=l"(y[c]) : "r"(lo), "l"(5ll)); }
+        }
+    }
+    double s = 0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) s += x[c] + (double)y[c];
+    if (s == 123456789.0) out[threadIdx.x] = s;
+    span_end(sp, t0);
+}
+
+// ---- IMAD.WIDE + IMAD alternating ----
+__global__ void __launch_bounds__(512, 2) k_imadwide_imad(int32_t* out, Span* sp, int32_t a, int32_t b)
+{
+    unsigned long long t0; __syncthreads(); span_begin(t0);
+    int32_t x[CH]; long long y[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) { x[c] = threadIdx.x + c; y[c] = threadIdx.x - c; }
+    for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            asm volatile("mad.lo.s32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(a), "r"(b));
+            { int lo = (int)y[c]; asm volatile("mad.wide.s32 %0, %1, %1, %2;" : "=l"(y[c]) : "r"(lo), "l"(5ll)); }
+        }
+    }
+    long long s = 0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) s += x[c] + y[c];
+    if (s == 123456789) out[threadIdx.x] = (int32_t)s;
+    span_end(sp, t0);
+}
+
+// ---- groups of independent instructions: MASK bit 0 DFMA, 1 DADD, 2 IMAD.WIDE, 3 IADD3, 4 IMAD ----
+template <int MASK>
+__global__ void __launch_bounds__(512, 2) k_group(double* out, Span* sp, double a, double b)
+{
+    unsigned long long t0; __syncthreads(); span_begin(t0);
+    double x[CH], z[CH]; long long y[CH]; int w[CH], v[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) { x[c] = threadIdx.x + c; z[c] = threadIdx.x * 3 + c; y[c] = threadIdx.x - c; w[c] = c; v[c] = c + 1; }
+    const int ia = (int)a + 3, ib = (int)b + 5;
+    for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            if (MASK & 1) asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(x[c]) : "d"(a), "d"(b));
+            if (MASK & 2) asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(z[c]) : "d"(b));
+            if (MASK & 4) { int lo = (int)y[c]; asm volatile("mad.wide.s32 %0, %1, %1, %2;" : "=l"(y[c]) : "r"(lo), "l"(5ll)); }
+            if (MASK & 8) asm volatile("add.s32 %0, %0, %1;" : "+r"(w[c]) : "r"(ia));
+            if (MASK & 16) asm volatile("mad.lo.s32 %0, %0, %1, %2;" : "+r"(v[c]) : "r"(ia), "r"(ib));
+        }
+    }
+    double s = 0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) s += x[c] + z[c] + (double)y[c] + w[c] + v[c];
+    if (s == 123456789.0) out[threadIdx.x] = s;
+    span_end(sp, t0);
+}
+
+// ---- the four instructions of the float64 step with selectable dependences between them:
+// MODE bit 0: DFMA reads the IMAD.WIDE result, bit 1: DADD reads the DFMA result,
+// bit 2: IADD reads the low word of the DADD result (else each type has its own chain) ----
+template <int MODE>
+__global__ void __launch_bounds__(512, 2) k_dep(double* out, Span* sp, double a, double b)
+{
+    unsigned long long t0; __syncthreads(); span_begin(t0);
+    double x[CH], z[CH]; long long y[CH]; int w[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) { x[c] = threadIdx.x + c; z[c] = threadIdx.x * 3 + c; y[c] = threadIdx.x - c; w[c] = c + threadIdx.x; }
+    const int ia = (int)a + 3;
+    for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            asm volatile("mad.wide.s32 %0, %1, %1, %2;" : "=l"(y[c]) : "r"(w[c]), "l"(0x4330000000000000ll));
+            if (MODE & 1) asm volatile("fma.rn.f64 %0, %1, %2, %3;" : "=d"(x[c]) : "d"(__longlong_as_double(y[c])), "d"(a), "d"(b));
+            else asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(x[c]) : "d"(a), "d"(b));
+            if (MODE & 2) asm volatile("add.rn.f64 %0, %1, %2;" : "=d"(z[c]) : "d"(x[c]), "d"(6755399441055744.0));
+            else asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(z[c]) : "d"(b));
+            if (MODE & 4) asm volatile("add.s32 %0, %0, %1;" : "+r"(w[c]) : "r"(__double2loint(z[c])));
+            else asm volatile("add.s32 %0, %0, %1;" : "+r"(w[c]) : "r"(ia));
+        }
+    }
+    double s = 0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) s += x[c] + z[c] + (double)y[c] + w[c];
+    if (s == 123456789.0) out[threadIdx.x] = s;
+    span_end(sp, t0);
+}
+
 // ---- mixed streams: ALU + FMA-pipe interleaved 1:1 (independent chains) ----
 __global__ void __launch_bounds__(512, 2) k_mixed_alu_fma(int32_t* out, Span* sp, int32_t a, int32_t b)
 {
@@ -171,13 +269,12 @@ __global__ void __launch_bounds__(256, 2) k_eo_dp_step(int32_t* out, Span* sp, D
     int32_t q[SV];
 #pragma unroll
     for (int j = 0; j < SV; ++j) q[j] = 100000 + ((seed + 37 * j + 11 * (int)threadIdx.x) & 4095);
-    const EoDp c = eo_dp_consts(r);
     for (int s = 0; s < SSTEPS; ++s) {
-        const int32_t glast = eo_g_dp(q[SV - 1], c);
+        const int32_t glast = eo_g_dp(q[SV - 1], r);
         int32_t gp = __shfl_up_sync(0xffffffffu, glast, 1);
 #pragma unroll
         for (int j = 0; j + 1 < SV; ++j) {
-            const int32_t gj = eo_g_dp(q[j], c);
+            const int32_t gj = eo_g_dp(q[j], r);
             q[j] = q[j] + gp - gj;
             gp = gj;
         }
@@ -191,24 +288,73 @@ __global__ void __launch_bounds__(256, 2) k_eo_dp_step(int32_t* out, Span* sp, D
     span_end(sp, t0);
 }
 
-// ---- mixed: one cell in MIX takes the float32 + integer form, the rest the float64 form ----
-template <int MIX>
-__global__ void __launch_bounds__(256, 2) k_eo_mix_step(int32_t* out, Span* sp, DevRule r, int32_t seed)
+// ---- the float64 step at other occupancies / with the offset in an ordinary register ----
+template <int MINB, int NV, bool REGOFF>
+__global__ void __launch_bounds__(256, MINB) k_eo_dp_occ(int32_t* out, Span* sp, DevRule r, int32_t seed)
+{
+    unsigned long long t0; __syncthreads(); span_begin(t0);
+    const int lane = threadIdx.x & 31;
+    int32_t q[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) q[j] = 100000 + ((seed + 37 * j + 11 * (int)threadIdx.x) & 4095);
+    long long xo = r.eo_xoff;
+    double dinv = r.eo_dinv, dc1 = r.eo_dc1;
+    if (REGOFF) { xo += threadIdx.x >> 20; asm volatile("" : "+l"(xo), "+d"(dinv), "+d"(dc1)); }
+    auto gdp = [&](int32_t x) {
+        const long long X = (long long)x * (long long)x + xo;
+        return __double2loint(__dadd_rn(__fma_rn(__longlong_as_double(X), dinv, dc1), 6755399441055744.0));
+    };
+    for (int s = 0; s < SSTEPS; ++s) {
+        const int32_t glast = gdp(q[NV - 1]);
+        int32_t gp = __shfl_up_sync(0xffffffffu, glast, 1);
+#pragma unroll
+        for (int j = 0; j + 1 < NV; ++j) {
+            const int32_t gj = gdp(q[j]);
+            q[j] = q[j] + gp - gj;
+            gp = gj;
+        }
+        q[NV - 1] = q[NV - 1] + gp - glast;
+        if (lane == 0) q[0] = 100000;
+    }
+    int32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) acc ^= q[j];
+    if (acc == 123456789) out[threadIdx.x] = acc;
+    span_end(sp, t0);
+}
+
+// ---- the float64 step in batches of B cells (producer -> consumer distance B) ----
+template <int B>
+__global__ void __launch_bounds__(256, 2) k_eo_dp_batch(int32_t* out, Span* sp, DevRule r, int32_t seed)
 {
     unsigned long long t0; __syncthreads(); span_begin(t0);
     const int lane = threadIdx.x & 31;
     int32_t q[SV];
 #pragma unroll
     for (int j = 0; j < SV; ++j) q[j] = 100000 + ((seed + 37 * j + 11 * (int)threadIdx.x) & 4095);
-    const EoDp c = eo_dp_consts(r, 0x4B400000u);
     for (int s = 0; s < SSTEPS; ++s) {
-        const int32_t glast = eo_g_dp(q[SV - 1], c);
+        const int32_t glast = eo_g_dp(q[SV - 1], r);
         int32_t gp = __shfl_up_sync(0xffffffffu, glast, 1);
 #pragma unroll
-        for (int j = 0; j + 1 < SV; ++j) {
-            const int32_t gj = (j % MIX) == 0 ? eo_g_biased_f32<R_EO_P1>(q[j], r) : eo_g_dp(q[j], c);
-            q[j] = q[j] + gp - gj;
-            gp = gj;
+        for (int j0 = 0; j0 + 1 < SV; j0 += B) {
+            double X[B], t[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b)
+                if (j0 + b + 1 < SV)
+                    X[b] = __longlong_as_double((long long)q[j0 + b] * (long long)q[j0 + b] + r.eo_xoff);
+#pragma unroll
+            for (int b = 0; b < B; ++b)
+                if (j0 + b + 1 < SV) t[b] = __fma_rn(X[b], r.eo_dinv, r.eo_dc1);
+#pragma unroll
+            for (int b = 0; b < B; ++b)
+                if (j0 + b + 1 < SV) t[b] = __dadd_rn(t[b], 6755399441055744.0);
+#pragma unroll
+            for (int b = 0; b < B; ++b)
+                if (j0 + b + 1 < SV) {
+                    const int32_t gj = __double2loint(t[b]);
+                    q[j0 + b] = q[j0 + b] + gp - gj;
+                    gp = gj;
+                }
         }
         q[SV - 1] = q[SV - 1] + gp - glast;
         if (lane == 0) q[0] = 100000;
@@ -342,6 +488,20 @@ int main(int argc, char** argv)
     measure("dadd", "DADD", 2, 512, n1, L1(k_dadd, double, 1.5, 0.5));
     measure("dfma_dadd", "DFMA + DADD interleaved (per op)", 2, 512, 2 * n1, L1(k_dfma_dadd, double, 1.0000001, 0.5));
     measure("imad_wide", "IMAD.WIDE", 2, 512, n1, L1(k_imad_wide, long long, 3, 5));
+    measure("imadwide_dfma", "IMAD.WIDE + DFMA interleaved (per op)", 2, 512, 2 * n1, L1(k_imadwide_dfma, double, 1.0000001, 0.5));
+    measure("imadwide_imad", "IMAD.WIDE + IMAD interleaved (per op)", 2, 512, 2 * n1, L1(k_imadwide_imad, int32_t, a, b));
+#define GRP(M, N, NAME, WHAT) measure(NAME, WHAT " (per op)", 2, 512, N * n1, \
+        [&](int g, int t) { k_group<M><<<g, t>>>((double*)out, sp, 1.0000001, 0.5); })
+    GRP(7, 3, "grp_dfma_dadd_imadwide", "DFMA + DADD + IMAD.WIDE");
+    GRP(11, 3, "grp_dfma_dadd_iadd", "DFMA + DADD + IADD");
+    GRP(15, 4, "grp_dfma_dadd_imadwide_iadd", "DFMA + DADD + IMAD.WIDE + IADD");
+    GRP(19, 3, "grp_dfma_dadd_imad", "DFMA + DADD + IMAD");
+    GRP(9, 2, "grp_dfma_iadd", "DFMA + IADD");
+    GRP(13, 3, "grp_dfma_imadwide_iadd", "DFMA + IMAD.WIDE + IADD");
+#define DEP(M, NAME) measure(NAME, "IMAD.WIDE, DFMA, DADD, IADD with dependences (mode bits) (per op)", 2, 512, 4 * n1, \
+        [&](int g, int t) { k_dep<M><<<g, t>>>((double*)out, sp, 1.0000001, 0.5); })
+    DEP(0, "dep0_none"); DEP(1, "dep1_wide_to_dfma"); DEP(2, "dep2_dfma_to_dadd"); DEP(4, "dep4_dadd_to_iadd");
+    DEP(3, "dep3"); DEP(6, "dep6"); DEP(7, "dep7_all");
     measure("i2fp_shf", "I2FP + SHF pairs (per op)", 2, 512, 2 * n1, L1(k_i2fp, int32_t, 0, 0));
     measure("lea_hi", "LEA.HI + LOP3 pairs (per op)", 2, 512, 2 * n1, L1(k_lea_hi, int32_t, a, b));
     measure("mixed_alu_fma_int", "LOP3 + IMAD interleaved", 2, 512, 2 * n1, L1(k_mixed_alu_fma, int32_t, a, b));
@@ -365,10 +525,13 @@ int main(int argc, char** argv)
     // 4 instructions per cell-update (IMAD.WIDE, DFMA, DADD, IADD3)
     measure("eo_dp_step", "K2 sign-uniform step, float64 map, 4 instr/cell", 2, 256, 4.0 * SSTEPS * SV,
             [&](int g, int t) { k_eo_dp_step<<<g, t>>>((int32_t*)out, sp, r, 17); });
-    // mixes, reported as cells x 4 (comparable with eo_dp_step)
-#define MIXV(M, NAME) measure(NAME, "float64 map with one float32-form cell in M (cells x 4)", 2, 256, \
-        4.0 * SSTEPS * SV, [&](int g, int t) { k_eo_mix_step<M><<<g, t>>>((int32_t*)out, sp, r, 17); })
-    MIXV(2, "eo_mix2"); MIXV(3, "eo_mix3"); MIXV(4, "eo_mix4"); MIXV(6, "eo_mix6"); MIXV(8, "eo_mix8");
+#define DPO(MB, NV, RO, NAME) measure(NAME, "float64 step variants (4 instr/cell)", MB, 256, \
+        4.0 * SSTEPS * NV, [&](int g, int t) { k_eo_dp_occ<MB, NV, RO><<<g, t>>>((int32_t*)out, sp, r, 17); })
+    DPO(2, 32, true, "eo_dp_regoff"); DPO(3, 32, false, "eo_dp_occ3"); DPO(4, 32, false, "eo_dp_occ4");
+    DPO(4, 16, false, "eo_dp_occ4_v16"); DPO(8, 16, false, "eo_dp_occ8_v16"); DPO(1, 32, false, "eo_dp_occ1");
+#define DPB(BB, NAME) measure(NAME, "float64 step in batches of B cells (4 instr/cell)", 2, 256, \
+        4.0 * SSTEPS * SV, [&](int g, int t) { k_eo_dp_batch<BB><<<g, t>>>((int32_t*)out, sp, r, 17); })
+    DPB(4, "eo_dp_batch4"); DPB(8, "eo_dp_batch8"); DPB(16, "eo_dp_batch16"); DPB(31, "eo_dp_batch31");
     // EO variants: reported as lane-ops at 7 per cell, i.e. cells/clk x 7 (comparable)
 #define EOV(C, O, M, NAME) measure(NAME, "EO sign-step variant (7-op-equivalent cells)", M, 256, \
         7.0 * SSTEPS * SV, [&](int g, int t) { k_eo_var<C, O, M><<<g, t>>>((int32_t*)out, sp, r, 17); })
