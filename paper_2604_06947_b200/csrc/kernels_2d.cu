@@ -100,7 +100,7 @@ struct K9Ring {
 // pairs at the strip ends are skipped), guarded scalar stores otherwise
 __device__ __forceinline__ void k9_store(int32_t* row, bool vec, int lane, int xl,
                                          const int32_t (&out)[K9_V], const bool (&st)[K9_V],
-                                         const Step2DArgs& a)
+                                         const Step2DArgs& a, unsigned& gacc)
 {
     if (vec) {
 #pragma unroll
@@ -108,8 +108,8 @@ __device__ __forceinline__ void k9_store(int32_t* row, bool vec, int lane, int x
             const int p = lane * K9_V + 2 * h;
             if (p >= K9_H && p < K9_W - K9_H) {
                 *reinterpret_cast<int2*>(row + xl + 2 * h) = make_int2(out[2 * h], out[2 * h + 1]);
-                md_note(a.guard, out[2 * h], a.glo, a.ghi);
-                md_note(a.guard, out[2 * h + 1], a.glo, a.ghi);
+                md_acc(gacc, out[2 * h], a.glo);
+                md_acc(gacc, out[2 * h + 1], a.glo);
             }
         }
     } else {
@@ -117,7 +117,7 @@ __device__ __forceinline__ void k9_store(int32_t* row, bool vec, int lane, int x
         for (int j = 0; j < K9_V; ++j)
             if (st[j]) {
                 row[xl + j] = out[j];
-                md_note(a.guard, out[j], a.glo, a.ghi);
+                md_acc(gacc, out[j], a.glo);
             }
     }
 }
@@ -207,6 +207,7 @@ template <int RULE, bool SAME>
 __global__ void K9_LB1 k_step2d_s(Step2DArgs a, DevRule rx, DevRule ry)
 {
     if (a.guard && *a.guard) return;                    // state left the range earlier
+    unsigned gacc = 0;                                  // range guard: max (unsigned)(q - lo) seen
     constexpr int V = K9_V;
     const int lane = threadIdx.x & 31;
     const int warp = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
@@ -265,7 +266,7 @@ __global__ void K9_LB1 k_step2d_s(Step2DArgs a, DevRule rx, DevRule ry)
         Nn.eval(rx, ry);
         int32_t out[V];
         update_row<RULE, SAME, false>(Bp, C, Nn, xl, nx, false, false, false, out);
-        k9_store(a.dst + r * nx, vec, lane, xl, out, st, a);
+        k9_store(a.dst + r * nx, vec, lane, xl, out, st, a, gacc);
         sz = sn;
     };
     int r = y0;
@@ -277,6 +278,7 @@ __global__ void K9_LB1 k_step2d_s(Step2DArgs a, DevRule rx, DevRule ry)
     if (r < y1) body(r, P2, P0, P1);
     if (r + 1 < y1) body(r + 1, P0, P1, P2);
     asm volatile("cp.async.wait_all;" ::: "memory");
+    md_flush(a.guard, gacc, a.glo, a.ghi);
 }
 
 // K9 with two steps per launch (temporal blocking k = 2): the warp streams the step-0
@@ -290,6 +292,7 @@ template <int RULE, bool SAME>
 __global__ void K9_LB2 k_step2d_s2(Step2DArgs a, DevRule rx, DevRule ry)
 {
     if (a.guard && *a.guard) return;                    // state left the range earlier
+    unsigned gacc = 0;                                  // range guard: max (unsigned)(q - lo) seen
     constexpr int V = K9_V, L = K9_LOOK;
     const int lane = threadIdx.x & 31;
     const int warp = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
@@ -347,7 +350,7 @@ __global__ void K9_LB2 k_step2d_s2(Step2DArgs a, DevRule rx, DevRule ry)
             if (a.guard && r >= 0 && r < ny) {             // range guard on the step-1 row
 #pragma unroll
                 for (int j = 0; j < V; ++j)
-                    if (ck1[j]) md_note(a.guard, C1.q[j], a.glo, a.ghi);
+                    if (ck1[j]) md_acc(gacc, C1.q[j], a.glo);
             }
             C1.eval(rx, ry);
             if (t >= y0 + 2) {                             // step-2 row t - 2: store
@@ -355,7 +358,7 @@ __global__ void K9_LB2 k_step2d_s2(Step2DArgs a, DevRule rx, DevRule ry)
                 int32_t out[V];
                 if (wall) update_row<RULE, SAME, true>(A1, B1, C1, xl, nx, xwall, r2 == 0, r2 == ny - 1, out);
                 else update_row<RULE, SAME, false>(A1, B1, C1, xl, nx, false, false, false, out);
-                k9_store(a.dst + r2 * nx, vec, lane, xl, out, stc, a);
+                k9_store(a.dst + r2 * nx, vec, lane, xl, out, stc, a, gacc);
             }
         }
     };
@@ -369,6 +372,7 @@ __global__ void K9_LB2 k_step2d_s2(Step2DArgs a, DevRule rx, DevRule ry)
     if (i < niter) body(t0 + i, P1, P2, P0, Q0, Q1, Q2);
     if (i + 1 < niter) body(t0 + i + 1, P2, P0, P1, Q1, Q2, Q0);
     asm volatile("cp.async.wait_all;" ::: "memory");
+    md_flush(a.guard, gacc, a.glo, a.ghi);
 }
 
 template <int RULE>

@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(32 * K8_WARPS, k8_minb<RULE>()) k_step3d(Step3
                                                         DevRule rz)
 {
     if (a.guard && *a.guard) return;                    // state left the range earlier
+    unsigned gacc = 0;                                  // range guard: max (unsigned)(q - lo) seen
     constexpr int V = K8_V;
     // y maps of the plane, per row; double-buffered by plane parity so one barrier per
     // plane suffices (a warp writing buffer b for plane z + 2 has passed the barrier of
@@ -245,13 +246,13 @@ __global__ void __launch_bounds__(32 * K8_WARPS, k8_minb<RULE>()) k_step3d(Step3
                     *reinterpret_cast<int4*>(a.dst + base + xl) =
                         make_int4(out[0], out[1], out[2], out[3]);
 #pragma unroll
-                    for (int j = 0; j < V; ++j) md_note(a.guard, out[j], a.glo, a.ghi);
+                    for (int j = 0; j < V; ++j) md_acc(gacc, out[j], a.glo);
                 } else {
 #pragma unroll
                     for (int j = 0; j < V; ++j)
                         if (xl + j < nx) {
                             a.dst[base + xl + j] = out[j];
-                            md_note(a.guard, out[j], a.glo, a.ghi);
+                            md_acc(gacc, out[j], a.glo);
                         }
                 }
             }
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(32 * K8_WARPS, k8_minb<RULE>()) k_step3d(Step3
     if (z < z1) body(z, Q0, Q1, M2, M0, M1);
     if (z + 1 < z1) body(z + 1, Q1, Q2, M0, M1, M2);
     asm volatile("cp.async.wait_all;" ::: "memory");
+    md_flush(a.guard, gacc, a.glo, a.ghi);
 }
 
 template <int RULE>

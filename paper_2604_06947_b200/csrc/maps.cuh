@@ -333,5 +333,17 @@ __device__ __forceinline__ void md_note(int* guard, int32_t v, int32_t lo, int32
 {
     if (guard && (v < lo || v > hi)) atomicOr(guard, 1);
 }
+// the same guard without a branch per cell: acc = max over cells of (unsigned)(v - lo); the
+// cell is outside [lo, hi] exactly when that exceeds hi - lo (v < lo wraps to a huge value).
+// One add + one max per cell, one test per thread at the end of its chunk (md_flush).
+__device__ __forceinline__ void md_acc(unsigned& acc, int32_t v, int32_t lo)
+{
+    const unsigned d = (unsigned)v - (unsigned)lo;
+    acc = d > acc ? d : acc;
+}
+__device__ __forceinline__ void md_flush(int* guard, unsigned acc, int32_t lo, int32_t hi)
+{
+    if (guard && acc > (unsigned)hi - (unsigned)lo) atomicOr(guard, 1);
+}
 
 }  // namespace fqnm
