@@ -231,6 +231,9 @@ struct fqnm_plan {
     int* pipe_guard_host = nullptr;
     int64_t pipe_guard_n = 0;
     cudaStream_t pipe_h2d = nullptr, pipe_d2h = nullptr;
+    // ensemble e2e pipeline (fqnm_step_host on a batched plan): own streams + one event pair per chunk
+    cudaStream_t ens_h2d = nullptr, ens_d2h = nullptr;
+    cudaEvent_t ens_ev[2 * 16 + 1] = {};
     cudaEvent_t pipe_ev[9] = {};         // [0..2] h2d done, [3..5] compute done, [6..8] d2h done
     // profiling (fqnm_profile_enable)
     bool prof = false;
@@ -969,6 +972,10 @@ extern "C" void fqnm_destroy(fqnm_plan_t* p)
     if (p->d_minmax) cudaFree(p->d_minmax);
     if (p->h_minmax) cudaFreeHost(p->h_minmax);
     if (p->e2e_dev) cudaFree(p->e2e_dev);
+    if (p->ens_h2d) cudaStreamDestroy(p->ens_h2d);
+    if (p->ens_d2h) cudaStreamDestroy(p->ens_d2h);
+    for (cudaEvent_t e : p->ens_ev)
+        if (e) cudaEventDestroy(e);
     if (p->edges) cudaFree(p->edges);
     if (p->flags) cudaFree(p->flags);
     for (int i = 0; i < 2; ++i)
@@ -1806,6 +1813,58 @@ static int step_host_pipelined_impl(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
     return FQNM_OK;
 }
 
+// fqnm_step_host on an ensemble (warp / CTA ensemble kernels, independent problems): the batch
+// is cut into up to 16 chunks of whole problems; chunk c's H2D copy, stepping and D2H copy run
+// on three streams, so the copies of neighbouring chunks overlap the stepping (no halos, no
+// buffer rotation: every chunk has its own region of the device buffer).  Same result as
+// the plain path (the kernels step problems independently).
+static int step_host_ensemble(fqnm_plan_t* p, int32_t* qh, int64_t nsteps)
+{
+    const fqnm_plan_desc& d = p->d;
+    const int64_t n = d.n_local, B = d.batch;
+    const int m = (int)(B < 16 ? B : 16);
+    cudaError_t e = cudaSuccess;
+    if (!p->ens_h2d) {
+        e = cudaStreamCreateWithFlags(&p->ens_h2d, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->ens_d2h, cudaStreamNonBlocking);
+        for (int i = 0; i < 33 && e == cudaSuccess; ++i)
+            e = cudaEventCreateWithFlags(&p->ens_ev[i], cudaEventDisableTiming);
+        if (e != cudaSuccess) return fail(FQNM_ERR_CUDA, "ensemble e2e streams: %s", cudaGetErrorString(e));
+    }
+    int32_t* dev = (int32_t*)p->e2e_dev;
+    const int bm = bmode_of(d);
+    int rc = FQNM_OK;
+    // the caller's stream orders this call after its earlier work: the copies start after it
+    e = cudaEventRecord(p->ens_ev[32], p->st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->ens_h2d, p->ens_ev[32], 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->ens_d2h, p->ens_ev[32], 0);
+    for (int c = 0; c < m && e == cudaSuccess; ++c) {
+        const int64_t b0 = B * c / m, b1 = B * (c + 1) / m;
+        const size_t off = (size_t)b0 * n, cnt = (size_t)(b1 - b0) * n;
+        e = cudaMemcpyAsync(dev + off, qh + off, cnt * 4, cudaMemcpyHostToDevice, p->ens_h2d);
+        if (e == cudaSuccess) e = cudaEventRecord(p->ens_ev[2 * c], p->ens_h2d);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(p->st, p->ens_ev[2 * c], 0);
+        if (e != cudaSuccess) break;
+        if (p->family == 3)
+            e = launch_warp_ensemble(p->rule, p->V, dev + off, b1 - b0, nsteps, bm, p->dr, p->st);
+        else
+            e = launch_cta_ensemble(p->rule, dev + off, n, b1 - b0, nsteps, bm, p->dr, p->st);
+        p->launches++;
+        if (e == cudaSuccess) e = cudaEventRecord(p->ens_ev[2 * c + 1], p->st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(p->ens_d2h, p->ens_ev[2 * c + 1], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(qh + off, dev + off, cnt * 4, cudaMemcpyDeviceToHost, p->ens_d2h);
+    }
+    // drain all three streams before returning, also on failure (no copy into the caller's
+    // buffer may still be in flight)
+    cudaError_t e2 = cudaStreamSynchronize(p->ens_h2d);
+    cudaError_t e3 = cudaStreamSynchronize(p->st);
+    cudaError_t e4 = cudaStreamSynchronize(p->ens_d2h);
+    if (e == cudaSuccess) e = e2 != cudaSuccess ? e2 : (e3 != cudaSuccess ? e3 : e4);
+    if (e != cudaSuccess) rc = fail(FQNM_ERR_CUDA, "ensemble e2e pipeline: %s", cudaGetErrorString(e));
+    return rc;
+}
+
 extern "C" int fqnm_step_host(fqnm_plan_t* p, void* q_host, int64_t nsteps)
 {
     if (!p || !q_host) return fail(FQNM_ERR_ARG, "null argument");
@@ -1820,6 +1879,10 @@ extern "C" int fqnm_step_host(fqnm_plan_t* p, void* q_host, int64_t nsteps)
         if (e != cudaSuccess) return fail(FQNM_ERR_NOMEM, "cudaMalloc e2e: %s", cudaGetErrorString(e));
         p->e2e_bytes = bytes;
     }
+    // ensembles without the (whole-buffer, synchronous) range check: chunked pipeline
+    if (nsteps > 0 && d.nvar == 1 && d.batch >= 4 && (p->family == 3 || p->family == 4) &&
+        !d.check_range && bytes >= ((size_t)1 << 22))
+        return step_host_ensemble(p, (int32_t*)q_host, nsteps);
     CUDA_TRY(cudaMemcpyAsync(p->e2e_dev, q_host, bytes, cudaMemcpyHostToDevice, p->st));
     int rc = fqnm_step(p, p->e2e_dev, nsteps);
     if (rc != FQNM_OK) return rc;

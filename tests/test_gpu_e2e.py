@@ -141,3 +141,20 @@ def test_pipelined_step_host_sign_chunks(F, sign):
     qh = torch.tensor(q0).pin_memory()
     F.fqnm_step_host(plan, qh, 77)
     assert torch.equal(qh, ref.cpu())
+
+
+@pytest.mark.parametrize("n,B", [(1024, 6000), (1000, 5003), (32, 40000)])
+def test_step_host_ensemble_pipeline(F, n, B):
+    """fqnm_step_host on an ensemble plan (warp kernel for n = 32 V, CTA kernel otherwise) runs
+    the chunked copy / step / copy pipeline over whole problems; the result equals the
+    device-resident fqnm_step, twice in a row on the same plan (the events are reused)."""
+    rng = np.random.default_rng(n + B)
+    q0 = rng.integers(-5000, 5000, size=(B, n)).astype(np.int32)
+    plan = F.fqnm_plan_ex(n, 1e-4, 0.5, F.LINEAR, batch=B)
+    assert plan.info()["kernel"] in (3, 4)
+    ref = torch.tensor(q0, device="cuda")
+    qh = torch.tensor(q0).pin_memory()
+    for _ in range(2):
+        F.fqnm_step(plan, ref, 53)
+        F.fqnm_step_host(plan, qh, 53)
+        assert torch.equal(qh, ref.cpu())
