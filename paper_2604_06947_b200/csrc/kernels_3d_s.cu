@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(32 * K10_WARPS) k_step3d_s(Step3DArgs a, DevRu
                                                            DevRule rz)
 {
     if (a.guard && *a.guard) return;                    // state left the range earlier
+    unsigned gacc = 0;                                  // range guard accumulator (md_acc)
     constexpr int V = K10_V, R = K10_R, L = K10_LOOK, S = K10_LOOK + 1;
     constexpr int NR = R + 2;                              // loaded rows per plane
     __shared__ int4 ring[S][K10_WARPS][NR][32];
@@ -214,13 +215,13 @@ __global__ void __launch_bounds__(32 * K10_WARPS) k_step3d_s(Step3DArgs a, DevRu
                     }
 #pragma unroll
                     for (int j = 0; j < V; ++j)
-                        if ((lane > 0 || j >= 2) && (lane < 31 || j < 2)) md_note(a.guard, out[j], a.glo, a.ghi);
+                        if ((lane > 0 || j >= 2) && (lane < 31 || j < 2)) md_acc(gacc, out[j], a.glo);
                 } else {
 #pragma unroll
                     for (int j = 0; j < V; ++j)
                         if (stc[j]) {
                             row[xl + j] = out[j];
-                            md_note(a.guard, out[j], a.glo, a.ghi);
+                            md_acc(gacc, out[j], a.glo);
                         }
                 }
             }
@@ -238,6 +239,7 @@ __global__ void __launch_bounds__(32 * K10_WARPS) k_step3d_s(Step3DArgs a, DevRu
     }
     if (z < z1) body(z, MA, MB);
     asm volatile("cp.async.wait_all;" ::: "memory");
+    md_flush(a.guard, gacc, a.glo, a.ghi);
 }
 
 int64_t step3d_s_zchunk(int64_t nx, int64_t ny, int64_t nz)

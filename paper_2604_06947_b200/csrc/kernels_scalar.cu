@@ -1075,6 +1075,7 @@ template <int RULE, bool SAME, bool WALL>
 __global__ void __launch_bounds__(512) k_step2d(Step2DArgs a, DevRule rx, DevRule ry)
 {
     if (a.guard && *a.guard) return;                    // state left the range earlier
+    unsigned gacc = 0;                                  // range guard accumulator (md_acc)
     extern __shared__ int32_t sm2[];
     constexpr int TX = STEP2D_TX, TY = STEP2D_TY;
     constexpr int NA = (TX + 2 * STEP2D_KMAX + 31) / 32;       // cell columns per thread
@@ -1156,8 +1157,7 @@ __global__ void __launch_bounds__(512) k_step2d(Step2DArgs a, DevRule rx, DevRul
                     // shrinking trapezoid inside the domain; the last step at the store)
                     if (a.guard && s + 1 < K && x > s && x < RX - 1 - s && y > s && y < RY - 1 - s) {
                         const int64_t gi = ox + x, gj = oy + y;
-                        if (gi >= 0 && gi < nx && gj >= 0 && gj < ny)
-                            md_note(a.guard, q[b][c], a.glo, a.ghi);
+                        if (gi >= 0 && gi < nx && gj >= 0 && gj < ny) md_acc(gacc, q[b][c], a.glo);
                     }
                 }
             }
@@ -1174,9 +1174,10 @@ __global__ void __launch_bounds__(512) k_step2d(Step2DArgs a, DevRule rx, DevRul
             const int64_t gi = ox + x, gj = oy + y;
             if (x >= K && x < K + TX && y >= K && y < K + TY && gi < nx && gj < ny) {
                 a.dst[gj * nx + gi] = q[b][c];
-                md_note(a.guard, q[b][c], a.glo, a.ghi);
+                md_acc(gacc, q[b][c], a.glo);
             }
         }
+    md_flush(a.guard, gacc, a.glo, a.ghi);
 }
 
 #if FQNM_PART(2)
