@@ -323,6 +323,59 @@ __global__ void __launch_bounds__(256, MINB) k_eo_dp_occ(int32_t* out, Span* sp,
     span_end(sp, t0);
 }
 
+// ---- float64 step variants of how the FP64 result reaches the integer update:
+// MODE 1: through an IMAD (FMA-heavy pipe) copy; MODE 2: the update itself as two IMADs;
+// MODE 3: differences taken in float64 (DADD of the two magic-biased values), one conversion ----
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) k_eo_dp_route(int32_t* out, Span* sp, DevRule r, int32_t seed)
+{
+    unsigned long long t0; __syncthreads(); span_begin(t0);
+    const int lane = threadIdx.x & 31;
+    int32_t q[SV];
+#pragma unroll
+    for (int j = 0; j < SV; ++j) q[j] = 100000 + ((seed + 37 * j + 11 * (int)threadIdx.x) & 4095);
+    const int one = r.one, mone = r.mone;
+    auto tdp = [&](int32_t x) {
+        const long long X = (long long)x * (long long)x + r.eo_xoff;
+        return __dadd_rn(__fma_rn(__longlong_as_double(X), r.eo_dinv, r.eo_dc1), 6755399441055744.0);
+    };
+    for (int s = 0; s < SSTEPS; ++s) {
+        const double tl = tdp(q[SV - 1]);
+        const int32_t glast = __double2loint(tl);
+        int32_t gp = __shfl_up_sync(0xffffffffu, glast, 1);
+        double tp = __hiloint2double(0x43380000, gp);
+#pragma unroll
+        for (int j = 0; j + 1 < SV; ++j) {
+            const double t = tdp(q[j]);
+            if (MODE == 1) {
+                int32_t gj;
+                asm volatile("mad.lo.s32 %0, %1, %2, 0;" : "=r"(gj) : "r"(__double2loint(t)), "r"(one));
+                q[j] = q[j] + gp - gj;
+                gp = gj;
+            } else if (MODE == 2) {
+                const int32_t gj = __double2loint(t);
+                int32_t u;
+                asm volatile("mad.lo.s32 %0, %1, %2, %3;" : "=r"(u) : "r"(gj), "r"(mone), "r"(q[j]));
+                asm volatile("mad.lo.s32 %0, %1, %2, %3;" : "=r"(q[j]) : "r"(gp), "r"(one), "r"(u));
+                gp = gj;
+            } else {
+                // d = tp - t is exact (both 1.5 2^52 + g); q + d in float64 needs q as double: instead
+                // take the low word of (tp - t) + magic
+                const double d = __dadd_rn(__dadd_rn(tp, -t), 6755399441055744.0);
+                q[j] = q[j] + __double2loint(d);
+                tp = t;
+            }
+        }
+        q[SV - 1] = q[SV - 1] + (MODE == 3 ? __double2loint(tp) : gp) - glast;
+        if (lane == 0) q[0] = 100000;
+    }
+    int32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < SV; ++j) acc ^= q[j];
+    if (acc == 123456789) out[threadIdx.x] = acc;
+    span_end(sp, t0);
+}
+
 // ---- the float64 step in batches of B cells (producer -> consumer distance B) ----
 template <int B>
 __global__ void __launch_bounds__(256, 2) k_eo_dp_batch(int32_t* out, Span* sp, DevRule r, int32_t seed)
@@ -529,6 +582,9 @@ int main(int argc, char** argv)
         4.0 * SSTEPS * NV, [&](int g, int t) { k_eo_dp_occ<MB, NV, RO><<<g, t>>>((int32_t*)out, sp, r, 17); })
     DPO(2, 32, true, "eo_dp_regoff"); DPO(3, 32, false, "eo_dp_occ3"); DPO(4, 32, false, "eo_dp_occ4");
     DPO(4, 16, false, "eo_dp_occ4_v16"); DPO(8, 16, false, "eo_dp_occ8_v16"); DPO(1, 32, false, "eo_dp_occ1");
+#define DPR(M, NI, NAME) measure(NAME, "float64 step, result routing variants (cells x 4)", 2, 256, \
+        4.0 * SSTEPS * SV, [&](int g, int t) { k_eo_dp_route<M><<<g, t>>>((int32_t*)out, sp, r, 17); })
+    DPR(1, 5, "eo_dp_route_imadcopy"); DPR(2, 5, "eo_dp_route_imadupdate"); DPR(3, 6, "eo_dp_route_f64diff");
 #define DPB(BB, NAME) measure(NAME, "float64 step in batches of B cells (4 instr/cell)", 2, 256, \
         4.0 * SSTEPS * SV, [&](int g, int t) { k_eo_dp_batch<BB><<<g, t>>>((int32_t*)out, sp, r, 17); })
     DPB(4, "eo_dp_batch4"); DPB(8, "eo_dp_batch8"); DPB(16, "eo_dp_batch16"); DPB(31, "eo_dp_batch31");
