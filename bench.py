@@ -490,13 +490,17 @@ def run_cfg4(args):
             qh.copy_(q.cpu())
             F.fqnm_step_host(plan, qh, T)              # warm (allocates the e2e pipeline)
             torch.cuda.synchronize()
+            eclk = Clocks(local)
+            eclk.start()
             t0 = time.perf_counter()
             for _ in range(args.steps):
                 F.fqnm_step_host(plan, qh, T)          # synchronous: H2D, T steps, D2H
             e2e_s = time.perf_counter() - t0
+            ec = eclk.stop()
             del qh
             e2e = {"value": N * T * args.steps / e2e_s / 1e9, "unit": UNIT,
-                   "h2d_bytes_per_step": 4 * N, "d2h_bytes_per_step": 4 * N}
+                   "h2d_bytes_per_step": 4 * N, "d2h_bytes_per_step": 4 * N,
+                   "clocks": ec}
         else:
             qh = torch.empty(n_local, dtype=torch.int32, pin_memory=True)
             qh.copy_(owned().cpu())
