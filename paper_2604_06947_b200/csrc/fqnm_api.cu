@@ -1614,6 +1614,9 @@ extern "C" int fqnm_observe(const fqnm_plan_t* p, const void* q, double* u)
                                // measured 2977 vs 3615 GCUPS e2e; K2S on chunk-sized problems
                                // is not faster than the voting K2 either: dual 3539-3593)
 #endif
+#ifndef FQNM_PIPE_LOG2C
+#define FQNM_PIPE_LOG2C 27     // largest chunk of the e2e pipeline: 2^27 cells
+#endif
 static int pipe_setup(fqnm_plan_t* p, int64_t nsteps)
 {
     const int64_t n = p->d.n_local;
@@ -1623,7 +1626,7 @@ static int pipe_setup(fqnm_plan_t* p, int64_t nsteps)
         if (n % mm) break;
         const int64_t c = n / mm;
         if (c % 32) break;
-        if (c <= ((int64_t)1 << 27) && H * 16 <= c) { m = mm; C = c; break; }
+        if (c <= ((int64_t)1 << FQNM_PIPE_LOG2C) && H * 16 <= c) { m = mm; C = c; break; }
     }
     if (!m) return FQNM_ERR_UNSUPPORTED;
     if (p->pipe_child && p->pipe_H == H && p->pipe_C == C) return FQNM_OK;
