@@ -532,6 +532,32 @@ static int build_rule(fqnm_plan_t* p)
         r.tp_den = p->hp.den;
         r.tp_fast = tp_fast;
     }
+    // round(num / den) in float64 (maps.cuh round_div_dp): RHA, den > 0 and |num| < 2^44 on the
+    // admissible range; otherwise the int64 division stays
+    {
+        auto dv_set = [&](int which, int64_t den, i128 num_bound) {
+            r.dv_ok[which] = 0;
+            if (d.rounding != FQNM_ROUND_HALF_AWAY || den <= 0 || num_bound >= ((i128)1 << 44)) return;
+            const long double inv = (1.0L / (long double)den) * (1.0L + std::ldexp(1.0L, -46));
+            double dv = (double)inv;
+            uint64_t bits;
+            std::memcpy(&bits, &dv, sizeof bits);
+            bits &= ~3ull;                               // 1.5 * dv must be exact: 3 (m / 4) < 2^53
+            std::memcpy(&dv, &bits, sizeof bits);
+            r.dv_inv[which] = dv;
+            r.dv_c[which] = -(std::ldexp(dv, 52) + std::ldexp(dv, 51));
+            r.dv_ok[which] = 1;
+        };
+        const bool bounded = p->lo > INT64_MIN / 2 && p->hi < INT64_MAX / 2;
+        const i128 A = bounded ? (i128)std::max(std::llabs((long long)p->lo), std::llabs((long long)p->hi))
+                               : ((i128)1 << 40);
+        auto map_bound = [&](const HostMap& m) {
+            return (i128)(m.c2 < 0 ? -m.c2 : m.c2) * A * A + (i128)(m.c1 < 0 ? -m.c1 : m.c1) * A;
+        };
+        dv_set(0, p->hp.den, map_bound(p->hp));
+        dv_set(1, p->hm.den, map_bound(p->hm));
+        if (tp_kind) dv_set(2, p->hp.den, 2 * map_bound(p->hp));
+    }
     if (p->rule == R_EO_FAST || p->rule == R_EO_P1 || tp_fast) {
         r.eo_ntwoP = (int32_t)(-2 * P);
         r.eo_twoQ = (int32_t)(2 * Q);

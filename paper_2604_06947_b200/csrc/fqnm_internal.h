@@ -55,6 +55,11 @@ struct DevRule {
     int32_t tp_kind;      // 0 = split rule, 5 Godunov, 6 EO2, 7 LF2 (fqnm_flux_kind codes)
     int32_t tp_fast;      // Godunov on the EO fast domain: 1 = EO P = 1 closed form, 2 = general P
     int64_t tp_c2, tp_c1, tp_den;
+    // round(num / den) in float64 (maps.cuh round_div_dp; RHA only, |num| < 2^44 on the range):
+    // index 0: phi+ (denp), 1: phi- (denm), 2: the two-point rule (tp_den)
+    int32_t dv_ok[3];
+    double dv_inv[3];     // (1/den)(1 + 2^-46), last two significand bits 0
+    double dv_c[3];       // -1.5 2^52 * dv_inv (exact)
 };
 
 enum Bmode : int32_t { BM_PERIODIC = 0, BM_TRANSMISSIVE = 1, BM_HALO = 2 };

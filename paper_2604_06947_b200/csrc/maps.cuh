@@ -39,6 +39,20 @@ __device__ __forceinline__ int64_t round_div_i64(int64_t num, int64_t den, int r
     return num < 0 ? -r : r;
 }
 
+// RHA(num / den) in float64 for |num| < 2^44 (planner), instead of a 64-bit division:
+//   X = bits(1.5 2^52) + num is the double 1.5 2^52 + num exactly (|num| < 2^51);
+//   t = fma(X, d, -1.5 2^52 d) = fl(num d), d = (1/den)(1 + 2^-46) with its last two significand
+//       bits cleared so that 1.5 2^52 d is exact; the relative bias b of t, 2^-47 < b < 2^-45, moves
+//       v = num/den away from zero: an exact tie rounds away from zero (RHA), and any other v
+//       is >= 1/(2 den) from a half-integer while |v| b < 2^-45 |num| / den < 1/(2 den);
+//   result = low word of bits(t + 1.5 2^52) (two's complement of rint(t), |result| < 2^31).
+__device__ __forceinline__ int32_t round_div_dp(int64_t num, double dinv, double dc)
+{
+    const double X = __longlong_as_double(num + 0x4338000000000000ll);
+    const double t = __fma_rn(X, dinv, dc);
+    return __double2loint(__dadd_rn(t, 6755399441055744.0));
+}
+
 __device__ __forceinline__ int32_t generic_phi(int32_t q, int64_t c2, int64_t c1, int64_t den,
                                                int32_t supp, int rounding)
 {
@@ -48,6 +62,18 @@ __device__ __forceinline__ int32_t generic_phi(int32_t q, int64_t c2, int64_t c1
     int64_t qq = q;
     int64_t num = c2 * qq * qq + c1 * qq;
     return (int32_t)round_div_i64(num, den, rounding);
+}
+
+// the same with the float64 division where the planner allows it (which: 0 phi+, 1 phi-)
+__device__ __forceinline__ int32_t generic_phi_sel(int32_t q, int64_t c2, int64_t c1, int64_t den,
+                                                   int32_t supp, const DevRule& r, int which)
+{
+    if (!r.dv_ok[which]) return generic_phi(q, c2, c1, den, supp, r.rounding);
+    if (supp == SUPP_NONE) return 0;
+    if (supp == SUPP_POS && q <= 0) return 0;
+    if (supp == SUPP_NEG && q >= 0) return 0;
+    const int64_t qq = q;
+    return round_div_dp(c2 * qq * qq + c1 * qq, r.dv_inv[which], r.dv_c[which]);
 }
 
 __device__ __forceinline__ int32_t imad_hi(int32_t a, int32_t b, int32_t c)
@@ -262,8 +288,8 @@ __device__ __forceinline__ void phi_gm(int32_t q, int32_t& g, int32_t& m, const 
         if (r.lin_minus) { g = -v; m = -v; }
         else { g = v; m = 0; }
     } else {
-        const int32_t p = generic_phi(q, r.c2p, r.c1p, r.denp, r.suppp, r.rounding);
-        m = generic_phi(q, r.c2m, r.c1m, r.denm, r.suppm, r.rounding);
+        const int32_t p = generic_phi_sel(q, r.c2p, r.c1p, r.denp, r.suppp, r, 0);
+        m = generic_phi_sel(q, r.c2m, r.c1m, r.denm, r.suppm, r, 1);
         g = p + m;
     }
 }
@@ -291,6 +317,7 @@ __device__ __forceinline__ int32_t tp_phi(int32_t qL, int32_t qR, const DevRule&
         const int64_t A = a * a, B = b * b;
         num = r.tp_c2 * (r.tp_kind == 5 ? (A > B ? A : B) : A + B);
     }
+    if (r.dv_ok[2]) return round_div_dp(num, r.dv_inv[2], r.dv_c[2]);
     return (int32_t)round_div_i64(num, r.tp_den, r.rounding);
 }
 

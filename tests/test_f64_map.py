@@ -52,3 +52,36 @@ def test_f64_map_exact_ties_round_away():
     d = _dinv(1, 2)
     for q in range(1, 2001, 2):
         assert _g_f64(q, d) == (q * q + 1) // 2
+
+
+def _round_div_f64(num, den):
+    """maps.cuh round_div_dp replayed exactly: d = (1/den)(1 + 2^-46) rounded to binary64 with
+    its last two significand bits cleared (so that 1.5 2^52 d is exact), X = 1.5 2^52 + num,
+    t = fma(X, d, -1.5 2^52 d) (one rounding), result = rint(t)."""
+    import struct
+    d = float(Fraction(1, den) * (1 + Fraction(1, 2 ** 46)))
+    bits = struct.unpack("<Q", struct.pack("<d", d))[0] & ~3
+    d = struct.unpack("<d", struct.pack("<Q", bits))[0]
+    c = -(d * 2.0 ** 52 + d * 2.0 ** 51)
+    assert Fraction(c) == -Fraction(d) * 3 * 2 ** 51            # the constant is exact
+    X = float(Fraction(3 * 2 ** 51) + num)
+    assert Fraction(X) == Fraction(3 * 2 ** 51) + num           # and so is the conversion
+    return int(np.rint(float(Fraction(X) * Fraction(d) + Fraction(c))))
+
+
+@pytest.mark.parametrize("den", [1, 2, 3, 9, 18, 750000, 1724240, (1 << 31) - 1, 10 ** 9 + 7, (1 << 40) + 15])
+def test_f64_rounded_division_equals_rha(den):
+    """RHA(num / den) for |num| < 2^44, both signs, exact ties and their neighbours."""
+    rng = np.random.default_rng(den % 997)
+
+    def ref(num):
+        r = (2 * abs(num) + den) // (2 * den)
+        return -r if num < 0 else r
+
+    nums = [int(x) for x in rng.integers(-(1 << 44) + 1, 1 << 44, 3000)]
+    for k in range(-60, 60):
+        for dn in (-1, 0, 1):
+            nums.append((2 * k + 1) * den // 2 + dn)
+    nums += [0, 1, -1, (1 << 44) - 1, -(1 << 44) + 1]
+    bad = [(x, _round_div_f64(x, den), ref(x)) for x in nums if abs(x) < (1 << 44) and _round_div_f64(x, den) != ref(x)]
+    assert not bad, bad[:5]
